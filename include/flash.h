@@ -1,0 +1,145 @@
+/*
+ * flash.h — C ABI of libflash.so, the B200 (sm_100a) hot path of FLASH
+ * (Wang, Shrivastava, Wang, Ryu, SIGMOD'18, arXiv 1709.01190).
+ *
+ * Citations: P:n = PAPER.md line n; DESIGN.md §2 (HASHSPEC) gives the exact integer
+ * definitions; R#n = DESIGN.md readings ledger.
+ *
+ * Conventions (all calls):
+ *   - Pointers are DEVICE pointers unless a function says "host".  The caller owns
+ *     every input and output buffer; the library never frees them.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *     Every call is stream-ordered and returns after enqueueing; results are valid
+ *     once the stream reaches that point.  No call synchronizes the host unless it
+ *     says so.
+ *   - CSR input: row r's column indices are col_idx[row_ptr[r] .. row_ptr[r+1])
+ *     (absolute indexing into col_idx, so a row slice of a larger CSR can be passed
+ *     with the same col_idx).  Rows are sets: order and duplicates do not matter.
+ *     Column indices must be < 0xFFFFFFFF.  An empty row hashes to all-EMPTY codes and
+ *     EMPTY addresses, is never inserted, and a query on it returns k pads (R#15).
+ *   - Ids are uint32, unique across inserts (caller contract, as SPEC S:213) and
+ *     < 0xFFFFFFFF.
+ *   - Errors: argument errors are detected on the host before anything is enqueued
+ *     and leave the index unchanged (FLASH_EINVAL).  CUDA errors surface as
+ *     FLASH_ECUDA from the call that observes them.  flash_last_error() returns a
+ *     thread-local message for the last non-OK status.  No C++ exception crosses
+ *     the ABI.
+ *   - Thread safety: one handle must not be used concurrently from several host
+ *     threads; distinct handles are independent.
+ */
+#ifndef FLASH_H_
+#define FLASH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLASH_EMPTY 0xFFFFFFFFu /* empty code / no address / output pad id */
+
+/* Limits checked by flash_create (FLASH_EINVAL otherwise). */
+#define FLASH_MAX_BINS 8192u    /* K*L */
+#define FLASH_MAX_R 4096u
+#define FLASH_MAX_TOPK 1024u
+
+typedef struct flash_index flash_index; /* opaque; owned by the library */
+
+typedef enum {
+    FLASH_OK = 0,
+    FLASH_EINVAL = 1, /* bad argument; nothing enqueued */
+    FLASH_ENOMEM = 2, /* device allocation failed */
+    FLASH_ECUDA = 3,  /* CUDA runtime error (message in flash_last_error) */
+    FLASH_ENCCL = 4,  /* reserved for the distributed exchange */
+    FLASH_ESTATE = 5  /* call not valid in the handle's state */
+} flash_status;
+
+/* Create an empty index: L hash tables of `range` buckets, each bucket a reservoir of
+ * at most R ids; every table key is a K-tuple of DOPH hashes (§2.2,
+ * P:185-195 §3.2).  seed: the single 64-bit seed all hash keys derive from (R#2).
+ * Requires 1 <= K, 1 <= L, K*L <= FLASH_MAX_BINS, 1 <= R <= FLASH_MAX_R,
+ * 1 <= range <= 2^31, and a CUDA device (the current device at create time is
+ * the handle's device).  Allocates O(L*range) device memory. */
+flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed,
+                          flash_index **out);
+
+/* Free the tables and the handle (synchronizes the device first).  NULL is a no-op. */
+void flash_destroy(flash_index *h);
+
+/* DOPH of n_rows CSR rows (H1-H3; §2.3, Alg. 2 lines 3-5 P:213-215).
+ * codes: [n_rows][K*L] uint32, table t owns [t*K, (t+1)*K) — or NULL.
+ * addrs: [n_rows][L] uint32 bucket addresses in [0, range) or FLASH_EMPTY — or NULL.
+ * At least one of codes / addrs must be non-NULL. */
+flash_status flash_hash(const flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                        uint64_t n_rows, uint32_t *codes, uint32_t *addrs, void *stream);
+
+/* Adding phase (Alg. 2): hash n_rows rows and insert ids id_base + r into
+ * every table's addressed bucket under the bottom-R rule (R#7): each bucket keeps the
+ * min(arrivals, R) ids with smallest (prio(t,b,id), id), ascending by id.  Inserting in
+ * several batches gives the same tables as one batch (bottom-R is composable). */
+flash_status flash_insert(flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                          uint64_t n_rows, uint32_t id_base, void *stream);
+
+/* Same as flash_insert with precomputed addresses addrs [n_rows][L] (e.g. gathered from
+ * other ranks).  Entries >= range other than FLASH_EMPTY are invalid: they are skipped
+ * and counted in the handle's device error counter (flash_check). */
+flash_status flash_insert_addrs(flash_index *h, const uint32_t *addrs, uint64_t n_rows,
+                                uint32_t id_base, void *stream);
+
+/* Querying phase (Alg. 3) for n_q CSR query rows: aggregate the L addressed
+ * buckets, count each candidate's multiplicity (full count, R#11), drop exclude[q] (if
+ * exclude != NULL, R#14), order by (count desc, id asc) (R#12), keep k, pad with
+ * (FLASH_EMPTY, 0) (R#13).  out_ids / out_counts: [n_q][k] uint32.  1 <= k <= FLASH_MAX_TOPK. */
+flash_status flash_query_topk(const flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                              uint64_t n_q, uint32_t k, const uint32_t *exclude, uint32_t *out_ids,
+                              uint32_t *out_counts, void *stream);
+
+/* Same as flash_query_topk with precomputed query addresses addrs [n_q][L]. */
+flash_status flash_query_addrs(const flash_index *h, const uint32_t *addrs, uint64_t n_q, uint32_t k,
+                               const uint32_t *exclude, uint32_t *out_ids, uint32_t *out_counts,
+                               void *stream);
+
+/* Approximate k-NN graph from scratch: insert rows as ids 0..n_rows-1, then
+ * query every row with its own addresses, excluding itself.  Requires a fresh handle
+ * (nothing inserted yet), else FLASH_ESTATE.  out_ids / out_counts: [n_rows][k]. */
+flash_status flash_knn_graph(flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                             uint64_t n_rows, uint32_t k, uint32_t *out_ids, uint32_t *out_counts,
+                             void *stream);
+
+/* flash_knn_graph on HOST buffers (row_ptr [n_rows+1], col_idx [row_ptr[n_rows]],
+ * out_ids / out_counts [n_rows][k], all host; pinned memory is fastest): copies the CSR
+ * to the device (chunked, overlapped with hashing), runs the graph, copies the results
+ * back, and synchronizes `stream` before returning. */
+flash_status flash_knn_graph_host(flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                                  uint64_t n_rows, uint32_t k, uint32_t *out_ids, uint32_t *out_counts,
+                                  void *stream);
+
+/* Device pointers to table t: off [range+1] (bucket b holds ids[off[b]..off[b+1])),
+ * ids [*n_ids] (ascending within each bucket), arrivals [range] (ReservoirCounter).
+ * Synchronizes the handle's last stream.  Pointers stay valid until the next insert or
+ * destroy.  Before any insert: FLASH_ESTATE. */
+flash_status flash_get_table(const flash_index *h, uint32_t t, const uint32_t **off,
+                             const uint32_t **ids, const uint32_t **arrivals, uint64_t *n_ids);
+
+/* Synchronize the handle's last stream and report the device-side error counter
+ * (invalid addresses seen by flash_insert_addrs / flash_query_addrs) in *n_errors (host). */
+flash_status flash_check(const flash_index *h, uint64_t *n_errors);
+
+/* Profiling: when enabled, every call records CUDA events around its phases on the
+ * caller's stream.  flash_phase_ms (host out, synchronizes) returns the accumulated
+ * milliseconds of phase i: 0 = hash (H1-H3), 1 = build (B1-B2), 2 = query (Q1-Q3),
+ * 3 = host<->device copies (flash_knn_graph_host), and their launch counts.
+ * flash_launch_count returns the number of kernels this handle has launched. */
+flash_status flash_set_profiling(flash_index *h, int enable);
+flash_status flash_phase_ms(const flash_index *h, double ms_out[4], uint64_t calls_out[4]);
+uint64_t flash_launch_count(const flash_index *h);
+flash_status flash_reset_counters(flash_index *h);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char *flash_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASH_H_ */

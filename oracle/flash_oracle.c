@@ -117,7 +117,6 @@ int oracle_doph(uint32_t K, uint32_t L, uint64_t seed, const int64_t *row_ptr,
     const uint32_t B = K * L;
     oracle_seeds s;
     oracle_derive_seeds(seed, &s);
-    const int64_t base = row_ptr[0];
 #pragma omp parallel
     {
         uint32_t *v = (uint32_t *)malloc(sizeof(uint32_t) * B);
@@ -126,7 +125,7 @@ int oracle_doph(uint32_t K, uint32_t L, uint64_t seed, const int64_t *row_ptr,
             /* H1 — one pass over the nonzeros: bin b holds min pi(c) over the row's
              * indices c whose pi(c) falls in b's range (Eq. 1 restricted to bin b). */
             for (uint32_t i = 0; i < B; ++i) v[i] = ORACLE_EMPTY;
-            for (int64_t e = row_ptr[r] - base; e < row_ptr[r + 1] - base; ++e) {
+            for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) { /* absolute CSR indexing */
                 uint32_t h = oracle_fmix32(((col_idx[e] ^ s.a1) * s.m1) + s.a2); /* pi(c) */
                 uint32_t b = mulhi_range(h, B);                                  /* bin */
                 if (h < v[b]) v[b] = h;
@@ -360,7 +359,7 @@ static void normalize_rows(const int64_t *row_ptr, const uint32_t *col_idx, uint
     int64_t base = row_ptr[0];
     uint64_t nnz = (uint64_t)(row_ptr[n] - base);
     uint32_t *tmp = (uint32_t *)malloc(sizeof(uint32_t) * (nnz + 1));
-    memcpy(tmp, col_idx, sizeof(uint32_t) * nnz);
+    memcpy(tmp, col_idx + base, sizeof(uint32_t) * nnz); /* absolute CSR indexing */
     int64_t *len = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t r = 0; r < (int64_t)n; ++r) {

@@ -1,0 +1,391 @@
+// build.cu — B1-B2: the adding phase (Alg. 2) with deterministic bottom-R
+// reservoirs (north_star; R#7, R#9, R#10), sm_100a.
+//
+// For every bucket (t, b):  S = old kept ids ∪ newly arriving ids,
+//   arrivals[t][b] += #new arrivals                              (ReservoirCounter)
+//   kept(t,b) = the min(|S|, R) members of S with smallest (prio(t,b,id), id), ascending id.
+// Using old KEPT ids instead of all old arrivals is exact: an id outside the bottom-R of
+// a subset can never enter the bottom-R of a superset.  The result does not depend on the
+// order in which ids arrive or on atomic ordering: the pool order written by the
+// scatter is erased by the per-bucket (prio, id) selection and the final id sort.
+//
+// Kernels: k_count (B1 histogram) -> k_pool_sizes -> 2 scans -> k_fill_old / k_fill_new
+// (scatter every member into a bucket-contiguous pool) -> k_select_warp (one warp per
+// bucket: warp-shuffle sort for |S| <= 32, else a priority-threshold filter to ~R+6sqrt(R)
+// survivors then a shared-memory bitonic sort) -> k_select_big (one CTA per leftover
+// bucket: exact radix select on the priority, any size).
+#include <cub/device/device_scan.cuh>
+
+#include "flash_internal.cuh"
+
+namespace flash {
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kSelThreads = 256;
+constexpr uint32_t kWarpCap = 1024;   // per-warp sort buffer (u64 keys)
+constexpr uint32_t kBigCap = 4096;    // CTA path: kept ids sorted in smem (R <= kBigCap)
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) {
+  return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
+}
+
+// Ascending bitonic sort of one u64 key per lane.
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t key) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t other = __shfl_xor_sync(kFull, key, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      key = (lower == up) ? (key < other ? key : other) : (key > other ? key : other);
+    }
+  }
+  return key;
+}
+
+// Ascending bitonic sort of n (power of two) keys in shared memory by one warp.
+template <typename T>
+__device__ void warp_bitonic(T* a, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t k = 2; k <= n; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t p = lane; p < (n >> 1); p += 32) {
+        const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const uint32_t ixj = i + j;
+        const T x = a[i], y = a[ixj];
+        const bool up = (i & k) == 0;
+        if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Same, by a whole CTA.
+template <typename T>
+__device__ void block_bitonic(T* a, uint32_t n) {
+  for (uint32_t k = 2; k <= n; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t p = threadIdx.x; p < (n >> 1); p += blockDim.x) {
+        const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const uint32_t ixj = i + j;
+        const T x = a[i], y = a[ixj];
+        const bool up = (i & k) == 0;
+        if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// B1: per-bucket arrival histogram of the new rows (warp per row, lanes over tables).
+__global__ void k_count(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t range,
+                        uint32_t* __restrict__ cnt, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+    for (uint32_t t = lane; t < L; t += 32) {
+      const uint32_t a = addrs[r * L + t];
+      if (a == kEmpty) continue;
+      if (a >= range) { atomicAdd(err, 1ull); continue; }
+      atomicAdd(&cnt[t * range + a], 1u);
+    }
+  }
+}
+
+__global__ void k_pool_sizes(uint32_t nb, uint32_t R, const uint64_t* __restrict__ goff_old,
+                             uint32_t* __restrict__ cursor, uint32_t* __restrict__ arrivals,
+                             uint64_t* __restrict__ pool_cnt, uint64_t* __restrict__ keep_cnt) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= nb; i += gridDim.x * blockDim.x) {
+    if (i == nb) { pool_cnt[nb] = 0; keep_cnt[nb] = 0; continue; }
+    const uint64_t old = goff_old ? goff_old[i + 1] - goff_old[i] : 0;
+    const uint32_t c = cursor[i];
+    arrivals[i] += c;
+    const uint64_t m = old + c;
+    pool_cnt[i] = m;
+    keep_cnt[i] = m < R ? m : R;
+    cursor[i] = (uint32_t)old;
+  }
+}
+
+__global__ void k_fill_old(uint32_t nb, const uint64_t* __restrict__ goff_old,
+                           const uint32_t* __restrict__ ids_old, const uint64_t* __restrict__ pool_off,
+                           uint32_t* __restrict__ pool) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb; i += nw) {
+    const uint64_t s = goff_old[i], m = goff_old[i + 1] - s, d = pool_off[i];
+    for (uint64_t j = lane; j < m; j += 32) pool[d + j] = ids_old[s + j];
+  }
+}
+
+__global__ void k_fill_new(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t range,
+                           uint32_t id_base, uint32_t* __restrict__ cursor,
+                           const uint64_t* __restrict__ pool_off, uint32_t* __restrict__ pool) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+    for (uint32_t t = lane; t < L; t += 32) {
+      const uint32_t a = addrs[r * L + t];
+      if (a >= range) continue;  // EMPTY or invalid (counted by k_count)
+      const uint32_t i = t * range + a;
+      const uint32_t pos = atomicAdd(&cursor[i], 1u);
+      pool[pool_off[i] + pos] = id_base + (uint32_t)r;
+    }
+  }
+}
+
+__device__ __forceinline__ void push_big(uint32_t i, uint32_t* big_list, uint32_t* big_count) {
+  if ((threadIdx.x & 31) == 0) big_list[atomicAdd(big_count, 1u)] = i;
+}
+
+// B2, common case: one warp per bucket.
+__global__ void __launch_bounds__(kSelThreads)
+k_select_warp(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
+              const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
+              const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
+              uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  extern __shared__ uint64_t sel_smem[];
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t* buf = sel_smem + (size_t)(threadIdx.x >> 5) * kWarpCap;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb; i += nw) {
+    const uint64_t p0 = pool_off[i];
+    const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
+    if (m == 0) continue;
+    const uint32_t keep = m < R ? m : R;
+    uint32_t* out = ids_out + goff[i];
+    const uint32_t t = i / range, b = i - t * range;
+
+    if (m <= 32 && !force_big) {
+      uint32_t id = lane < m ? pool[p0 + lane] : kEmpty;
+      uint64_t key;
+      if (m > R) {  // bottom-R by (prio, id)
+        const uint64_t tb = prio_bucket_key(keys, t, b);
+        key = lane < m ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
+        key = warp_sort32(key);
+        id = (uint32_t)key;
+      }
+      key = lane < keep ? (uint64_t)id : ~0ull;
+      key = warp_sort32(key);  // ascending id
+      if (lane < keep) out[lane] = (uint32_t)key;
+      continue;
+    }
+    if (force_big) { push_big(i, big_list, big_count); continue; }
+
+    if (m <= R) {  // keep every member; sort ids
+      if (m > kWarpCap) { push_big(i, big_list, big_count); continue; }
+      const uint32_t n2 = pow2_ceil(m);
+      for (uint32_t j = lane; j < n2; j += 32) buf[j] = j < m ? (uint64_t)pool[p0 + j] : ~0ull;
+      __syncwarp();
+      warp_bitonic(buf, n2);
+      for (uint32_t j = lane; j < m; j += 32) out[j] = (uint32_t)buf[j];
+      __syncwarp();
+      continue;
+    }
+
+    // m > R: keep every member whose priority is below a threshold that leaves
+    // ~R + 6 sqrt(R) + 16 survivors in expectation; the bottom-R of the survivors is
+    // the bottom-R of the bucket whenever at least R survive (else: exact CTA path).
+    const double expect = (double)R + 6.0 * sqrt((double)R) + 16.0;
+    const uint64_t tau = expect >= (double)m ? (1ull << 32)
+                                             : (uint64_t)ceil(expect / (double)m * 4294967296.0);
+    const uint64_t tb = prio_bucket_key(keys, t, b);
+    uint32_t cnt = 0;
+    for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      bool pass = false;
+      uint64_t key = 0;
+      if (j < m) {
+        const uint32_t id = pool[p0 + j];
+        const uint32_t pr = prio_of(tb, id);
+        pass = (uint64_t)pr < tau;
+        key = ((uint64_t)pr << 32) | id;
+      }
+      const uint32_t ballot = __ballot_sync(kFull, pass);
+      const uint32_t pos = cnt + __popc(ballot & lanemask_lt());
+      if (pass && pos < kWarpCap) buf[pos] = key;
+      cnt += __popc(ballot);
+    }
+    if (cnt < keep || cnt > kWarpCap) {
+      __syncwarp();
+      push_big(i, big_list, big_count);
+      continue;
+    }
+    const uint32_t n2 = pow2_ceil(cnt);
+    for (uint32_t j = cnt + lane; j < n2; j += 32) buf[j] = ~0ull;
+    __syncwarp();
+    warp_bitonic(buf, n2);  // by (prio, id)
+    const uint32_t n3 = pow2_ceil(keep);
+    for (uint32_t j = lane; j < n3; j += 32) buf[j] = j < keep ? (buf[j] & 0xFFFFFFFFull) : ~0ull;
+    __syncwarp();
+    warp_bitonic(buf, n3);  // kept ids ascending
+    for (uint32_t j = lane; j < keep; j += 32) out[j] = (uint32_t)buf[j];
+    __syncwarp();
+  }
+}
+
+// B2, exact path for any bucket size (R <= kBigCap): radix select of the keep-th smallest
+// (prio, id) key, 8 bits at a time, then gather and id-sort.
+__global__ void __launch_bounds__(kSelThreads)
+k_select_big(uint32_t range, uint32_t R, HashKeys keys, const uint64_t* __restrict__ pool_off,
+             const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
+             uint32_t* __restrict__ ids_out, const uint32_t* __restrict__ big_list,
+             const uint32_t* __restrict__ big_count) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t buf[kBigCap];
+  __shared__ uint32_t s_prefix, s_need, s_ties, s_n;
+  const uint32_t nbig = *big_count;
+  for (uint32_t it = blockIdx.x; it < nbig; it += gridDim.x) {
+    const uint32_t i = big_list[it];
+    const uint64_t p0 = pool_off[i];
+    const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
+    const uint32_t keep = m < R ? m : R;
+    uint32_t* out = ids_out + goff[i];
+    const uint32_t t = i / range, b = i - t * range;
+    const uint64_t tb = prio_bucket_key(keys, t, b);
+
+    uint32_t pstar = 0xFFFFFFFFu, theta = 0xFFFFFFFFu;
+    if (m > R) {
+      // pass A: keep-th smallest priority value pstar, and its rank among equal priorities
+      uint32_t prefix = 0, pmask = 0, need = keep, ties = 0;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+          const uint32_t pr = prio_of(tb, pool[p0 + j]);
+          if ((pr & pmask) == prefix) atomicAdd(&hist[(pr >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t cum = 0, d = 0;
+          for (; d < 255; ++d) {
+            if (cum + hist[d] >= need) break;
+            cum += hist[d];
+          }
+          s_need = need - cum;
+          s_prefix = prefix | (d << shift);
+          s_ties = hist[d];
+        }
+        __syncthreads();
+        need = s_need;
+        prefix = s_prefix;
+        ties = s_ties;
+        pmask |= 255u << shift;
+        __syncthreads();
+      }
+      pstar = prefix;
+      if (need < ties) {
+        // pass B: need-th smallest id among priorities equal to pstar
+        uint32_t iprefix = 0, imask = 0;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+          for (uint32_t d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
+          __syncthreads();
+          for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+            const uint32_t id = pool[p0 + j];
+            if (prio_of(tb, id) == pstar && (id & imask) == iprefix)
+              atomicAdd(&hist[(id >> shift) & 255u], 1u);
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            uint32_t cum = 0, d = 0;
+            for (; d < 255; ++d) {
+              if (cum + hist[d] >= need) break;
+              cum += hist[d];
+            }
+            s_need = need - cum;
+            s_prefix = iprefix | (d << shift);
+          }
+          __syncthreads();
+          need = s_need;
+          iprefix = s_prefix;
+          imask |= 255u << shift;
+          __syncthreads();
+        }
+        theta = iprefix;
+      }
+    }
+    // gather the kept ids
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      const uint32_t id = pool[p0 + j];
+      bool k = true;
+      if (m > R) {
+        const uint32_t pr = prio_of(tb, id);
+        k = pr < pstar || (pr == pstar && id <= theta);
+      }
+      if (k) buf[atomicAdd(&s_n, 1u)] = id;
+    }
+    __syncthreads();
+    const uint32_t n2 = pow2_ceil(keep);
+    for (uint32_t j = keep + threadIdx.x; j < n2; j += blockDim.x) buf[j] = 0xFFFFFFFFu;
+    __syncthreads();
+    block_bitonic(buf, n2);
+    for (uint32_t j = threadIdx.x; j < keep; j += blockDim.x) out[j] = buf[j];
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t build_scan_tmp_bytes(uint64_t nb) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                (int64_t)(nb + 1));
+  return bytes;
+}
+
+int launch_build(const BuildArgs& a, cudaStream_t s) {
+  const uint32_t nb = a.L * a.range;
+  int launches = 0;
+  const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < 148ull * 32 ? (a.n + 7) / 8 : 148ull * 32);
+  const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
+  cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
+  cudaMemsetAsync(a.big_count, 0, sizeof(uint32_t), s);
+  if (a.n) {
+    k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.L, a.range, a.cursor, a.err);
+    launches++;
+  }
+  k_pool_sizes<<<nb_blocks, 256, 0, s>>>(nb, a.R, a.goff_old, a.cursor, a.arrivals, a.pool_cnt, a.keep_cnt);
+  launches++;
+  size_t tmp = a.scan_tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.pool_cnt, a.pool_off, (int64_t)nb + 1, s);
+  tmp = a.scan_tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.keep_cnt, a.goff_new, (int64_t)nb + 1, s);
+  launches += 4;  // two kernels per CUB scan
+  if (a.goff_old) {
+    const unsigned wb = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 32 ? ((uint64_t)nb + 7) / 8 : 148ull * 32);
+    k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);
+    launches++;
+  }
+  if (a.n) {
+    k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.L, a.range, a.id_base, a.cursor, a.pool_off, a.pool);
+    launches++;
+  }
+  static bool attr = false;
+  const size_t sel_smem = (size_t)(kSelThreads / 32) * kWarpCap * sizeof(uint64_t);
+  if (!attr) {
+    cudaFuncSetAttribute(k_select_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
+    attr = true;
+  }
+  const int force_big = getenv("FLASH_DEBUG_FORCE_BIG") ? 1 : 0;
+  const unsigned sel_blocks = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 24 ? ((uint64_t)nb + 7) / 8 : 148ull * 24);
+  k_select_warp<<<sel_blocks, kSelThreads, sel_smem, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off,
+                                                          a.pool, a.goff_new, a.ids_new, a.big_list,
+                                                          a.big_count);
+  k_select_big<<<148 * 2, kSelThreads, 0, s>>>(a.range, a.R, a.keys, a.pool_off, a.pool, a.goff_new,
+                                              a.ids_new, a.big_list, a.big_count);
+  launches += 2;
+  return launches;
+}
+
+}  // namespace flash

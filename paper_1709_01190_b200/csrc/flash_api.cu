@@ -1,0 +1,563 @@
+// flash_api.cu — the C ABI of libflash.so (include/flash.h): handle, validation,
+// stream-ordered scratch, phase orchestration, profiling counters.
+//
+// Every entry point validates on the host before enqueueing anything, enqueues on the
+// caller's stream, and returns without synchronizing (except where flash.h says so).
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "flash.h"
+#include "flash_internal.cuh"
+
+using namespace flash;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+flash_status fail(flash_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      cudaGetLastError();                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? FLASH_ENOMEM : FLASH_ECUDA,        \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    }                                                                                  \
+  } while (0)
+
+struct PendingPhase {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct flash_index {
+  uint32_t K, L, R, range;
+  uint64_t seed;
+  HashKeys keys;
+  int device;
+  uint32_t table_log2;
+  // tables (null before the first insert)
+  uint32_t* arrivals = nullptr;  // [L*range]
+  uint64_t* goff = nullptr;      // [L*range+1]
+  uint32_t* ids = nullptr;       // [kept_ub]
+  uint64_t kept_ub = 0;          // host upper bound on kept ids
+  uint64_t n_inserted = 0;       // rows passed to insert (host count)
+  uint32_t* off_tmp = nullptr;   // [range+1] for flash_get_table
+  unsigned long long* err = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
+  cudaEvent_t order_ev = nullptr;
+  // profiling
+  int profiling = 0;
+  std::vector<PendingPhase> pending;
+  double phase_ms[4] = {0, 0, 0, 0};
+  uint64_t phase_calls[4] = {0, 0, 0, 0};
+  uint64_t launches = 0;
+};
+
+namespace {
+
+// Order this call after everything previously enqueued on the handle.
+flash_status enter(const flash_index* hc, cudaStream_t s) {
+  flash_index* h = const_cast<flash_index*>(hc);
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (h->have_last && h->last_stream != s) {
+    CUDA_TRY(cudaEventRecord(h->order_ev, h->last_stream));
+    CUDA_TRY(cudaStreamWaitEvent(s, h->order_ev, 0));
+  }
+  h->last_stream = s;
+  h->have_last = true;
+  return FLASH_OK;
+}
+
+struct Phase {
+  flash_index* h;
+  int phase;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Phase(const flash_index* hc, int p, cudaStream_t st) : h(const_cast<flash_index*>(hc)), phase(p), s(st) {
+    if (h->profiling) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Phase() {
+    if (a) {
+      cudaEventRecord(b, s);
+      h->pending.push_back({phase, a, b});
+    }
+  }
+};
+
+template <typename T>
+flash_status salloc(T** p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CUDA_TRY(cudaMallocAsync((void**)p, sizeof(T) * count, s));
+  return FLASH_OK;
+}
+
+// True when the GPU can dereference p (device, managed, or mapped host memory).
+bool device_accessible(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ||
+         (at.type == cudaMemoryTypeHost && at.devicePointer != nullptr);
+}
+
+#define REQUIRE_DEV(p)                                                              \
+  do {                                                                              \
+    if (!device_accessible(p)) return fail(FLASH_EINVAL, "%s is not a device pointer", #p); \
+  } while (0)
+
+__global__ void k_table_off(const uint64_t* goff, uint32_t t, uint32_t range, uint32_t* off) {
+  const uint64_t base = goff[(uint64_t)t * range];
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= range; b += gridDim.x * blockDim.x)
+    off[b] = (uint32_t)(goff[(uint64_t)t * range + b] - base);
+}
+
+flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n,
+                     uint32_t* codes, uint32_t* addrs, cudaStream_t s) {
+  Phase ph(h, 0, s);
+  const_cast<flash_index*>(h)->launches +=
+      launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, addrs, s);
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
+flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
+                             cudaStream_t s) {
+  Phase ph(h, 1, s);
+  const uint64_t nb = (uint64_t)h->L * h->range;
+  BuildArgs a;
+  memset(&a, 0, sizeof a);
+  a.addrs = addrs;
+  a.n = n;
+  a.id_base = id_base;
+  a.L = h->L;
+  a.R = h->R;
+  a.range = h->range;
+  a.keys = h->keys;
+  a.goff_old = h->goff;
+  a.ids_old = h->ids;
+  a.arrivals = h->arrivals;
+  a.err = h->err;
+  uint64_t pool_cap = h->kept_ub + n * h->L;
+  uint64_t kept_cap = pool_cap < nb * h->R ? pool_cap : nb * h->R;
+  flash_status st;
+  if ((st = salloc(&a.cursor, nb, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.pool_cnt, nb + 1, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.pool_off, nb + 1, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.keep_cnt, nb + 1, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.goff_new, nb + 1, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.pool, pool_cap, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.ids_new, kept_cap, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.big_list, nb, s)) != FLASH_OK) return st;
+  if ((st = salloc(&a.big_count, 1, s)) != FLASH_OK) return st;
+  a.scan_tmp_bytes = build_scan_tmp_bytes(nb);
+  if ((st = salloc((uint8_t**)&a.scan_tmp, a.scan_tmp_bytes, s)) != FLASH_OK) return st;
+  h->launches += launch_build(a, s);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(a.cursor, s));
+  CUDA_TRY(cudaFreeAsync(a.pool_cnt, s));
+  CUDA_TRY(cudaFreeAsync(a.pool_off, s));
+  CUDA_TRY(cudaFreeAsync(a.keep_cnt, s));
+  CUDA_TRY(cudaFreeAsync(a.pool, s));
+  CUDA_TRY(cudaFreeAsync(a.big_list, s));
+  CUDA_TRY(cudaFreeAsync(a.big_count, s));
+  CUDA_TRY(cudaFreeAsync(a.scan_tmp, s));
+  if (h->goff) CUDA_TRY(cudaFreeAsync(h->goff, s));
+  if (h->ids) CUDA_TRY(cudaFreeAsync(h->ids, s));
+  h->goff = a.goff_new;
+  h->ids = a.ids_new;
+  h->kept_ub = kept_cap;
+  h->n_inserted += n;
+  return FLASH_OK;
+}
+
+flash_status do_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_t nq, uint32_t k,
+                            const uint32_t* exclude, int exclude_self, uint32_t self_base,
+                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s) {
+  Phase ph(h, 2, s);
+  if (!h->goff) {  // nothing inserted: every query returns k pads
+    CUDA_TRY(cudaMemsetAsync(out_ids, 0xFF, sizeof(uint32_t) * nq * k, s));
+    CUDA_TRY(cudaMemsetAsync(out_counts, 0, sizeof(uint32_t) * nq * k, s));
+    return FLASH_OK;
+  }
+  QueryArgs a;
+  a.addrs = addrs;
+  a.nq = nq;
+  a.goff = h->goff;
+  a.ids = h->ids;
+  a.L = h->L;
+  a.range = h->range;
+  a.k = k;
+  a.exclude = exclude;
+  a.exclude_self = exclude_self;
+  a.self_base = self_base;
+  a.out_ids = out_ids;
+  a.out_counts = out_counts;
+  a.err = h->err;
+  a.table_log2 = h->table_log2;
+  const_cast<flash_index*>(h)->launches += launch_query(a, s);
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
+flash_status check_query_shape(const flash_index* h, uint32_t k) {
+  if (k == 0 || k > FLASH_MAX_TOPK) return fail(FLASH_EINVAL, "k=%u outside [1, %u]", k, FLASH_MAX_TOPK);
+  const size_t smem = query_smem_bytes(h->table_log2, k) + 4 * ((h->L + 1) > 256 ? h->L + 1 : 256);
+  if (smem > 227 * 1024)
+    return fail(FLASH_EINVAL, "L*R=%llu too large for the shared-memory count table (current limit L*R <= 8192)",
+                (unsigned long long)h->L * h->R);
+  return FLASH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* flash_last_error(void) { return g_last_error.c_str(); }
+
+flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed,
+                          flash_index** out) {
+  if (!out) return fail(FLASH_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (K < 1 || L < 1 || (uint64_t)K * L > FLASH_MAX_BINS)
+    return fail(FLASH_EINVAL, "need 1 <= K, 1 <= L, K*L <= %u (K=%u L=%u)", FLASH_MAX_BINS, K, L);
+  if (R < 1 || R > FLASH_MAX_R) return fail(FLASH_EINVAL, "R=%u outside [1, %u]", R, FLASH_MAX_R);
+  if (range < 1 || range > (1u << 31)) return fail(FLASH_EINVAL, "range=%u outside [1, 2^31]", range);
+  if ((uint64_t)L * range > (1ull << 31)) return fail(FLASH_EINVAL, "L*range must be <= 2^31");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  flash_index* h = new (std::nothrow) flash_index();
+  if (!h) return fail(FLASH_ENOMEM, "host allocation failed");
+  h->K = K;
+  h->L = L;
+  h->R = R;
+  h->range = range;
+  h->seed = seed;
+  h->keys = derive_keys(seed);
+  h->device = dev;
+  h->table_log2 = query_table_log2(L, R);
+  cudaError_t e = cudaMalloc(&h->arrivals, sizeof(uint32_t) * (size_t)L * range);
+  if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * (size_t)L * range);
+  if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&h->off_tmp, sizeof(uint32_t) * ((size_t)range + 1));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed scratch cached across calls
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    flash_destroy(h);
+    return fail(e == cudaErrorMemoryAllocation ? FLASH_ENOMEM : FLASH_ECUDA, "flash_create: %s",
+                cudaGetErrorString(e));
+  }
+  *out = h;
+  return FLASH_OK;
+}
+
+void flash_destroy(flash_index* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& p : h->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  cudaFree(h->arrivals);
+  cudaFree(h->goff);
+  cudaFree(h->ids);
+  cudaFree(h->err);
+  cudaFree(h->off_tmp);
+  if (h->order_ev) cudaEventDestroy(h->order_ev);
+  delete h;
+}
+
+flash_status flash_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
+                        uint32_t* codes, uint32_t* addrs, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (!codes && !addrs) return fail(FLASH_EINVAL, "codes and addrs are both NULL");
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(row_ptr);
+  REQUIRE_DEV(col_idx);
+  if (codes) REQUIRE_DEV(codes);
+  if (addrs) REQUIRE_DEV(addrs);
+  cudaStream_t s = (cudaStream_t)stream;
+  flash_status st = enter(h, s);
+  if (st != FLASH_OK) return st;
+  return do_hash(h, row_ptr, col_idx, n_rows, codes, addrs, s);
+}
+
+flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
+                                void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(addrs);
+  if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
+    return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
+  cudaStream_t s = (cudaStream_t)stream;
+  flash_status st = enter(h, s);
+  if (st != FLASH_OK) return st;
+  return do_insert_addrs(h, addrs, n_rows, id_base, s);
+}
+
+flash_status flash_insert(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
+                          uint32_t id_base, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(row_ptr);
+  REQUIRE_DEV(col_idx);
+  if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
+    return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
+  cudaStream_t s = (cudaStream_t)stream;
+  flash_status st = enter(h, s);
+  if (st != FLASH_OK) return st;
+  uint32_t* addrs = nullptr;
+  if ((st = salloc(&addrs, n_rows * h->L, s)) != FLASH_OK) return st;
+  if ((st = do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s)) != FLASH_OK) return st;
+  if ((st = do_insert_addrs(h, addrs, n_rows, id_base, s)) != FLASH_OK) return st;
+  CUDA_TRY(cudaFreeAsync(addrs, s));
+  return FLASH_OK;
+}
+
+flash_status flash_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_t n_q, uint32_t k,
+                               const uint32_t* exclude, uint32_t* out_ids, uint32_t* out_counts, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_status st = check_query_shape(h, k);
+  if (st != FLASH_OK) return st;
+  if (n_q == 0) return FLASH_OK;
+  REQUIRE_DEV(addrs);
+  REQUIRE_DEV(out_ids);
+  REQUIRE_DEV(out_counts);
+  if (exclude) REQUIRE_DEV(exclude);
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = enter(h, s)) != FLASH_OK) return st;
+  return do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s);
+}
+
+flash_status flash_query_topk(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,
+                              uint64_t n_q, uint32_t k, const uint32_t* exclude, uint32_t* out_ids,
+                              uint32_t* out_counts, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_status st = check_query_shape(h, k);
+  if (st != FLASH_OK) return st;
+  if (n_q == 0) return FLASH_OK;
+  REQUIRE_DEV(row_ptr);
+  REQUIRE_DEV(col_idx);
+  REQUIRE_DEV(out_ids);
+  REQUIRE_DEV(out_counts);
+  if (exclude) REQUIRE_DEV(exclude);
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = enter(h, s)) != FLASH_OK) return st;
+  uint32_t* addrs = nullptr;
+  if ((st = salloc(&addrs, n_q * h->L, s)) != FLASH_OK) return st;
+  if ((st = do_hash(h, row_ptr, col_idx, n_q, nullptr, addrs, s)) != FLASH_OK) return st;
+  if ((st = do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s)) != FLASH_OK) return st;
+  CUDA_TRY(cudaFreeAsync(addrs, s));
+  return FLASH_OK;
+}
+
+flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
+                             uint32_t k, uint32_t* out_ids, uint32_t* out_counts, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->goff || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph needs a fresh handle");
+  flash_status st = check_query_shape(h, k);
+  if (st != FLASH_OK) return st;
+  if (n_rows == 0) return FLASH_OK;
+  if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
+  REQUIRE_DEV(row_ptr);
+  REQUIRE_DEV(col_idx);
+  REQUIRE_DEV(out_ids);
+  REQUIRE_DEV(out_counts);
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = enter(h, s)) != FLASH_OK) return st;
+  uint32_t* addrs = nullptr;
+  if ((st = salloc(&addrs, n_rows * h->L, s)) != FLASH_OK) return st;
+  if ((st = do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s)) != FLASH_OK) return st;
+  if ((st = do_insert_addrs(h, addrs, n_rows, 0, s)) != FLASH_OK) return st;
+  if ((st = do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s)) != FLASH_OK) return st;
+  CUDA_TRY(cudaFreeAsync(addrs, s));
+  return FLASH_OK;
+}
+
+flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,
+                                  uint64_t n_rows, uint32_t k, uint32_t* out_ids, uint32_t* out_counts,
+                                  void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->goff || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph_host needs a fresh handle");
+  flash_status st = check_query_shape(h, k);
+  if (st != FLASH_OK) return st;
+  if (n_rows == 0) return FLASH_OK;
+  if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
+  if (!row_ptr || !col_idx || !out_ids || !out_counts) return fail(FLASH_EINVAL, "NULL buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = enter(h, s)) != FLASH_OK) return st;
+  const int64_t nnz_begin = row_ptr[0], nnz_end = row_ptr[n_rows];
+  const uint64_t nnz = (uint64_t)(nnz_end - nnz_begin);
+  int64_t* d_rp = nullptr;
+  uint32_t *d_col = nullptr, *d_addrs = nullptr, *d_ids = nullptr, *d_cnt = nullptr;
+  cudaStream_t cs = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  if ((st = salloc(&d_rp, n_rows + 1, s)) != FLASH_OK) return st;
+  if ((st = salloc(&d_col, nnz, s)) != FLASH_OK) return st;
+  if ((st = salloc(&d_addrs, n_rows * h->L, s)) != FLASH_OK) return st;
+  if ((st = salloc(&d_ids, n_rows * k, s)) != FLASH_OK) return st;
+  if ((st = salloc(&d_cnt, n_rows * k, s)) != FLASH_OK) return st;
+  {
+    Phase ph(h, 3, s);
+    CUDA_TRY(cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice, s));
+  }
+  // col_idx is indexed from row_ptr[0]: shift the device pointer so absolute offsets work
+  const uint32_t* d_col_abs = d_col - nnz_begin;
+  // chunked H2D on a copy stream, hashing chunk i while chunk i+1 is in flight
+  const uint64_t chunk_bytes = 256ull << 20;
+  std::vector<cudaEvent_t> evs;
+  cudaEvent_t ready;
+  CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ready, s));  // allocations are ordered on s
+  CUDA_TRY(cudaStreamWaitEvent(cs, ready, 0));
+  uint64_t r0 = 0;
+  while (r0 < n_rows) {
+    uint64_t r1 = r0 + 1;
+    // grow the chunk to ~chunk_bytes of col_idx
+    uint64_t lo = r0 + 1, hi = n_rows;
+    while (lo < hi) {
+      uint64_t mid = lo + (hi - lo + 1) / 2;
+      if ((uint64_t)(row_ptr[mid] - row_ptr[r0]) * 4 <= chunk_bytes) lo = mid; else hi = mid - 1;
+    }
+    r1 = lo;
+    const uint64_t e0 = (uint64_t)(row_ptr[r0] - nnz_begin), e1 = (uint64_t)(row_ptr[r1] - nnz_begin);
+    if (e1 > e0)
+      CUDA_TRY(cudaMemcpyAsync(d_col + e0, col_idx + nnz_begin + e0, sizeof(uint32_t) * (e1 - e0),
+                               cudaMemcpyHostToDevice, cs));
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, cs));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
+    evs.push_back(ev);
+    if ((st = do_hash(h, d_rp + r0, d_col_abs, r1 - r0, nullptr, d_addrs + r0 * h->L, s)) != FLASH_OK) return st;
+    r0 = r1;
+  }
+  if ((st = do_insert_addrs(h, d_addrs, n_rows, 0, s)) != FLASH_OK) return st;
+  if ((st = do_query_addrs(h, d_addrs, n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s)) != FLASH_OK) return st;
+  {
+    Phase ph(h, 3, s);
+    CUDA_TRY(cudaMemcpyAsync(out_ids, d_ids, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(out_counts, d_cnt, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(cudaFreeAsync(d_rp, s));
+  CUDA_TRY(cudaFreeAsync(d_col, s));
+  CUDA_TRY(cudaFreeAsync(d_addrs, s));
+  CUDA_TRY(cudaFreeAsync(d_ids, s));
+  CUDA_TRY(cudaFreeAsync(d_cnt, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ready);
+  cudaStreamDestroy(cs);
+  return FLASH_OK;
+}
+
+flash_status flash_get_table(const flash_index* h, uint32_t t, const uint32_t** off, const uint32_t** ids,
+                             const uint32_t** arrivals, uint64_t* n_ids) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (t >= h->L) return fail(FLASH_EINVAL, "table %u >= L=%u", t, h->L);
+  if (!h->goff) return fail(FLASH_ESTATE, "nothing inserted yet");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+  uint64_t b[2];
+  CUDA_TRY(cudaMemcpy(&b[0], h->goff + (uint64_t)t * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&b[1], h->goff + (uint64_t)(t + 1) * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  k_table_off<<<(h->range + 256) / 256 < 4096 ? (h->range + 256) / 256 : 4096, 256>>>(h->goff, t, h->range,
+                                                                                     h->off_tmp);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  const_cast<flash_index*>(h)->launches++;
+  if (off) *off = h->off_tmp;
+  if (ids) *ids = h->ids + b[0];
+  if (arrivals) *arrivals = h->arrivals + (uint64_t)t * h->range;
+  if (n_ids) *n_ids = b[1] - b[0];
+  return FLASH_OK;
+}
+
+flash_status flash_check(const flash_index* h, uint64_t* n_errors) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+  unsigned long long e = 0;
+  CUDA_TRY(cudaMemcpy(&e, h->err, sizeof e, cudaMemcpyDeviceToHost));
+  if (n_errors) *n_errors = e;
+  return FLASH_OK;
+}
+
+flash_status flash_set_profiling(flash_index* h, int enable) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  h->profiling = enable;
+  return FLASH_OK;
+}
+
+flash_status flash_phase_ms(const flash_index* hc, double ms_out[4], uint64_t calls_out[4]) {
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  for (auto& p : h->pending) {
+    CUDA_TRY(cudaEventSynchronize(p.b));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+    h->phase_ms[p.phase] += ms;
+    h->phase_calls[p.phase] += 1;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  h->pending.clear();
+  for (int i = 0; i < 4; ++i) {
+    if (ms_out) ms_out[i] = h->phase_ms[i];
+    if (calls_out) calls_out[i] = h->phase_calls[i];
+  }
+  return FLASH_OK;
+}
+
+uint64_t flash_launch_count(const flash_index* h) { return h ? h->launches : 0; }
+
+flash_status flash_reset_counters(flash_index* h) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  double ms[4];
+  flash_status st = flash_phase_ms(h, ms, nullptr);
+  if (st != FLASH_OK) return st;
+  for (int i = 0; i < 4; ++i) {
+    h->phase_ms[i] = 0;
+    h->phase_calls[i] = 0;
+  }
+  h->launches = 0;
+  return FLASH_OK;
+}
+
+}  // extern "C"

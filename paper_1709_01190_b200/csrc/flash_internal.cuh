@@ -1,0 +1,121 @@
+// flash_internal.cuh — device primitives and kernel launchers of libflash.so (sm_100a).
+//
+// The integer definitions implemented here are DESIGN.md §2 (HASHSPEC); they are
+// written independently of the CPU oracle (oracle/), which shares no code with this
+// directory.  Citations: P:n = PAPER.md line n; R#n = DESIGN.md readings ledger.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "flash.h"
+
+namespace flash {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // R#3
+constexpr uint32_t kProbes = 64;          // densification chain cap T (R#4)
+
+// Per-index hash keys derived from the single seed (R#2).
+struct HashKeys {
+  uint32_t a1, m1, a2, s_dens;  // DOPH's "4 random numbers"
+  uint32_t s_addr;              // K-tuple -> address key (R#5)
+  uint64_t s_prio;              // bottom-R priority key (R#9)
+};
+
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline HashKeys derive_keys(uint64_t seed) {
+  uint64_t w[4];
+  for (int k = 0; k < 4; ++k) w[k] = mix64(seed + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ull);
+  HashKeys s;
+  s.a1 = (uint32_t)w[0];
+  s.m1 = (uint32_t)(w[0] >> 32) | 1u;
+  s.a2 = (uint32_t)w[1];
+  s.s_dens = (uint32_t)(w[1] >> 32);
+  s.s_addr = (uint32_t)w[2];
+  s.s_prio = w[3];
+  return s;
+}
+
+// pi(c): keyed bijection on uint32 standing in for the random permutation of Eq. 1.
+__device__ __forceinline__ uint32_t perm(const HashKeys& k, uint32_t c) {
+  return fmix32(((c ^ k.a1) * k.m1) + k.a2);
+}
+
+// prio(t, b, id) = hi32(mix64(tb ^ id)) with tb = mix64(s_prio ^ (t<<32 | b)).
+__device__ __forceinline__ uint64_t prio_bucket_key(const HashKeys& k, uint32_t t, uint32_t b) {
+  return mix64(k.s_prio ^ (((uint64_t)t << 32) | (uint64_t)b));
+}
+__device__ __forceinline__ uint32_t prio_of(uint64_t tb, uint32_t id) {
+  return (uint32_t)(mix64(tb ^ (uint64_t)id) >> 32);
+}
+
+// ---------------------------------------------------------------------------
+// Launchers (each returns the number of kernels it launched).
+// ---------------------------------------------------------------------------
+
+// H1-H3: DOPH bin minima, densification, addresses.  codes / addrs may be null.
+int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
+                uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
+                cudaStream_t s);
+
+// Build scratch / state.  All bucket-indexed arrays have nb = L*range entries (+1).
+struct BuildArgs {
+  const uint32_t* addrs;  // [n][L]
+  uint64_t n;
+  uint32_t id_base;
+  uint32_t L, R, range;
+  HashKeys keys;
+  // old tables (null when empty)
+  const uint64_t* goff_old;  // [nb+1]
+  const uint32_t* ids_old;
+  // outputs / scratch
+  uint32_t* arrivals;         // [nb], accumulated
+  uint32_t* cursor;           // [nb] scratch
+  uint64_t* pool_cnt;         // [nb+1] scratch (becomes pool offsets after scan)
+  uint64_t* pool_off;         // [nb+1]
+  uint64_t* keep_cnt;         // [nb+1]
+  uint64_t* goff_new;         // [nb+1]
+  uint32_t* pool;             // [pool capacity]
+  uint32_t* ids_new;          // [kept capacity]
+  uint32_t* big_list;         // [nb] bucket indices for the CTA path
+  uint32_t* big_count;        // [1]
+  unsigned long long* err;    // device error counter
+  void* scan_tmp;
+  size_t scan_tmp_bytes;
+};
+size_t build_scan_tmp_bytes(uint64_t nb);
+int launch_build(const BuildArgs& a, cudaStream_t s);
+
+struct QueryArgs {
+  const uint32_t* addrs;  // [nq][L]
+  uint64_t nq;
+  const uint64_t* goff;   // [L*range+1]
+  const uint32_t* ids;
+  uint32_t L, range, k;
+  const uint32_t* exclude;  // [nq] or null
+  int exclude_self;         // exclude id = self_base + q
+  uint32_t self_base;
+  uint32_t* out_ids;
+  uint32_t* out_counts;
+  unsigned long long* err;
+  uint32_t table_log2;      // count-table slots = 2^table_log2
+};
+int launch_query(const QueryArgs& a, cudaStream_t s);
+size_t query_smem_bytes(uint32_t table_log2, uint32_t k);
+uint32_t query_table_log2(uint32_t L, uint32_t R);
+
+}  // namespace flash

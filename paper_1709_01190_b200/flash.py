@@ -1,0 +1,302 @@
+"""ctypes binding for libflash.so (include/flash.h) — argument marshalling only.
+
+Every function here has the same name as the C-ABI entry point it wraps and only
+converts torch tensors / numpy arrays to pointers and sizes; all steps of FLASH's
+hot path run in the library's sm_100a kernels.  There is no CPU fallback: if
+``libflash.so`` is missing or no CUDA device is visible, calls raise.
+
+Tensors: CSR ``row_ptr`` int64 [n+1], ``col_idx`` int32 [nnz] (reinterpreted as
+uint32; col ids >= 2^31 are stored as their two's-complement int32 bit pattern),
+addresses / ids / counts int32 [n, L] / [n, k] holding uint32 bit patterns
+(``as_u32`` converts to numpy uint32).  ``stream`` defaults to torch's current
+stream on the tensors' device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflash.so")
+EMPTY = 0xFFFFFFFF
+
+FLASH_OK, FLASH_EINVAL, FLASH_ENOMEM, FLASH_ECUDA, FLASH_ENCCL, FLASH_ESTATE = range(6)
+_NAMES = {1: "FLASH_EINVAL", 2: "FLASH_ENOMEM", 3: "FLASH_ECUDA", 4: "FLASH_ENCCL", 5: "FLASH_ESTATE"}
+
+# Every symbol include/flash.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "flash_create", "flash_destroy", "flash_hash", "flash_insert", "flash_insert_addrs",
+    "flash_query_topk", "flash_query_addrs", "flash_knn_graph", "flash_knn_graph_host",
+    "flash_get_table", "flash_check", "flash_set_profiling", "flash_phase_ms",
+    "flash_launch_count", "flash_reset_counters", "flash_last_error",
+)
+
+
+class FlashError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libflash.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(path)
+    vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    L.flash_create.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(vp)]
+    L.flash_destroy.argtypes = [vp]
+    L.flash_destroy.restype = None
+    L.flash_hash.argtypes = [vp, vp, vp, u64, vp, vp, vp]
+    L.flash_insert.argtypes = [vp, vp, vp, u64, u32, vp]
+    L.flash_insert_addrs.argtypes = [vp, vp, u64, u32, vp]
+    L.flash_query_topk.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, vp]
+    L.flash_query_addrs.argtypes = [vp, vp, u64, u32, vp, vp, vp, vp]
+    L.flash_knn_graph.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
+    L.flash_knn_graph_host.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
+    L.flash_get_table.argtypes = [vp, u32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                  ctypes.POINTER(u64)]
+    L.flash_check.argtypes = [vp, ctypes.POINTER(u64)]
+    L.flash_set_profiling.argtypes = [vp, i32]
+    L.flash_phase_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
+    L.flash_launch_count.argtypes = [vp]
+    L.flash_launch_count.restype = u64
+    L.flash_reset_counters.argtypes = [vp]
+    L.flash_last_error.argtypes = []
+    L.flash_last_error.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        f = getattr(L, name)
+        if name not in ("flash_destroy", "flash_launch_count", "flash_last_error"):
+            f.restype = i32
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != FLASH_OK:
+        raise FlashError(st, load_library().flash_last_error().decode())
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return t.ctypes.data
+    return int(t)
+
+
+def _stream(stream, ref: torch.Tensor | None = None) -> int | None:
+    if stream is None:
+        dev = ref.device if isinstance(ref, torch.Tensor) and ref.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        return torch.cuda.current_stream(dev).cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def as_u32(t) -> np.ndarray:
+    """int32 tensor/array holding uint32 bit patterns -> numpy uint32."""
+    if isinstance(t, torch.Tensor):
+        t = t.detach().cpu().numpy()
+    return np.ascontiguousarray(t).view(np.uint32)
+
+
+def to_device_csr(row_ptr, col_idx, device="cuda"):
+    """numpy CSR (int64, uint32) -> torch CUDA tensors (int64, int32 bit patterns)."""
+    rp = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int64)).to(device)
+    ci_np = np.ascontiguousarray(col_idx, dtype=np.uint32)
+    if ci_np.size == 0:
+        ci_np = np.zeros(1, np.uint32)
+    ci = torch.from_numpy(ci_np.view(np.int32)).to(device)
+    return rp, ci
+
+
+# ---------------------------------------------------------------------------
+# C-ABI wrappers (same names)
+# ---------------------------------------------------------------------------
+
+def flash_create(K: int, L: int, R: int, range_: int, seed: int) -> int:
+    torch.cuda.current_device()  # make sure the CUDA context exists
+    h = ctypes.c_void_p()
+    _check(load_library().flash_create(K, L, R, range_, seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(h)))
+    return h.value
+
+
+def flash_destroy(h: int) -> None:
+    load_library().flash_destroy(h)
+
+
+def flash_hash(h, row_ptr, col_idx, n_rows, codes=None, addrs=None, stream=None):
+    _check(load_library().flash_hash(h, _ptr(row_ptr), _ptr(col_idx), n_rows, _ptr(codes), _ptr(addrs),
+                                     _stream(stream, row_ptr)))
+
+
+def flash_insert(h, row_ptr, col_idx, n_rows, id_base=0, stream=None):
+    _check(load_library().flash_insert(h, _ptr(row_ptr), _ptr(col_idx), n_rows, id_base, _stream(stream, row_ptr)))
+
+
+def flash_insert_addrs(h, addrs, n_rows, id_base=0, stream=None):
+    _check(load_library().flash_insert_addrs(h, _ptr(addrs), n_rows, id_base, _stream(stream, addrs)))
+
+
+def flash_query_topk(h, row_ptr, col_idx, n_q, k, exclude, out_ids, out_counts, stream=None):
+    _check(load_library().flash_query_topk(h, _ptr(row_ptr), _ptr(col_idx), n_q, k, _ptr(exclude),
+                                           _ptr(out_ids), _ptr(out_counts), _stream(stream, row_ptr)))
+
+
+def flash_query_addrs(h, addrs, n_q, k, exclude, out_ids, out_counts, stream=None):
+    _check(load_library().flash_query_addrs(h, _ptr(addrs), n_q, k, _ptr(exclude), _ptr(out_ids),
+                                            _ptr(out_counts), _stream(stream, addrs)))
+
+
+def flash_knn_graph(h, row_ptr, col_idx, n_rows, k, out_ids, out_counts, stream=None):
+    _check(load_library().flash_knn_graph(h, _ptr(row_ptr), _ptr(col_idx), n_rows, k, _ptr(out_ids),
+                                          _ptr(out_counts), _stream(stream, row_ptr)))
+
+
+def flash_knn_graph_host(h, row_ptr, col_idx, n_rows, k, out_ids, out_counts, stream=None):
+    """Host buffers in and out (numpy or pinned CPU tensors); synchronizes."""
+    _check(load_library().flash_knn_graph_host(h, _ptr(row_ptr), _ptr(col_idx), n_rows, k, _ptr(out_ids),
+                                               _ptr(out_counts), _stream(stream)))
+
+
+def flash_get_table(h, t: int):
+    """(off, ids, arrivals) device pointers and n_ids for table t."""
+    off, ids, arr = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    n = ctypes.c_uint64()
+    _check(load_library().flash_get_table(h, t, ctypes.byref(off), ctypes.byref(ids), ctypes.byref(arr),
+                                          ctypes.byref(n)))
+    return off.value, ids.value, arr.value, n.value
+
+
+def flash_check(h) -> int:
+    n = ctypes.c_uint64()
+    _check(load_library().flash_check(h, ctypes.byref(n)))
+    return n.value
+
+
+def flash_set_profiling(h, enable: bool):
+    _check(load_library().flash_set_profiling(h, 1 if enable else 0))
+
+
+def flash_phase_ms(h):
+    ms = (ctypes.c_double * 4)()
+    calls = (ctypes.c_uint64 * 4)()
+    _check(load_library().flash_phase_ms(h, ms, calls))
+    return list(ms), list(calls)
+
+
+def flash_launch_count(h) -> int:
+    return int(load_library().flash_launch_count(h))
+
+
+def flash_reset_counters(h):
+    _check(load_library().flash_reset_counters(h))
+
+
+def flash_last_error() -> str:
+    return load_library().flash_last_error().decode()
+
+
+# ---------------------------------------------------------------------------
+# Convenience object
+# ---------------------------------------------------------------------------
+
+class _DeviceArray:
+    """Zero-copy view of library-owned device memory (CUDA array interface)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, True),
+                                         "version": 2, "strides": None}
+
+
+def _copy_device(ptr: int, n: int, device) -> torch.Tensor:
+    if n == 0:
+        return torch.empty(0, dtype=torch.int32, device=device)
+    return torch.as_tensor(_DeviceArray(ptr, n), device=device).clone()
+
+
+class FlashIndex:
+    """Owns one flash_index handle (device = the current CUDA device)."""
+
+    def __init__(self, K: int, L: int, R: int, range_: int, seed: int):
+        self.K, self.L, self.R, self.range, self.seed = K, L, R, range_, seed
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.h = flash_create(K, L, R, range_, seed)
+
+    def close(self):
+        if getattr(self, "h", None):
+            flash_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def hash(self, row_ptr, col_idx, codes=True, addrs=True):
+        n = row_ptr.numel() - 1
+        c = torch.empty((n, self.K * self.L), dtype=torch.int32, device=self.device) if codes else None
+        a = torch.empty((n, self.L), dtype=torch.int32, device=self.device) if addrs else None
+        flash_hash(self.h, row_ptr, col_idx, n, c, a)
+        return c, a
+
+    def insert(self, row_ptr, col_idx, id_base=0):
+        flash_insert(self.h, row_ptr, col_idx, row_ptr.numel() - 1, id_base)
+
+    def insert_addrs(self, addrs, id_base=0):
+        flash_insert_addrs(self.h, addrs, addrs.shape[0], id_base)
+
+    def query(self, row_ptr, col_idx, k, exclude=None):
+        n = row_ptr.numel() - 1
+        ids = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        cnt = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        flash_query_topk(self.h, row_ptr, col_idx, n, k, exclude, ids, cnt)
+        return ids, cnt
+
+    def query_addrs(self, addrs, k, exclude=None):
+        n = addrs.shape[0]
+        ids = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        cnt = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        flash_query_addrs(self.h, addrs, n, k, exclude, ids, cnt)
+        return ids, cnt
+
+    def knn_graph(self, row_ptr, col_idx, k):
+        n = row_ptr.numel() - 1
+        ids = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        cnt = torch.empty((n, k), dtype=torch.int32, device=self.device)
+        flash_knn_graph(self.h, row_ptr, col_idx, n, k, ids, cnt)
+        return ids, cnt
+
+    def table(self, t: int):
+        """(off, ids, arrivals) of table t as numpy uint32 (synchronizes)."""
+        off_p, ids_p, arr_p, n = flash_get_table(self.h, t)
+        off = _copy_device(off_p, self.range + 1, self.device)
+        ids = _copy_device(ids_p, n, self.device)
+        arr = _copy_device(arr_p, self.range, self.device)
+        return as_u32(off), as_u32(ids), as_u32(arr)
+
+    def errors(self) -> int:
+        return flash_check(self.h)

@@ -1,0 +1,302 @@
+"""Bit-exact parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Integer work end to end, so the bar is bit-exactness (north_star): codes, addresses,
+per-bucket arrivals / offsets / kept ids, top-k ids and counts.  Inputs are seeded
+synthetic CSR (synth/) at sizes the oracle finishes in seconds, spanning many tiles
+and ragged tails, plus the degenerate cases of SURVEY §4's edge matrix.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1709_01190_b200 import flash
+
+pytestmark = pytest.mark.gpu
+EMPTY = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "these tests need a B200"
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.synchronize()
+
+
+def shape_slice(name, n, **kw):
+    s = synth.SHAPES[name].with_(N=n, **kw)
+    return synth.generate(s)
+
+
+def edge_csr():
+    return synth.csr_from_rows(synth.edge_case_rows())
+
+
+def skew_csr(n=3000, seed=5):
+    """Half the rows identical (SURVEY §4 / S:219 heavy bucket), rest tiny-shaped."""
+    rp, col = synth.generate(synth.SHAPES["tiny"].with_(N=n, seed=seed))
+    rows = [col[rp[i]:rp[i + 1]] for i in range(n)]
+    for i in range(0, n, 2):
+        rows[i] = rows[0]
+    return synth.csr_from_rows(rows)
+
+
+HASH_CASES = [
+    ("tiny", lambda: synth.generate("tiny"), 4, 16, 1 << 15),
+    ("edge", edge_csr, 4, 16, 1000),
+    ("edge_KL1", edge_csr, 1, 1, 1 << 15),
+    ("edge_range1", edge_csr, 2, 8, 1),
+    ("webspam_slice", lambda: shape_slice("webspam", 600), 4, 50, 1 << 15),
+    ("webspam_B768", lambda: shape_slice("webspam", 200), 6, 128, 1 << 15),
+    ("url_slice", lambda: shape_slice("url", 4000), 4, 128, 1 << 15),
+    ("kdd12_slice", lambda: shape_slice("kdd12", 20000), 4, 32, 1 << 20),
+    ("wide_K", lambda: shape_slice("url", 500), 64, 2, 12345),
+]
+
+
+@pytest.mark.parametrize("name,make,K,L,rng", HASH_CASES, ids=[c[0] for c in HASH_CASES])
+def test_hash_codes_and_addresses_bit_exact(name, make, K, L, rng):
+    rp, col = make()
+    seed = 0x5EED0000 + K * 131 + L
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, 8, rng, seed) as idx:
+        codes, addrs = idx.hash(d_rp, d_col)
+        o_codes = oracle.doph(K, L, seed, rp, col)
+        o_addrs = oracle.addresses(K, L, rng, seed, o_codes)
+        assert np.array_equal(flash.as_u32(codes), o_codes)
+        assert np.array_equal(flash.as_u32(addrs), o_addrs)
+        # addresses alone (the insert/graph kernel variant)
+        _, a2 = idx.hash(d_rp, d_col, codes=False)
+        assert np.array_equal(flash.as_u32(a2), o_addrs)
+
+
+def test_hash_row_slice_with_absolute_offsets_and_unaligned_col_idx():
+    rp, col = shape_slice("webspam", 300)
+    K, L, rng, seed = 4, 50, 1 << 15, 77
+    o = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, 8, rng, seed) as idx:
+        # rows 100..199 through a row_ptr slice (absolute offsets into the same col_idx)
+        sub = d_rp[100:201].contiguous()
+        a = torch.empty((100, L), dtype=torch.int32, device="cuda")
+        flash.flash_hash(idx.h, sub, d_col, 100, None, a)
+        assert np.array_equal(flash.as_u32(a), o[100:200])
+        # col_idx starting 1 element past a 16-B boundary
+        shifted = torch.empty(d_col.numel() + 1, dtype=torch.int32, device="cuda")
+        shifted[1:] = d_col
+        view = shifted[1:]
+        a = torch.empty((300, L), dtype=torch.int32, device="cuda")
+        flash.flash_hash(idx.h, d_rp, view, 300, None, a)
+        assert np.array_equal(flash.as_u32(a), o)
+
+
+def _check_tables(idx, T):
+    for t in range(idx.L):
+        off, ids, arr = idx.table(t)
+        o_off, o_ids, o_arr = T.table(t)
+        assert np.array_equal(arr, o_arr), f"arrivals t={t}"
+        assert np.array_equal(off, o_off), f"off t={t}"
+        assert np.array_equal(ids, o_ids), f"ids t={t}"
+
+
+BUILD_CASES = [
+    ("tiny", lambda: synth.generate("tiny"), 4, 16, 32, 1 << 15),
+    ("edge", edge_csr, 4, 16, 3, 1000),
+    ("skew_R8_range64", skew_csr, 2, 6, 8, 64),
+    ("skew_R1", skew_csr, 2, 6, 1, 64),
+    ("range1_R128", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 3, 128, 1),
+    ("range1_R2000_big", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 2, 2000, 1),
+    ("range1_R4096_m_le_R", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 2, 4096, 1),
+    ("webspam_slice", lambda: shape_slice("webspam", 1500), 4, 50, 128, 1 << 10),
+    ("url_slice", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 12),
+]
+
+
+@pytest.mark.parametrize("name,make,K,L,R,rng", BUILD_CASES, ids=[c[0] for c in BUILD_CASES])
+def test_tables_bit_exact(name, make, K, L, R, rng):
+    rp, col = make()
+    n = rp.size - 1
+    seed = 0xB0 + R
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    T = oracle.build(L, R, rng, seed, addrs, np.arange(n, dtype=np.uint32))
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert(d_rp, d_col, 0)
+        _check_tables(idx, T)
+        assert idx.errors() == 0
+
+
+def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch):
+    """FLASH_DEBUG_FORCE_BIG routes every bucket with > 32 members through the exact
+    radix-select CTA kernel (normally only reached by rare threshold misses)."""
+    monkeypatch.setenv("FLASH_DEBUG_FORCE_BIG", "1")
+    for make, K, L, R, rng in [(skew_csr, 2, 6, 8, 64),
+                               (lambda: shape_slice("webspam", 1500), 4, 50, 128, 256),
+                               (lambda: synth.generate(synth.SHAPES["tiny"].with_(N=2000)), 1, 2, 300, 1)]:
+        rp, col = make()
+        n = rp.size - 1
+        seed = 4242
+        addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+        T = oracle.build(L, R, rng, seed, addrs, np.arange(n, dtype=np.uint32))
+        d_rp, d_col = flash.to_device_csr(rp, col)
+        with flash.FlashIndex(K, L, R, rng, seed) as idx:
+            idx.insert(d_rp, d_col, 0)
+            _check_tables(idx, T)
+
+
+def test_incremental_inserts_equal_one_build():
+    rp, col = shape_slice("url", 5000)
+    n = rp.size - 1
+    K, L, R, rng, seed = 3, 20, 16, 1 << 9, 99
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    ids = np.arange(n, dtype=np.uint32) + 1000
+    T = oracle.build(L, R, rng, seed, addrs, ids)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        for a, b in [(0, 1700), (1700, 1701), (1701, 5000)]:
+            flash.flash_insert(idx.h, d_rp[a:b + 1].contiguous(), d_col, b - a, 1000 + a)
+        _check_tables(idx, T)
+    # precomputed-address insert in a different batch split, rows out of order
+    d_addrs = torch.from_numpy(addrs.view(np.int32)).cuda()
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert_addrs(d_addrs[3000:].contiguous(), 1000 + 3000)
+        idx.insert_addrs(d_addrs[:3000].contiguous(), 1000)
+        _check_tables(idx, T)
+
+
+QUERY_CASES = [
+    ("tiny_k10", lambda: synth.generate("tiny"), 4, 16, 32, 1 << 15, 10),
+    ("tiny_k1", lambda: synth.generate("tiny"), 4, 16, 32, 1 << 15, 1),
+    ("skew_k7", skew_csr, 2, 6, 8, 64, 7),
+    ("skew_small_range_k1024", skew_csr, 1, 8, 64, 16, 1024),
+    ("webspam_k128", lambda: shape_slice("webspam", 2500), 4, 50, 128, 1 << 15, 128),
+    ("webspam_dense_buckets_k128", lambda: shape_slice("webspam", 2500), 4, 50, 128, 1 << 7, 128),
+    ("url_k128", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 15, 128),
+    ("edge_k5", edge_csr, 4, 16, 4, 1000, 5),
+]
+
+
+@pytest.mark.parametrize("name,make,K,L,R,rng,k", QUERY_CASES, ids=[c[0] for c in QUERY_CASES])
+def test_query_topk_bit_exact(name, make, K, L, R, rng, k):
+    rp, col = make()
+    n = rp.size - 1
+    seed = 0xC0DE + k
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    ids = np.arange(n, dtype=np.uint32)
+    T = oracle.build(L, R, rng, seed, addrs, ids)
+    g = np.random.default_rng(k)
+    excl = g.integers(0, n + 5, size=n).astype(np.uint32)
+    o_ids, o_cnt = oracle.query(T, addrs, k, exclude=excl)
+    o_ids2, o_cnt2 = oracle.query(T, addrs, k)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert(d_rp, d_col, 0)
+        d_addrs = torch.from_numpy(addrs.view(np.int32)).cuda()
+        d_ex = torch.from_numpy(excl.view(np.int32)).cuda()
+        g_ids, g_cnt = idx.query_addrs(d_addrs, k, d_ex)
+        assert np.array_equal(flash.as_u32(g_ids), o_ids)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
+        g_ids, g_cnt = idx.query(d_rp, d_col, k)  # CSR query path, no exclusion
+        assert np.array_equal(flash.as_u32(g_ids), o_ids2)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt2)
+
+
+GRAPH_CASES = [
+    ("tiny", lambda: synth.generate("tiny"), 4, 16, 32, 1 << 15, 10),
+    ("edge", edge_csr, 4, 16, 32, 1 << 15, 10),
+    ("webspam_slice", lambda: shape_slice("webspam", 4000), 4, 50, 128, 1 << 15, 128),
+    ("url_slice", lambda: shape_slice("url", 8000), 4, 128, 32, 1 << 15, 128),
+    ("kdd12_slice", lambda: shape_slice("kdd12", 30000), 4, 32, 64, 1 << 20, 128),
+]
+
+
+@pytest.mark.parametrize("name,make,K,L,R,rng,k", GRAPH_CASES, ids=[c[0] for c in GRAPH_CASES])
+def test_knn_graph_bit_exact(name, make, K, L, R, rng, k):
+    rp, col = make()
+    seed = 0x5EED0002
+    o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        g_ids, g_cnt = idx.knn_graph(d_rp, d_col, k)
+        assert np.array_equal(flash.as_u32(g_ids), o_ids)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
+    # the host-buffer entry point (pageable and pinned inputs) gives the same graph
+    n = rp.size - 1
+    for pinned in (False, True):
+        hrp = torch.from_numpy(rp.copy())
+        hcol = torch.from_numpy(col.view(np.int32).copy())
+        out_i = torch.empty((n, k), dtype=torch.int32)
+        out_c = torch.empty((n, k), dtype=torch.int32)
+        if pinned:
+            hrp, hcol, out_i, out_c = (t.pin_memory() for t in (hrp, hcol, out_i, out_c))
+        with flash.FlashIndex(K, L, R, rng, seed) as idx:
+            flash.flash_knn_graph_host(idx.h, hrp, hcol, n, k, out_i, out_c)
+        assert np.array_equal(out_i.numpy().view(np.uint32), o_ids)
+        assert np.array_equal(out_c.numpy().view(np.uint32), o_cnt)
+
+
+def test_graph_is_deterministic_across_runs_and_streams():
+    rp, col = shape_slice("webspam", 3000)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    outs = []
+    for i in range(3):
+        s = torch.cuda.Stream() if i == 2 else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            with flash.FlashIndex(4, 50, 128, 1 << 12, 3) as idx:
+                ids, cnt = idx.knn_graph(d_rp, d_col, 64)
+                torch.cuda.synchronize()
+                outs.append((flash.as_u32(ids), flash.as_u32(cnt)))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+
+
+def test_errors_and_states():
+    rp, col = synth.generate("tiny")
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(4, 16, 32, 1 << 15, 1) as idx:
+        # query before any insert: all pads
+        ids, cnt = idx.query(d_rp, d_col, 5)
+        assert (flash.as_u32(ids) == EMPTY).all() and (flash.as_u32(cnt) == 0).all()
+        idx.insert(d_rp, d_col)
+        with pytest.raises(flash.FlashError) as e:
+            idx.knn_graph(d_rp, d_col, 5)
+        assert e.value.status == flash.FLASH_ESTATE
+        with pytest.raises(flash.FlashError) as e:
+            idx.query(d_rp, d_col, 0)
+        assert e.value.status == flash.FLASH_EINVAL
+        with pytest.raises(flash.FlashError) as e:  # host pointer where a device one is required
+            flash.flash_hash(idx.h, torch.from_numpy(rp), d_col, 3, None,
+                             torch.empty((3, 16), dtype=torch.int32, device="cuda"))
+        assert e.value.status == flash.FLASH_EINVAL
+        bad = torch.full((4, 16), 1 << 20, dtype=torch.int32, device="cuda")  # >= range
+        idx.insert_addrs(bad, 5000)
+        assert idx.errors() == 64
+    with flash.FlashIndex(4, 64, 256, 1 << 15, 1) as idx:  # L*R = 16384: beyond the count table
+        with pytest.raises(flash.FlashError) as e:
+            idx.query(d_rp, d_col, 5)
+        assert e.value.status == flash.FLASH_EINVAL
+
+
+def test_full_webspam_graph_sampled_parity():
+    """The bench's workload and launch configuration (350K x 3,728 nnz, K=4, L=50, R=128,
+    range 2^15, k=128): addresses of sampled rows and the graph rows of sampled queries
+    match the oracle (which builds the full tables on the host)."""
+    rp, col = synth.generate("webspam")
+    n = rp.size - 1
+    K, L, R, rng, seed, k = 4, 50, 128, 1 << 15, 0x5EED0002, 128
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        g_ids, g_cnt = idx.knn_graph(d_rp, d_col, k)
+        _, g_addrs = idx.hash(d_rp, d_col, codes=False)
+        torch.cuda.synchronize()
+    o_addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    assert np.array_equal(flash.as_u32(g_addrs), o_addrs)
+    T = oracle.build(L, R, rng, seed, o_addrs, np.arange(n, dtype=np.uint32))
+    sample = np.random.default_rng(0).choice(n, size=400, replace=False)
+    o_ids, o_cnt = oracle.query(T, o_addrs[sample], k, exclude=sample.astype(np.uint32))
+    assert np.array_equal(flash.as_u32(g_ids)[sample], o_ids)
+    assert np.array_equal(flash.as_u32(g_cnt)[sample], o_cnt)
