@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py — webspam-shaped approximate k-NN graph (FLASH hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one full k-NN graph from scratch over the resident webspam-shaped CSR:
+DOPH hashing of every row (H1-H3), bottom-R table build (B1-B2) and count-based
+top-k for every row (Q1-Q3) — all SURVEY §8(a) rows.  Workload = BASELINE.json
+configs[1]: N=350,000 rows, D=16,609,143, ~3,728 nnz/row (~1.3 G nnz), K=4, L=50,
+R=128, range=2^15, k=128 (synthetic, synth/ seed 2).
+
+`value` = N / graph time (queries/s over the whole graph; every row is a query),
+device-timed with CUDA events, max over ranks.  `e2e` = the same metric through
+flash_knn_graph_host (pinned host CSR in, host top-k out, copies inside the timed
+region).  N>1: one rank per GPU (torchrun), replicated tables (paper_1709_01190_b200
+/dist.py), strong scaling of the fixed graph.
+
+The reference arm (--impl reference) times the CPU oracle (oracle/) as it stands on
+the host cores, on a bounded sample of the same workload (hash + build of every row,
+top-k for a row sample, extrapolated per query); it is a deliberately slow baseline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+K, L, R, RANGE, SEED, TOPK = 4, 50, 128, 1 << 15, 0x5EED0002, 128
+METRIC = "webspam-shaped k-NN graph time (s), queries/s, hash nnz/s at 1/2/4/8 B200"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(shape, nnz, args):
+    return {
+        "workload": "webspam-shaped approximate k-NN graph from scratch (hash + build + query every row)",
+        "N": shape.N, "D": shape.D, "nnz": int(nnz), "nnz_per_row": round(nnz / shape.N, 1),
+        "K": K, "L": L, "R": R, "range": RANGE, "k": TOPK, "seed": SEED,
+        "parallelism": f"replicated-tables x{args.gpus}" if args.gpus > 1 else "1 GPU",
+        "l2_policy": "inputs larger than L2 (col_idx 5.2 GB vs 126 MB L2); no flush",
+    }
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = max(smax, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gen_local(shape, bounds, rank):
+    """This rank's rows (all rows at N=1), in pinned host memory."""
+    import torch
+
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    lens = np.empty(r1 - r0, dtype=np.int64)
+    p = synth._cparams(shape)
+    import ctypes
+
+    synth._load().synth_row_lengths(ctypes.byref(p), r0, r1, lens.ctypes.data)
+    nnz = int(lens.sum())
+    rp_t = torch.empty(r1 - r0 + 1, dtype=torch.int64).pin_memory()
+    col_t = torch.empty(max(nnz, 1), dtype=torch.int32).pin_memory()
+    synth.generate(shape, rows=(r0, r1), row_ptr_out=rp_t.numpy(), col_out=col_t.numpy().view(np.uint32))
+    return rp_t, col_t, nnz
+
+
+def query_work(idx_tables, addrs_np):
+    """Candidates gathered per graph (sum over queries of their L bucket sizes)."""
+    total = 0
+    for t in range(L):
+        off, _, _ = idx_tables(t)
+        sizes = np.diff(off.astype(np.int64))
+        a = addrs_np[:, t]
+        valid = a != 0xFFFFFFFF
+        total += int(sizes[a[valid].astype(np.int64)].sum())
+    return total
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_01190_b200 import dist as fdist
+    from paper_1709_01190_b200 import flash
+
+    rank, world, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = synth.SHAPES["webspam"]
+    t0 = time.time()
+    all_lens = np.empty(shape.N, dtype=np.int64)
+    import ctypes
+
+    synth._load().synth_row_lengths(ctypes.byref(synth._cparams(shape)), 0, shape.N, all_lens.ctypes.data)
+    bounds = fdist.shard_bounds(all_lens, world)
+    h_rp, h_col, nnz_local = gen_local(shape, bounds, rank)
+    nnz_total = int(all_lens.sum())
+    log(f"[rank {rank}] generated rows {bounds[rank]}..{bounds[rank + 1]} nnz={nnz_local} in {time.time() - t0:.1f}s")
+    n_local = bounds[rank + 1] - bounds[rank]
+    dev = torch.device("cuda", local)
+    # device-resident CSR (row_ptr rebased to this shard's col_idx)
+    d_rp = (h_rp.to(dev, non_blocking=True) - h_rp[0].item()).contiguous()
+    d_col = h_col.to(dev, non_blocking=True)
+    out_ids = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
+    idx = flash.FlashIndex(K, L, R, RANGE, SEED)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        idx.clear()
+        if world == 1:
+            flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, TOPK, out_ids, out_cnt)
+            return out_ids, out_cnt
+        return fdist.knn_graph_replicated(idx, d_rp, d_col, TOPK, bounds, rank)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flash.flash_reset_counters(idx.h)
+    flash.flash_set_profiling(idx.h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    phase_ms, phase_calls = flash.flash_phase_ms(idx.h)
+    launches = flash.flash_launch_count(idx.h)
+    flash.flash_set_profiling(idx.h, False)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    ms_step = ms_max / args.steps
+
+    # end-to-end through the host-buffer C-ABI entry point (N=1) / host copies around the
+    # distributed graph (N>1)
+    e2e_ms = []
+    h_ids = torch.empty((n_local, TOPK), dtype=torch.int32).pin_memory()
+    h_cnt = torch.empty((n_local, TOPK), dtype=torch.int32).pin_memory()
+    h_rp_local = (h_rp - h_rp[0]).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    for i in range(e2e_steps + 1):
+        idx.clear()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        if world == 1:
+            flash.flash_knn_graph_host(idx.h, h_rp_local, h_col, n_local, TOPK, h_ids, h_cnt)
+        else:
+            d_rp2 = h_rp_local.to(dev, non_blocking=True)
+            d_col2 = h_col.to(dev, non_blocking=True)
+            ids_, cnt_ = fdist.knn_graph_replicated(idx, d_rp2, d_col2, TOPK, bounds, rank)
+            h_ids.copy_(ids_, non_blocking=True)
+            h_cnt.copy_(cnt_, non_blocking=True)
+            torch.cuda.synchronize()
+        dt = (time.perf_counter() - t) * 1e3
+        if i > 0:  # first is warm-up
+            e2e_ms.append(dt)
+    e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(e2e_local.item())
+
+    # work counts for the roofline (graph of the last step; rank-local)
+    idx.clear()
+    step()
+    torch.cuda.synchronize()
+    addrs_np = flash.as_u32(idx.hash_addrs(d_rp, d_col))
+    n_cand = query_work(lambda t: idx.table(t), addrs_np) if world == 1 else None
+
+    result = None
+    if rank == 0:
+        hbm_peak, peak_kind = peaks()
+        per_step = {name: phase_ms[i] / max(phase_calls[i], 1) * (phase_calls[i] / args.steps)
+                    for i, name in enumerate(["hash", "build", "query", "copy"])}
+        # algorithmic bytes per launch
+        hash_bytes = 4 * nnz_local + 8 * (n_local + 1) + 4 * L * n_local
+        hash_ms = per_step["hash"]
+        query_ms = per_step["query"]
+        build_ms = per_step["build"]
+        dominant = max(("hash", hash_ms), ("build", build_ms), ("query", query_ms), key=lambda x: x[1])[0]
+        traffic = None
+        try:
+            with open(TRAFFIC_PATH) as f:
+                traffic = json.load(f)
+        except Exception:
+            pass
+        if dominant == "query" and n_cand is not None:
+            qbytes = 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local
+            roof = {"kernel": "k_query", "bound": "hbm", "achieved": qbytes / (query_ms * 1e-3) / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
+                    "traffic": (traffic or {}).get("k_query"), "algorithmic_bytes": qbytes,
+                    "candidates": n_cand}
+        elif dominant == "build":
+            bbytes = 8 * L * n_local * 2 + 12 * L * n_local
+            roof = {"kernel": "build (k_count..k_select_big)", "bound": "hbm",
+                    "achieved": bbytes / (build_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "peak_kind": peak_kind, "traffic": (traffic or {}).get("build"), "algorithmic_bytes": bbytes}
+        else:
+            roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
+                    "traffic": (traffic or {}).get("k_doph"), "algorithmic_bytes": hash_bytes}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        hash_roof = {"achieved_GBps": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                     "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak}
+        value = shape.N / (ms_step * 1e-3)
+        h2d = 8 * (n_local + 1) + 4 * nnz_local
+        d2h = 8 * n_local * TOPK
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "graph_time_s": ms_step * 1e-3,
+            "hash_nnz_per_s": nnz_local / (hash_ms * 1e-3) * world if hash_ms else None,
+            "queries_per_s": shape.N / (ms_step * 1e-3),
+            "phase_ms_per_step": per_step,
+            "hash_roofline": hash_roof,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (synth/, webspam shape, seed 2)",
+            "config": workload_config(shape, nnz_total, args),
+            "roofline": roof,
+            "e2e": {"value": shape.N / (e2e_ms_max * 1e-3), "unit": "queries/s",
+                    "ms_per_step": e2e_ms_max, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "flash_knn_graph_host (pinned host buffers)" if world == 1 else
+                           "host copies + replicated-table graph"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if n_cand is not None:
+            result["candidates_per_query"] = n_cand / n_local
+    idx.close()
+    return result
+
+
+def cpu_baseline(sample_queries: int, steps: int = 1):
+    """The oracle as it stands on the host cores: full hash + build, a query sample."""
+    import oracle
+
+    shape = synth.SHAPES["webspam"]
+    rp, col = synth.generate(shape)
+    n = rp.size - 1
+    cores = os.cpu_count()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        codes = oracle.doph(K, L, SEED, rp, col)
+        addrs = oracle.addresses(K, L, RANGE, SEED, codes)
+        del codes
+        t1 = time.perf_counter()
+        T = oracle.build(L, R, RANGE, SEED, addrs, np.arange(n, dtype=np.uint32))
+        t2 = time.perf_counter()
+        q = np.random.default_rng(0).choice(n, size=sample_queries, replace=False)
+        oracle.query(T, addrs[q], TOPK, exclude=q.astype(np.uint32))
+        t3 = time.perf_counter()
+        graph_s = (t1 - t0) + (t2 - t1) + (t3 - t2) * n / sample_queries
+        times.append((graph_s, t1 - t0, t2 - t1, t3 - t2))
+    g = statistics.median(x[0] for x in times)
+    return {"value": n / g, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"hash+build of all {n} rows, top-{TOPK} for {sample_queries} sampled rows, "
+                      f"query time extrapolated x{n / sample_queries:.1f}",
+            "graph_s_extrapolated": g, "hash_s": times[-1][1], "build_s": times[-1][2],
+            "query_sample_s": times[-1][3]}, times
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    shape = synth.SHAPES["webspam"]
+    cb, times = cpu_baseline(args.ref_sample, steps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    g = statistics.median(x[0] for x in timed)
+    return {
+        "metric": METRIC, "impl": "reference", "value": shape.N / g, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": g * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (synth/, webspam shape, seed 2)",
+        "config": workload_config(shape, int(0), args) | {"nnz": None},
+        "cpu_baseline": cb,
+        "e2e": {"value": shape.N / g, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-sample", type=int, default=20000, help="oracle query sample (rows)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res = run_ours(args)
+    rank, world, _ = dist_env()
+    if rank == 0 and res is not None:
+        if world == 1 and not args.no_cpu_baseline:
+            cb, _ = cpu_baseline(args.ref_sample, steps=1)
+            res["cpu_baseline"] = cb
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

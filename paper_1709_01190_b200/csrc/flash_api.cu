@@ -487,6 +487,21 @@ flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const 
   return FLASH_OK;
 }
 
+flash_status flash_clear(flash_index* h, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  flash_status st = enter(h, s);
+  if (st != FLASH_OK) return st;
+  CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * (size_t)h->L * h->range, s));
+  if (h->goff) CUDA_TRY(cudaFreeAsync(h->goff, s));
+  if (h->ids) CUDA_TRY(cudaFreeAsync(h->ids, s));
+  h->goff = nullptr;
+  h->ids = nullptr;
+  h->kept_ub = 0;
+  h->n_inserted = 0;
+  return FLASH_OK;
+}
+
 flash_status flash_get_table(const flash_index* h, uint32_t t, const uint32_t** off, const uint32_t** ids,
                              const uint32_t** arrivals, uint64_t* n_ids) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");

@@ -110,7 +110,10 @@ k_query(QueryArgs a, uint32_t hist_len) {
     const uint32_t D = s_nlist;
 
     // ---- Q3: threshold count c*, then the ids tied at c* ----
-    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) atomicAdd(&hist[get_count(cnt32, list[j])], 1u);
+    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
+      const uint32_t c = get_count(cnt32, list[j]);
+      atomicAdd(&hist[c < a.L ? c : a.L], 1u);  // counts <= L unless ids repeat (contract)
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t cum = 0, c = a.L, cstar = 0, need = 0, ties = 0;
@@ -217,10 +220,11 @@ int launch_query(const QueryArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
   const uint32_t hist_len = (a.L + 1) > 256 ? a.L + 1 : 256;
   const size_t smem = query_smem_bytes(a.table_log2, a.k) + hist_len * 4;
-  static size_t attr = 0;
+  static size_t attr = 48 * 1024;
   if (smem > attr) {
-    cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = 227 * 1024;
+    if (cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return 0;  // the launch below then fails and the caller reports it
+    attr = smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kQThreads, smem);

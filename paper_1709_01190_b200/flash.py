@@ -30,7 +30,7 @@ _NAMES = {1: "FLASH_EINVAL", 2: "FLASH_ENOMEM", 3: "FLASH_ECUDA", 4: "FLASH_ENCC
 EXPORTS = (
     "flash_create", "flash_destroy", "flash_hash", "flash_insert", "flash_insert_addrs",
     "flash_query_topk", "flash_query_addrs", "flash_knn_graph", "flash_knn_graph_host",
-    "flash_get_table", "flash_check", "flash_set_profiling", "flash_phase_ms",
+    "flash_get_table", "flash_clear", "flash_check", "flash_set_profiling", "flash_phase_ms",
     "flash_launch_count", "flash_reset_counters", "flash_last_error",
 )
 
@@ -66,6 +66,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.flash_get_table.argtypes = [vp, u32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                                   ctypes.POINTER(u64)]
     L.flash_check.argtypes = [vp, ctypes.POINTER(u64)]
+    L.flash_clear.argtypes = [vp, vp]
     L.flash_set_profiling.argtypes = [vp, i32]
     L.flash_phase_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
     L.flash_launch_count.argtypes = [vp]
@@ -184,6 +185,10 @@ def flash_get_table(h, t: int):
     return off.value, ids.value, arr.value, n.value
 
 
+def flash_clear(h, stream=None):
+    _check(load_library().flash_clear(h, _stream(stream)))
+
+
 def flash_check(h) -> int:
     n = ctypes.c_uint64()
     _check(load_library().flash_check(h, ctypes.byref(n)))
@@ -221,7 +226,7 @@ class _DeviceArray:
     """Zero-copy view of library-owned device memory (CUDA array interface)."""
 
     def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, True),
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
                                          "version": 2, "strides": None}
 
 
@@ -263,6 +268,9 @@ class FlashIndex:
         flash_hash(self.h, row_ptr, col_idx, n, c, a)
         return c, a
 
+    def hash_addrs(self, row_ptr, col_idx):
+        return self.hash(row_ptr, col_idx, codes=False)[1]
+
     def insert(self, row_ptr, col_idx, id_base=0):
         flash_insert(self.h, row_ptr, col_idx, row_ptr.numel() - 1, id_base)
 
@@ -297,6 +305,9 @@ class FlashIndex:
         ids = _copy_device(ids_p, n, self.device)
         arr = _copy_device(arr_p, self.range, self.device)
         return as_u32(off), as_u32(ids), as_u32(arr)
+
+    def clear(self):
+        flash_clear(self.h)
 
     def errors(self) -> int:
         return flash_check(self.h)
