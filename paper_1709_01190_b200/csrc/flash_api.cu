@@ -1,8 +1,11 @@
 // flash_api.cu — the C ABI of libflash.so (include/flash.h): handle, validation,
-// stream-ordered scratch, phase orchestration, profiling counters.
+// handle-owned device arena, phase orchestration, profiling counters.
 //
 // Every entry point validates on the host before enqueueing anything, enqueues on the
 // caller's stream, and returns without synchronizing (except where flash.h says so).
+// Device memory: the handle owns every buffer the path needs (tables double-buffered,
+// scratch sized to the largest call so far).  Buffers only grow, so steady-state calls
+// never allocate (growth uses cudaMalloc/cudaFree, which synchronize the device).
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -41,10 +44,44 @@ flash_status fail(flash_status st, const char* fmt, ...) {
     }                                                                                  \
   } while (0)
 
+#define TRY(expr)                    \
+  do {                               \
+    flash_status st_ = (expr);       \
+    if (st_ != FLASH_OK) return st_; \
+  } while (0)
+
 struct PendingPhase {
   int phase;
   cudaEvent_t a, b;
 };
+
+// A grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+flash_status ensure(DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return FLASH_OK;
+  if (b.p) CUDA_TRY(cudaFree(b.p));
+  b.p = nullptr;
+  b.cap = 0;
+  const size_t want = bytes + bytes / 8;  // headroom against repeated regrowth
+  CUDA_TRY(cudaMalloc(&b.p, want));
+  b.cap = want;
+  return FLASH_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
 
 }  // namespace
 
@@ -54,17 +91,22 @@ struct flash_index {
   HashKeys keys;
   int device;
   uint32_t table_log2;
-  // tables (null before the first insert)
+  // tables: goff / ids double-buffered; `have_tables` false before the first insert
   uint32_t* arrivals = nullptr;  // [L*range]
-  uint64_t* goff = nullptr;      // [L*range+1]
-  uint32_t* ids = nullptr;       // [kept_ub]
-  uint64_t kept_ub = 0;          // host upper bound on kept ids
-  uint64_t n_inserted = 0;       // rows passed to insert (host count)
-  uint32_t* off_tmp = nullptr;   // [range+1] for flash_get_table
+  DevBuf goff[2], ids[2];
+  int cur = 0;
+  bool have_tables = false;
+  uint64_t kept_ub = 0;     // host upper bound on kept ids
+  uint64_t n_inserted = 0;  // rows passed to insert (host count)
+  // scratch
+  DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
+  DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
   bool have_last = false;
   cudaEvent_t order_ev = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_events;
   // profiling
   int profiling = 0;
   std::vector<PendingPhase> pending;
@@ -108,14 +150,6 @@ struct Phase {
   }
 };
 
-template <typename T>
-flash_status salloc(T** p, size_t count, cudaStream_t s) {
-  *p = nullptr;
-  if (count == 0) count = 1;
-  CUDA_TRY(cudaMallocAsync((void**)p, sizeof(T) * count, s));
-  return FLASH_OK;
-}
-
 // True when the GPU can dereference p (device, managed, or mapped host memory).
 bool device_accessible(const void* p) {
   if (!p) return false;
@@ -128,8 +162,8 @@ bool device_accessible(const void* p) {
          (at.type == cudaMemoryTypeHost && at.devicePointer != nullptr);
 }
 
-#define REQUIRE_DEV(p)                                                              \
-  do {                                                                              \
+#define REQUIRE_DEV(p)                                                                     \
+  do {                                                                                     \
     if (!device_accessible(p)) return fail(FLASH_EINVAL, "%s is not a device pointer", #p); \
   } while (0)
 
@@ -150,8 +184,22 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
 
 flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
                              cudaStream_t s) {
-  Phase ph(h, 1, s);
   const uint64_t nb = (uint64_t)h->L * h->range;
+  const uint64_t pool_cap = h->kept_ub + n * h->L;
+  const uint64_t kept_cap = pool_cap < nb * h->R ? pool_cap : nb * h->R;
+  const int nxt = h->have_tables ? 1 - h->cur : h->cur;
+  // buffers first (growth synchronizes; it happens outside the profiled phase)
+  TRY(ensure(h->cursor, sizeof(uint32_t) * nb));
+  TRY(ensure(h->pool_cnt, sizeof(uint64_t) * (nb + 1)));
+  TRY(ensure(h->pool_off, sizeof(uint64_t) * (nb + 1)));
+  TRY(ensure(h->keep_cnt, sizeof(uint64_t) * (nb + 1)));
+  TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
+  TRY(ensure(h->pool, sizeof(uint32_t) * pool_cap));
+  TRY(ensure(h->ids[nxt], sizeof(uint32_t) * kept_cap));
+  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 1)));
+  TRY(ensure(h->scan_tmp, build_scan_tmp_bytes(nb)));
+
+  Phase ph(h, 1, s);
   BuildArgs a;
   memset(&a, 0, sizeof a);
   a.addrs = addrs;
@@ -161,57 +209,47 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.R = h->R;
   a.range = h->range;
   a.keys = h->keys;
-  a.goff_old = h->goff;
-  a.ids_old = h->ids;
+  a.goff_old = h->have_tables ? h->goff[h->cur].as<uint64_t>() : nullptr;
+  a.ids_old = h->have_tables ? h->ids[h->cur].as<uint32_t>() : nullptr;
   a.arrivals = h->arrivals;
   a.err = h->err;
-  uint64_t pool_cap = h->kept_ub + n * h->L;
-  uint64_t kept_cap = pool_cap < nb * h->R ? pool_cap : nb * h->R;
-  flash_status st;
-  if ((st = salloc(&a.cursor, nb, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.pool_cnt, nb + 1, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.pool_off, nb + 1, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.keep_cnt, nb + 1, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.goff_new, nb + 1, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.pool, pool_cap, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.ids_new, kept_cap, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.big_list, nb, s)) != FLASH_OK) return st;
-  if ((st = salloc(&a.big_count, 1, s)) != FLASH_OK) return st;
-  a.scan_tmp_bytes = build_scan_tmp_bytes(nb);
-  if ((st = salloc((uint8_t**)&a.scan_tmp, a.scan_tmp_bytes, s)) != FLASH_OK) return st;
+  a.cursor = h->cursor.as<uint32_t>();
+  a.pool_cnt = h->pool_cnt.as<uint64_t>();
+  a.pool_off = h->pool_off.as<uint64_t>();
+  a.keep_cnt = h->keep_cnt.as<uint64_t>();
+  a.goff_new = h->goff[nxt].as<uint64_t>();
+  a.pool = h->pool.as<uint32_t>();
+  a.ids_new = h->ids[nxt].as<uint32_t>();
+  a.big_list = h->big_list.as<uint32_t>();
+  a.big_count = h->big_list.as<uint32_t>() + nb;
+  a.scan_tmp = h->scan_tmp.p;
+  a.scan_tmp_bytes = h->scan_tmp.cap;
   h->launches += launch_build(a, s);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaFreeAsync(a.cursor, s));
-  CUDA_TRY(cudaFreeAsync(a.pool_cnt, s));
-  CUDA_TRY(cudaFreeAsync(a.pool_off, s));
-  CUDA_TRY(cudaFreeAsync(a.keep_cnt, s));
-  CUDA_TRY(cudaFreeAsync(a.pool, s));
-  CUDA_TRY(cudaFreeAsync(a.big_list, s));
-  CUDA_TRY(cudaFreeAsync(a.big_count, s));
-  CUDA_TRY(cudaFreeAsync(a.scan_tmp, s));
-  if (h->goff) CUDA_TRY(cudaFreeAsync(h->goff, s));
-  if (h->ids) CUDA_TRY(cudaFreeAsync(h->ids, s));
-  h->goff = a.goff_new;
-  h->ids = a.ids_new;
+  h->cur = nxt;
+  h->have_tables = true;
   h->kept_ub = kept_cap;
   h->n_inserted += n;
   return FLASH_OK;
 }
 
-flash_status do_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_t nq, uint32_t k,
+flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64_t nq, uint32_t k,
                             const uint32_t* exclude, int exclude_self, uint32_t self_base,
                             uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s) {
-  Phase ph(h, 2, s);
-  if (!h->goff) {  // nothing inserted: every query returns k pads
+  flash_index* h = const_cast<flash_index*>(hc);
+  if (!h->have_tables) {  // nothing inserted: every query returns k pads
+    Phase ph(h, 2, s);
     CUDA_TRY(cudaMemsetAsync(out_ids, 0xFF, sizeof(uint32_t) * nq * k, s));
     CUDA_TRY(cudaMemsetAsync(out_counts, 0, sizeof(uint32_t) * nq * k, s));
     return FLASH_OK;
   }
+  TRY(ensure(h->qscratch, query_scratch_bytes(nq)));
+  Phase ph(h, 2, s);
   QueryArgs a;
   a.addrs = addrs;
   a.nq = nq;
-  a.goff = h->goff;
-  a.ids = h->ids;
+  a.goff = h->goff[h->cur].as<uint64_t>();
+  a.ids = h->ids[h->cur].as<uint32_t>();
   a.L = h->L;
   a.range = h->range;
   a.k = k;
@@ -222,17 +260,19 @@ flash_status do_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_
   a.out_counts = out_counts;
   a.err = h->err;
   a.table_log2 = h->table_log2;
-  const_cast<flash_index*>(h)->launches += launch_query(a, s);
+  h->launches += launch_query(a, h->qscratch.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }
 
 flash_status check_query_shape(const flash_index* h, uint32_t k) {
   if (k == 0 || k > FLASH_MAX_TOPK) return fail(FLASH_EINVAL, "k=%u outside [1, %u]", k, FLASH_MAX_TOPK);
-  const size_t smem = query_smem_bytes(h->table_log2, k) + 4 * ((h->L + 1) > 256 ? h->L + 1 : 256);
-  if (smem > 227 * 1024)
+  if ((uint64_t)h->L * h->R > 8192)
     return fail(FLASH_EINVAL, "L*R=%llu too large for the shared-memory count table (current limit L*R <= 8192)",
                 (unsigned long long)h->L * h->R);
+  if (h->L > 4096) return fail(FLASH_EINVAL, "L=%u too large for the query kernel (limit 4096)", h->L);
+  if (query_smem_bytes(h->table_log2, h->L, k) > 227 * 1024)
+    return fail(FLASH_EINVAL, "query shared memory for L=%u, R=%u, k=%u exceeds 227 KB", h->L, h->R, k);
   return FLASH_OK;
 }
 
@@ -267,15 +307,7 @@ flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, ui
   if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * (size_t)L * range);
   if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&h->off_tmp, sizeof(uint32_t) * ((size_t)range + 1));
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep freed scratch cached across calls
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     flash_destroy(h);
@@ -294,11 +326,14 @@ void flash_destroy(flash_index* h) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
   }
+  for (auto e : h->copy_events) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   cudaFree(h->arrivals);
-  cudaFree(h->goff);
-  cudaFree(h->ids);
   cudaFree(h->err);
-  cudaFree(h->off_tmp);
+  for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
+                    &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
+                    &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
+    release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
   delete h;
 }
@@ -313,8 +348,7 @@ flash_status flash_hash(const flash_index* h, const int64_t* row_ptr, const uint
   if (codes) REQUIRE_DEV(codes);
   if (addrs) REQUIRE_DEV(addrs);
   cudaStream_t s = (cudaStream_t)stream;
-  flash_status st = enter(h, s);
-  if (st != FLASH_OK) return st;
+  TRY(enter(h, s));
   return do_hash(h, row_ptr, col_idx, n_rows, codes, addrs, s);
 }
 
@@ -326,8 +360,7 @@ flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t 
   if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
     return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
   cudaStream_t s = (cudaStream_t)stream;
-  flash_status st = enter(h, s);
-  if (st != FLASH_OK) return st;
+  TRY(enter(h, s));
   return do_insert_addrs(h, addrs, n_rows, id_base, s);
 }
 
@@ -340,37 +373,33 @@ flash_status flash_insert(flash_index* h, const int64_t* row_ptr, const uint32_t
   if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
     return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
   cudaStream_t s = (cudaStream_t)stream;
-  flash_status st = enter(h, s);
-  if (st != FLASH_OK) return st;
-  uint32_t* addrs = nullptr;
-  if ((st = salloc(&addrs, n_rows * h->L, s)) != FLASH_OK) return st;
-  if ((st = do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s)) != FLASH_OK) return st;
-  if ((st = do_insert_addrs(h, addrs, n_rows, id_base, s)) != FLASH_OK) return st;
-  CUDA_TRY(cudaFreeAsync(addrs, s));
-  return FLASH_OK;
+  TRY(enter(h, s));
+  TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
+  uint32_t* addrs = h->addrs.as<uint32_t>();
+  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
+  return do_insert_addrs(h, addrs, n_rows, id_base, s);
 }
 
 flash_status flash_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_t n_q, uint32_t k,
                                const uint32_t* exclude, uint32_t* out_ids, uint32_t* out_counts, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  flash_status st = check_query_shape(h, k);
-  if (st != FLASH_OK) return st;
+  TRY(check_query_shape(h, k));
   if (n_q == 0) return FLASH_OK;
   REQUIRE_DEV(addrs);
   REQUIRE_DEV(out_ids);
   REQUIRE_DEV(out_counts);
   if (exclude) REQUIRE_DEV(exclude);
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = enter(h, s)) != FLASH_OK) return st;
+  TRY(enter(h, s));
   return do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s);
 }
 
-flash_status flash_query_topk(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,
+flash_status flash_query_topk(const flash_index* hc, const int64_t* row_ptr, const uint32_t* col_idx,
                               uint64_t n_q, uint32_t k, const uint32_t* exclude, uint32_t* out_ids,
                               uint32_t* out_counts, void* stream) {
-  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  flash_status st = check_query_shape(h, k);
-  if (st != FLASH_OK) return st;
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  TRY(check_query_shape(h, k));
   if (n_q == 0) return FLASH_OK;
   REQUIRE_DEV(row_ptr);
   REQUIRE_DEV(col_idx);
@@ -378,21 +407,18 @@ flash_status flash_query_topk(const flash_index* h, const int64_t* row_ptr, cons
   REQUIRE_DEV(out_counts);
   if (exclude) REQUIRE_DEV(exclude);
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = enter(h, s)) != FLASH_OK) return st;
-  uint32_t* addrs = nullptr;
-  if ((st = salloc(&addrs, n_q * h->L, s)) != FLASH_OK) return st;
-  if ((st = do_hash(h, row_ptr, col_idx, n_q, nullptr, addrs, s)) != FLASH_OK) return st;
-  if ((st = do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s)) != FLASH_OK) return st;
-  CUDA_TRY(cudaFreeAsync(addrs, s));
-  return FLASH_OK;
+  TRY(enter(h, s));
+  TRY(ensure(h->addrs, sizeof(uint32_t) * n_q * h->L));
+  uint32_t* addrs = h->addrs.as<uint32_t>();
+  TRY(do_hash(h, row_ptr, col_idx, n_q, nullptr, addrs, s));
+  return do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s);
 }
 
 flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
                              uint32_t k, uint32_t* out_ids, uint32_t* out_counts, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  if (h->goff || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph needs a fresh handle");
-  flash_status st = check_query_shape(h, k);
-  if (st != FLASH_OK) return st;
+  if (h->have_tables || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph needs a fresh handle");
+  TRY(check_query_shape(h, k));
   if (n_rows == 0) return FLASH_OK;
   if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
   REQUIRE_DEV(row_ptr);
@@ -400,125 +426,125 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
   REQUIRE_DEV(out_ids);
   REQUIRE_DEV(out_counts);
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = enter(h, s)) != FLASH_OK) return st;
-  uint32_t* addrs = nullptr;
-  if ((st = salloc(&addrs, n_rows * h->L, s)) != FLASH_OK) return st;
-  if ((st = do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s)) != FLASH_OK) return st;
-  if ((st = do_insert_addrs(h, addrs, n_rows, 0, s)) != FLASH_OK) return st;
-  if ((st = do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s)) != FLASH_OK) return st;
-  CUDA_TRY(cudaFreeAsync(addrs, s));
-  return FLASH_OK;
+  TRY(enter(h, s));
+  TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
+  uint32_t* addrs = h->addrs.as<uint32_t>();
+  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
+  TRY(do_insert_addrs(h, addrs, n_rows, 0, s));
+  return do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s);
 }
 
 flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,
                                   uint64_t n_rows, uint32_t k, uint32_t* out_ids, uint32_t* out_counts,
                                   void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  if (h->goff || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph_host needs a fresh handle");
-  flash_status st = check_query_shape(h, k);
-  if (st != FLASH_OK) return st;
+  if (h->have_tables || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph_host needs a fresh handle");
+  TRY(check_query_shape(h, k));
   if (n_rows == 0) return FLASH_OK;
   if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
   if (!row_ptr || !col_idx || !out_ids || !out_counts) return fail(FLASH_EINVAL, "NULL buffer");
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = enter(h, s)) != FLASH_OK) return st;
+  TRY(enter(h, s));
   const int64_t nnz_begin = row_ptr[0], nnz_end = row_ptr[n_rows];
+  if (nnz_end < nnz_begin) return fail(FLASH_EINVAL, "row_ptr must be non-decreasing");
   const uint64_t nnz = (uint64_t)(nnz_end - nnz_begin);
-  int64_t* d_rp = nullptr;
-  uint32_t *d_col = nullptr, *d_addrs = nullptr, *d_ids = nullptr, *d_cnt = nullptr;
-  cudaStream_t cs = nullptr;
-  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  if ((st = salloc(&d_rp, n_rows + 1, s)) != FLASH_OK) return st;
-  if ((st = salloc(&d_col, nnz, s)) != FLASH_OK) return st;
-  if ((st = salloc(&d_addrs, n_rows * h->L, s)) != FLASH_OK) return st;
-  if ((st = salloc(&d_ids, n_rows * k, s)) != FLASH_OK) return st;
-  if ((st = salloc(&d_cnt, n_rows * k, s)) != FLASH_OK) return st;
+  TRY(ensure(h->h_rp, sizeof(int64_t) * (n_rows + 1)));
+  TRY(ensure(h->h_col, sizeof(uint32_t) * nnz));
+  TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
+  TRY(ensure(h->h_ids, sizeof(uint32_t) * n_rows * k));
+  TRY(ensure(h->h_cnt, sizeof(uint32_t) * n_rows * k));
+  if (!h->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  int64_t* d_rp = h->h_rp.as<int64_t>();
+  uint32_t* d_col = h->h_col.as<uint32_t>();
+  uint32_t* d_addrs = h->addrs.as<uint32_t>();
+  uint32_t* d_ids = h->h_ids.as<uint32_t>();
+  uint32_t* d_cnt = h->h_cnt.as<uint32_t>();
+  const uint32_t* d_col_abs = d_col - nnz_begin;  // absolute CSR offsets index this
+  cudaStream_t cs = h->copy_stream;
   {
     Phase ph(h, 3, s);
     CUDA_TRY(cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice, s));
   }
-  // col_idx is indexed from row_ptr[0]: shift the device pointer so absolute offsets work
-  const uint32_t* d_col_abs = d_col - nnz_begin;
-  // chunked H2D on a copy stream, hashing chunk i while chunk i+1 is in flight
+  // chunked H2D of col_idx on the copy stream; chunk i is hashed while chunk i+1 copies
   const uint64_t chunk_bytes = 256ull << 20;
-  std::vector<cudaEvent_t> evs;
+  size_t ev_used = 0;
+  auto next_event = [&](cudaEvent_t* ev) -> flash_status {
+    if (ev_used == h->copy_events.size()) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->copy_events.push_back(e);
+    }
+    *ev = h->copy_events[ev_used++];
+    return FLASH_OK;
+  };
   cudaEvent_t ready;
-  CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventRecord(ready, s));  // allocations are ordered on s
+  TRY(next_event(&ready));
+  CUDA_TRY(cudaEventRecord(ready, s));  // previous users of the staging buffers are done
   CUDA_TRY(cudaStreamWaitEvent(cs, ready, 0));
   uint64_t r0 = 0;
   while (r0 < n_rows) {
-    uint64_t r1 = r0 + 1;
-    // grow the chunk to ~chunk_bytes of col_idx
     uint64_t lo = r0 + 1, hi = n_rows;
     while (lo < hi) {
-      uint64_t mid = lo + (hi - lo + 1) / 2;
+      const uint64_t mid = lo + (hi - lo + 1) / 2;
       if ((uint64_t)(row_ptr[mid] - row_ptr[r0]) * 4 <= chunk_bytes) lo = mid; else hi = mid - 1;
     }
-    r1 = lo;
+    const uint64_t r1 = lo;
     const uint64_t e0 = (uint64_t)(row_ptr[r0] - nnz_begin), e1 = (uint64_t)(row_ptr[r1] - nnz_begin);
-    if (e1 > e0)
-      CUDA_TRY(cudaMemcpyAsync(d_col + e0, col_idx + nnz_begin + e0, sizeof(uint32_t) * (e1 - e0),
-                               cudaMemcpyHostToDevice, cs));
     cudaEvent_t ev;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TRY(next_event(&ev));
+    {
+      Phase ph(h, 3, cs);
+      if (e1 > e0)
+        CUDA_TRY(cudaMemcpyAsync(d_col + e0, col_idx + nnz_begin + e0, sizeof(uint32_t) * (e1 - e0),
+                                 cudaMemcpyHostToDevice, cs));
+    }
     CUDA_TRY(cudaEventRecord(ev, cs));
     CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
-    evs.push_back(ev);
-    if ((st = do_hash(h, d_rp + r0, d_col_abs, r1 - r0, nullptr, d_addrs + r0 * h->L, s)) != FLASH_OK) return st;
+    TRY(do_hash(h, d_rp + r0, d_col_abs, r1 - r0, nullptr, d_addrs + r0 * h->L, s));
     r0 = r1;
   }
-  if ((st = do_insert_addrs(h, d_addrs, n_rows, 0, s)) != FLASH_OK) return st;
-  if ((st = do_query_addrs(h, d_addrs, n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s)) != FLASH_OK) return st;
+  TRY(do_insert_addrs(h, d_addrs, n_rows, 0, s));
+  TRY(do_query_addrs(h, d_addrs, n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s));
   {
     Phase ph(h, 3, s);
     CUDA_TRY(cudaMemcpyAsync(out_ids, d_ids, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(out_counts, d_cnt, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
   }
-  CUDA_TRY(cudaFreeAsync(d_rp, s));
-  CUDA_TRY(cudaFreeAsync(d_col, s));
-  CUDA_TRY(cudaFreeAsync(d_addrs, s));
-  CUDA_TRY(cudaFreeAsync(d_ids, s));
-  CUDA_TRY(cudaFreeAsync(d_cnt, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  for (auto e : evs) cudaEventDestroy(e);
-  cudaEventDestroy(ready);
-  cudaStreamDestroy(cs);
   return FLASH_OK;
 }
 
 flash_status flash_clear(flash_index* h, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
   cudaStream_t s = (cudaStream_t)stream;
-  flash_status st = enter(h, s);
-  if (st != FLASH_OK) return st;
+  TRY(enter(h, s));
   CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * (size_t)h->L * h->range, s));
-  if (h->goff) CUDA_TRY(cudaFreeAsync(h->goff, s));
-  if (h->ids) CUDA_TRY(cudaFreeAsync(h->ids, s));
-  h->goff = nullptr;
-  h->ids = nullptr;
+  h->have_tables = false;
   h->kept_ub = 0;
   h->n_inserted = 0;
   return FLASH_OK;
 }
 
-flash_status flash_get_table(const flash_index* h, uint32_t t, const uint32_t** off, const uint32_t** ids,
+flash_status flash_get_table(const flash_index* hc, uint32_t t, const uint32_t** off, const uint32_t** ids,
                              const uint32_t** arrivals, uint64_t* n_ids) {
-  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
   if (t >= h->L) return fail(FLASH_EINVAL, "table %u >= L=%u", t, h->L);
-  if (!h->goff) return fail(FLASH_ESTATE, "nothing inserted yet");
+  if (!h->have_tables) return fail(FLASH_ESTATE, "nothing inserted yet");
   CUDA_TRY(cudaSetDevice(h->device));
   if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+  TRY(ensure(h->off_tmp, sizeof(uint32_t) * ((size_t)h->range + 1)));
+  const uint64_t* goff = h->goff[h->cur].as<uint64_t>();
   uint64_t b[2];
-  CUDA_TRY(cudaMemcpy(&b[0], h->goff + (uint64_t)t * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(&b[1], h->goff + (uint64_t)(t + 1) * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  k_table_off<<<(h->range + 256) / 256 < 4096 ? (h->range + 256) / 256 : 4096, 256>>>(h->goff, t, h->range,
-                                                                                     h->off_tmp);
+  CUDA_TRY(cudaMemcpy(&b[0], goff + (uint64_t)t * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&b[1], goff + (uint64_t)(t + 1) * h->range, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  const unsigned blocks = (h->range + 256) / 256 < 4096 ? (h->range + 256) / 256 : 4096;
+  k_table_off<<<blocks, 256>>>(goff, t, h->range, h->off_tmp.as<uint32_t>());
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
-  const_cast<flash_index*>(h)->launches++;
-  if (off) *off = h->off_tmp;
-  if (ids) *ids = h->ids + b[0];
+  h->launches++;
+  if (off) *off = h->off_tmp.as<uint32_t>();
+  if (ids) *ids = h->ids[h->cur].as<uint32_t>() + b[0];
   if (arrivals) *arrivals = h->arrivals + (uint64_t)t * h->range;
   if (n_ids) *n_ids = b[1] - b[0];
   return FLASH_OK;
@@ -564,9 +590,7 @@ uint64_t flash_launch_count(const flash_index* h) { return h ? h->launches : 0; 
 
 flash_status flash_reset_counters(flash_index* h) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  double ms[4];
-  flash_status st = flash_phase_ms(h, ms, nullptr);
-  if (st != FLASH_OK) return st;
+  TRY(flash_phase_ms(h, nullptr, nullptr));
   for (int i = 0; i < 4; ++i) {
     h->phase_ms[i] = 0;
     h->phase_calls[i] = 0;

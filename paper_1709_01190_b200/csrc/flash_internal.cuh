@@ -112,10 +112,12 @@ struct QueryArgs {
   uint32_t* out_ids;
   uint32_t* out_counts;
   unsigned long long* err;
-  uint32_t table_log2;      // count-table slots = 2^table_log2
+  uint32_t table_log2;      // worst-case count-table slots = 2^table_log2 (from L*R)
 };
-int launch_query(const QueryArgs& a, cudaStream_t s);
-size_t query_smem_bytes(uint32_t table_log2, uint32_t k);
+// scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
+int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s);
+size_t query_scratch_bytes(uint64_t nq);
+size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k);
 uint32_t query_table_log2(uint32_t L, uint32_t R);
 
 }  // namespace flash

@@ -1,238 +1,453 @@
 // query.cu — Q1-Q3: the querying phase (Alg. 3) on sm_100a.
 //
-// One CTA owns one query at a time (persistent over queries):
-//   Q1 gather   warp w walks tables t = w, w+8, ...; lanes read the bucket
-//               ids[goff[t*range+a_t] .. goff[t*range+a_t+1]) (coalesced, ascending ids).
-//   Q2 count    each id is inserted into a shared-memory open-addressing table
-//               (keys u32, counts u16 packed in u32 words): CAS on a new key, RED.ADD on
-//               its count.  New keys are appended to a slot list so later passes touch
-//               only the D distinct candidates (COUNTFREQUENCY with full multiplicity, R#11).
-//   Q3 top-k    counts are <= L, so a histogram of counts gives the threshold count c*;
-//               the ids tied at c* are cut by an 8-bit radix select on the id (ties broken
-//               by ascending id, R#12); the <= k survivors are bitonic-sorted by
-//               (count desc, id asc) and written, padded with (EMPTY, 0) (R#13).
-//   The excluded id (self in the k-NN graph, R#14) is dropped before counting.
+// k_query_plan: one lane per query sums the sizes M of its L addressed buckets and
+//   files the query into a size class (count-table capacity 2^11 / 2^13 / 2^14 slots,
+//   load factor <= 1/2), so most queries run with a small shared-memory footprint and
+//   many CTAs per SM.
+// k_query<LOG2S, NT>: one CTA owns one query at a time (persistent over its class list):
+//   Q1 gather   warp 0 scans the L bucket sizes into prefix offsets; every thread then
+//               walks flattened candidate positions p (binary search of the owning table,
+//               4 loads in flight per thread), reading ids[goff[t*range+a_t] + ...].
+//   Q2 count    each id goes into a shared-memory open-addressing table (u32 keys, u16
+//               counts updated through their u32 word): CAS on a new key, RED.ADD on its
+//               count; new slots are appended (warp-aggregated) to a list so later passes
+//               touch only the D distinct candidates (COUNTFREQUENCY, full multiplicity,
+//               R#11).  The excluded id (self in the k-NN graph, R#14) is skipped.
+//   Q3 top-k    counts are <= L: a count histogram gives the threshold count c* (warp-
+//               parallel suffix search); the ids tied at c* are cut at the need-th smallest
+//               id by an 8-bit radix select starting at the top set bit of the largest
+//               candidate id, stopping as soon as a digit bucket is taken whole (ties by
+//               ascending id, R#12).  The <= k survivors are placed by rank (count desc,
+//               id asc) and written, padded with (EMPTY, 0) (R#13).
 #include "flash_internal.cuh"
 
 namespace flash {
 namespace {
 
-constexpr int kQThreads = 256;
-constexpr int kQWarps = kQThreads / 32;
+constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t pow2_ceil_q(uint32_t x) {
   return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
 }
-
-__device__ __forceinline__ uint32_t get_count(const uint32_t* cnt32, uint32_t slot) {
-  return (cnt32[slot >> 1] >> ((slot & 1) * 16)) & 0xFFFFu;
+__device__ __forceinline__ uint32_t lanemask_lt_q() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
-template <typename T>
-__device__ void cta_bitonic(T* a, uint32_t n) {
-  for (uint32_t k = 2; k <= n; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t p = threadIdx.x; p < (n >> 1); p += blockDim.x) {
-        const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
-        const uint32_t ixj = i + j;
-        const T x = a[i], y = a[ixj];
-        const bool up = (i & k) == 0;
-        if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+// Query size classes: count-table slots 2^11, 2^13, 2^14 for M <= 1024, 4096, 8192.
+constexpr int kClasses = 3;
+
+__global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
+                             uint32_t L, uint32_t range, uint32_t* __restrict__ lists,
+                             uint32_t* __restrict__ counts, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t q0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; q0 < nq;
+       q0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = q0 + lane;
+    uint64_t M = 0;
+    if (q < nq) {
+      for (uint32_t t = 0; t < L; ++t) {
+        const uint32_t a = addrs[q * L + t];
+        if (a < range) {
+          const uint64_t i = (uint64_t)t * range + a;
+          M += goff[i + 1] - goff[i];
+        } else if (a != kEmpty) {
+          atomicAdd(err, 1ull);
+        }
       }
-      __syncthreads();
+    }
+    const int cls = M <= 1024 ? 0 : (M <= 4096 ? 1 : 2);
+#pragma unroll
+    for (int c = 0; c < kClasses; ++c) {
+      const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
+      if (!m) continue;
+      uint32_t b = 0;
+      if (lane == 0) b = atomicAdd(&counts[c], __popc(m));
+      b = __shfl_sync(kFullMask, b, 0);
+      if ((m >> lane) & 1) lists[(uint64_t)c * nq + b + __popc(m & lanemask_lt_q())] = (uint32_t)q;
     }
   }
 }
 
-struct QSmem {
-  uint32_t* keys;    // [S]
-  uint32_t* cnt32;   // [S/2] packed u16 counts
-  uint32_t* list;    // [S] slots of distinct keys, in insertion order
-  uint64_t* outbuf;  // [pow2(k)]
-  uint32_t* hist;    // [max(L+1, 256)]
+struct QueryShared {
+  uint32_t M, nlist, nout, cstar, need, ties, theta, maxid, done, prefix;
 };
 
-__global__ void __launch_bounds__(kQThreads)
-k_query(QueryArgs a, uint32_t hist_len) {
-  extern __shared__ __align__(16) uint8_t qsm[];
-  const uint32_t S = 1u << a.table_log2;
-  const uint32_t mask = S - 1;
-  const uint32_t kp2 = pow2_ceil_q(a.k);
-  uint64_t* outbuf = reinterpret_cast<uint64_t*>(qsm);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(outbuf + kp2);
-  uint32_t* cnt32 = keys + S;
-  uint32_t* list = cnt32 + S / 2;
-  uint32_t* hist = list + S;
-  __shared__ uint32_t s_nlist, s_nout, s_cstar, s_need, s_ties, s_theta, s_prefix;
+template <int LOG2S, int NT>
+__global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __restrict__ qlist,
+                                             const uint32_t* __restrict__ qcount, uint32_t hist_len) {
+  constexpr uint32_t S = 1u << LOG2S;
+  constexpr uint32_t MASK = S - 1;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t L = a.L, k = a.k;
+  const uint32_t kp2 = pow2_ceil_q(k);
+  uint64_t* outbuf = reinterpret_cast<uint64_t*>(sm);      // [kp2]
+  uint64_t* base = outbuf + kp2;                             // [L]
+  uint32_t* keys = reinterpret_cast<uint32_t*>(base + L);    // [S]
+  uint32_t* pref = keys + S;                                 // [L+1]
+  uint32_t* hist = pref + L + 1;                             // [hist_len]
+  uint32_t* cnt32 = hist + hist_len;                         // [S/2] (u16 counts)
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(cnt32);
+  uint16_t* list = cnt + S;                                  // [S]
+  __shared__ QueryShared sh;
 
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t j = threadIdx.x; j < S; j += blockDim.x) keys[j] = kEmpty;
-  for (uint32_t j = threadIdx.x; j < S / 2; j += blockDim.x) cnt32[j] = 0;
-  for (uint32_t j = threadIdx.x; j < hist_len; j += blockDim.x) hist[j] = 0;
-  if (threadIdx.x == 0) s_nlist = 0;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t j = tid; j < S; j += NT) keys[j] = kEmpty;
+  for (uint32_t j = tid; j < S / 2; j += NT) cnt32[j] = 0;
+  for (uint32_t j = tid; j < hist_len; j += NT) hist[j] = 0;
+  if (tid == 0) {
+    sh.nlist = 0;
+    sh.maxid = 0;
+  }
   __syncthreads();
 
-  for (uint64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+  const uint32_t nq = *qcount;
+  for (uint32_t it = blockIdx.x; it < nq; it += gridDim.x) {
+    const uint64_t q = qlist[it];
     const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
 
-    // ---- Q1 + Q2: gather and count ----
-    for (uint32_t t = warp; t < a.L; t += kQWarps) {
-      const uint32_t addr = a.addrs[q * a.L + t];
-      if (addr == kEmpty) continue;
-      if (addr >= a.range) {
-        if (lane == 0) atomicAdd(a.err, 1ull);
-        continue;
-      }
-      const uint64_t i = (uint64_t)t * a.range + addr;
-      const uint64_t s = a.goff[i], e = a.goff[i + 1];
-      for (uint64_t p = s + lane; p < e; p += 32) {
-        const uint32_t id = a.ids[p];
-        if (id == excl) continue;
-        uint32_t slot = (id * 0x9E3779B1u) >> (32 - a.table_log2);
-        while (true) {
-          uint32_t cur = keys[slot];
-          if (cur == kEmpty) {
-            cur = atomicCAS(&keys[slot], kEmpty, id);
-            if (cur == kEmpty) {
-              list[atomicAdd(&s_nlist, 1u)] = slot;
-              cur = id;
-            }
+    // ---- Q1: bucket segments -> prefix offsets (warp 0) ----
+    if (warp == 0) {
+      uint32_t carry = 0;
+      for (uint32_t t0 = 0; t0 < L; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        uint32_t sz = 0;
+        uint64_t st = 0;
+        if (t < L) {
+          const uint32_t ad = a.addrs[q * L + t];
+          if (ad < a.range) {
+            const uint64_t i = (uint64_t)t * a.range + ad;
+            st = a.goff[i];
+            sz = (uint32_t)(a.goff[i + 1] - st);
           }
-          if (cur == id) {
-            atomicAdd(&cnt32[slot >> 1], 1u << ((slot & 1) * 16));
-            break;
-          }
-          slot = (slot + 1) & mask;
         }
+        uint32_t x = sz;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t ex = carry + x - sz;
+        if (t < L) {
+          pref[t] = ex;
+          base[t] = st - ex;
+        }
+        carry += __shfl_sync(kFullMask, x, 31);
+      }
+      if (lane == 0) {
+        pref[L] = carry;
+        sh.M = carry;
       }
     }
     __syncthreads();
-    const uint32_t D = s_nlist;
+    const uint32_t M = sh.M;
 
-    // ---- Q3: threshold count c*, then the ids tied at c* ----
-    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
-      const uint32_t c = get_count(cnt32, list[j]);
-      atomicAdd(&hist[c < a.L ? c : a.L], 1u);  // counts <= L unless ids repeat (contract)
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t cum = 0, c = a.L, cstar = 0, need = 0, ties = 0;
-      if (D > a.k) {
-        for (; c >= 1; --c) {
-          if (cum + hist[c] >= a.k) break;
-          cum += hist[c];
+    // ---- Q2: gather + count ----
+    uint32_t mymax = 0;
+    for (uint32_t p0 = warp * 32; p0 < M; p0 += 4 * NT) {
+      uint32_t idv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t p = p0 + u * NT + lane;
+        idv[u] = kEmpty;
+        if (p < M) {
+          uint32_t lo = 0, hi = L - 1;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (pref[mid] <= p) lo = mid; else hi = mid - 1;
+          }
+          idv[u] = a.ids[base[lo] + p];
         }
-        cstar = c;
-        need = a.k - cum;  // how many of the hist[c*] tied ids to keep
-        ties = hist[c];
       }
-      s_cstar = cstar;
-      s_need = need;
-      s_ties = ties;
-      s_theta = 0xFFFFFFFFu;
-      s_nout = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t id = idv[u];
+        uint32_t newslot = 0xFFFFFFFFu;
+        if (id != kEmpty && id != excl) {
+          mymax = id > mymax ? id : mymax;
+          uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
+          while (true) {
+            uint32_t cur = keys[slot];
+            if (cur == kEmpty) {
+              cur = atomicCAS(&keys[slot], kEmpty, id);
+              if (cur == kEmpty) {
+                newslot = slot;
+                cur = id;
+              }
+            }
+            if (cur == id) {
+              atomicAdd(&cnt32[slot >> 1], 1u << ((slot & 1) * 16));
+              break;
+            }
+            slot = (slot + 1) & MASK;
+          }
+        }
+        const uint32_t m = __ballot_sync(kFullMask, newslot != 0xFFFFFFFFu);
+        if (m) {
+          uint32_t b = 0;
+          if (lane == 0) b = atomicAdd(&sh.nlist, __popc(m));
+          b = __shfl_sync(kFullMask, b, 0);
+          if (newslot != 0xFFFFFFFFu) list[b + __popc(m & lanemask_lt_q())] = (uint16_t)newslot;
+        }
+      }
+    }
+#pragma unroll
+    for (uint32_t o = 16; o > 0; o >>= 1) {
+      const uint32_t y = __shfl_xor_sync(kFullMask, mymax, o);
+      mymax = y > mymax ? y : mymax;
+    }
+    if (lane == 0 && mymax) atomicMax(&sh.maxid, mymax);
+    __syncthreads();
+    const uint32_t D = sh.nlist;
+
+    // ---- Q3a: count histogram (count-1 ids, the bulk, aggregated per warp) ----
+    for (uint32_t j0 = warp * 32; j0 < D; j0 += NT) {
+      const uint32_t j = j0 + lane;
+      uint32_t c = 0;
+      if (j < D) c = cnt[list[j]];
+      const uint32_t ones = __ballot_sync(kFullMask, c == 1);
+      if (lane == 0 && ones) atomicAdd(&hist[1], __popc(ones));
+      if (c > 1) atomicAdd(&hist[c < L ? c : L], 1u);
     }
     __syncthreads();
-    const uint32_t cstar = s_cstar;
-    if (cstar > 0 && s_need < s_ties) {
-      // radix select: the need-th smallest id among those with count == c*
-      uint32_t need = s_need, prefix = 0, pmask = 0;
-      for (int shift = 24; shift >= 0; shift -= 8) {
-        for (uint32_t d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
+
+    // ---- Q3b: threshold count c* and how many of its ties to keep (warp 0) ----
+    if (warp == 0) {
+      uint32_t cstar = 0, need = 0, ties = 0;
+      if (D > k) {
+        const uint32_t cs = (L + 31) / 32;  // counts per lane, lane 0 = highest counts
+        const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
+        const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
+        uint32_t sum = 0;
+        for (int32_t c = hi; c >= lo; --c) sum += hist[c];
+        uint32_t x = sum;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t before = x - sum;
+        const uint32_t hit = __ballot_sync(kFullMask, before < k && x >= k);
+        const uint32_t src = __ffs(hit) - 1;
+        if (lane == src) {
+          uint32_t cum = before;
+          for (int32_t c = hi; c >= lo; --c) {
+            if (cum + hist[c] >= k) {
+              cstar = (uint32_t)c;
+              need = k - cum;
+              ties = hist[c];
+              break;
+            }
+            cum += hist[c];
+          }
+        }
+        cstar = __shfl_sync(kFullMask, cstar, src);
+        need = __shfl_sync(kFullMask, need, src);
+        ties = __shfl_sync(kFullMask, ties, src);
+      }
+      if (lane == 0) {
+        sh.cstar = cstar;
+        sh.need = need;
+        sh.ties = ties;
+        sh.theta = 0xFFFFFFFFu;
+        sh.nout = 0;
+        sh.done = 0;
+        sh.prefix = 0;
+      }
+    }
+    __syncthreads();
+    const uint32_t cstar = sh.cstar;
+
+    // ---- Q3c: the need-th smallest id among those tied at c* ----
+    if (cstar > 0 && sh.need < sh.ties) {
+      const uint32_t hb = 31 - __clz(sh.maxid | 1u);
+      int32_t shift = (int32_t)hb - 7 > 0 ? (int32_t)hb - 7 : 0;
+      uint32_t width = hb + 1 - (uint32_t)shift;
+      uint32_t pmask = 0;
+      while (true) {
+        for (uint32_t d = tid; d < 256; d += NT) hist[d] = 0;
         __syncthreads();
-        for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
+        const uint32_t prefix = sh.prefix;
+        const uint32_t dmask = (1u << width) - 1;
+        for (uint32_t j = tid; j < D; j += NT) {
           const uint32_t slot = list[j];
           const uint32_t id = keys[slot];
-          if (get_count(cnt32, slot) == cstar && (id & pmask) == prefix)
-            atomicAdd(&hist[(id >> shift) & 255u], 1u);
+          if (cnt[slot] == cstar && (id & pmask) == prefix) atomicAdd(&hist[(id >> shift) & dmask], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-          uint32_t cum = 0, d = 0;
-          for (; d < 255; ++d) {
-            if (cum + hist[d] >= need) break;
-            cum += hist[d];
+        if (warp == 0) {
+          uint32_t sum = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sum += hist[lane * 8 + i];
+          uint32_t x = sum;
+#pragma unroll
+          for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
           }
-          s_need = need - cum;
-          s_prefix = prefix | (d << shift);
+          const uint32_t need = sh.need;
+          const uint32_t before = x - sum;
+          const uint32_t hit = __ballot_sync(kFullMask, before < need && x >= need);
+          const uint32_t src = __ffs(hit) - 1;
+          if (lane == src) {
+            uint32_t cum = before, d = lane * 8;
+            for (int i = 0; i < 8; ++i, ++d) {
+              if (cum + hist[d] >= need) break;
+              cum += hist[d];
+            }
+            const uint32_t rem = need - cum;
+            const uint32_t np = prefix | (d << shift);
+            sh.need = rem;
+            sh.prefix = np;
+            if (hist[d] == rem || shift == 0) {  // take this digit bucket whole / last digit
+              sh.theta = np | ((1u << shift) - 1u);
+              sh.done = 1;
+            }
+          }
         }
         __syncthreads();
-        need = s_need;
-        prefix = s_prefix;
-        pmask |= 255u << shift;
-        __syncthreads();
+        if (sh.done) break;
+        pmask |= ((1u << width) - 1u) << shift;
+        width = shift >= 8 ? 8u : (uint32_t)shift;
+        shift -= (int32_t)width;
       }
-      if (threadIdx.x == 0) s_theta = prefix;
+    }
+    const uint32_t theta = sh.theta;
+
+    // ---- Q3d: collect <= k survivors, place them by rank ----
+    for (uint32_t j0 = warp * 32; j0 < D; j0 += NT) {
+      const uint32_t j = j0 + lane;
+      bool keep = false;
+      uint64_t key = 0;
+      if (j < D) {
+        const uint32_t slot = list[j];
+        const uint32_t c = cnt[slot];
+        const uint32_t id = keys[slot];
+        keep = c > cstar || (c == cstar && id <= theta);
+        key = ((uint64_t)(0xFFFFu - c) << 32) | id;
+      }
+      const uint32_t m = __ballot_sync(kFullMask, keep);
+      if (m) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&sh.nout, __popc(m));
+        b = __shfl_sync(kFullMask, b, 0);
+        if (keep) outbuf[b + __popc(m & lanemask_lt_q())] = key;
+      }
+    }
+    __syncthreads();
+    const uint32_t nout = sh.nout;
+    uint32_t* oid = a.out_ids + q * k;
+    uint32_t* ocnt = a.out_counts + q * k;
+    if (kp2 <= 256) {
+      for (uint32_t j = tid; j < nout; j += NT) {
+        const uint64_t key = outbuf[j];
+        uint32_t rank = 0;
+        for (uint32_t i = 0; i < nout; ++i) rank += outbuf[i] < key;
+        oid[rank] = (uint32_t)key;
+        ocnt[rank] = 0xFFFFu - (uint32_t)(key >> 32);
+      }
+    } else {
+      for (uint32_t j = nout + tid; j < kp2; j += NT) outbuf[j] = ~0ull;
       __syncthreads();
+      for (uint32_t kk = 2; kk <= kp2; kk <<= 1) {
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t p = tid; p < (kp2 >> 1); p += NT) {
+            const uint32_t i = ((p & ~(jj - 1)) << 1) | (p & (jj - 1));
+            const uint64_t x = outbuf[i], y = outbuf[i + jj];
+            if ((x > y) == ((i & kk) == 0)) {
+              outbuf[i] = y;
+              outbuf[i + jj] = x;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (uint32_t j = tid; j < nout; j += NT) {
+        const uint64_t key = outbuf[j];
+        oid[j] = (uint32_t)key;
+        ocnt[j] = 0xFFFFu - (uint32_t)(key >> 32);
+      }
     }
-    const uint32_t theta = s_theta;
+    for (uint32_t j = nout + tid; j < k; j += NT) {
+      oid[j] = kEmpty;
+      ocnt[j] = 0;
+    }
 
-    // ---- collect <= k survivors, sort by (count desc, id asc) ----
-    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
-      const uint32_t slot = list[j];
-      const uint32_t c = get_count(cnt32, slot);
-      const uint32_t id = keys[slot];
-      if (c > cstar || (c == cstar && id <= theta))
-        outbuf[atomicAdd(&s_nout, 1u)] = ((uint64_t)(0xFFFFu - c) << 32) | id;
-    }
-    __syncthreads();
-    const uint32_t nout = s_nout;
-    for (uint32_t j = nout + threadIdx.x; j < kp2; j += blockDim.x) outbuf[j] = ~0ull;
-    __syncthreads();
-    cta_bitonic(outbuf, kp2);
-    for (uint32_t j = threadIdx.x; j < a.k; j += blockDim.x) {
-      const uint64_t key = outbuf[j];
-      const bool ok = j < nout;
-      a.out_ids[q * a.k + j] = ok ? (uint32_t)key : kEmpty;
-      a.out_counts[q * a.k + j] = ok ? 0xFFFFu - (uint32_t)(key >> 32) : 0u;
-    }
-
-    // ---- reset the touched state for the next query ----
-    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
+    // ---- reset the touched state ----
+    for (uint32_t j = tid; j < D; j += NT) {
       const uint32_t slot = list[j];
       keys[slot] = kEmpty;
-      reinterpret_cast<uint16_t*>(cnt32)[slot] = 0;
+      cnt[slot] = 0;
     }
-    for (uint32_t j = threadIdx.x; j < hist_len; j += blockDim.x) hist[j] = 0;
-    if (threadIdx.x == 0) s_nlist = 0;
+    for (uint32_t j = tid; j < hist_len; j += NT) hist[j] = 0;
     __syncthreads();
+    if (tid == 0) {
+      sh.nlist = 0;
+      sh.maxid = 0;
+    }
   }
+}
+
+size_t class_smem(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
+  uint32_t kp2 = 1;
+  while (kp2 < k) kp2 <<= 1;
+  const size_t S = (size_t)1 << log2s;
+  return (size_t)kp2 * 8 + (size_t)L * 8 + S * 4 + (size_t)(L + 1) * 4 + (size_t)hist_len * 4 + S * 2 + S * 2;
+}
+
+template <int LOG2S, int NT>
+int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t hist_len,
+                 cudaStream_t s) {
+  const size_t smem = class_smem(LOG2S, a.L, a.k, hist_len);
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_query<LOG2S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return 0;
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<LOG2S, NT>, NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = 148ull * per_sm;
+  if (grid > a.nq) grid = a.nq;
+  k_query<LOG2S, NT><<<(unsigned)grid, NT, smem, s>>>(a, list, count, hist_len);
+  return 1;
 }
 
 }  // namespace
 
 uint32_t query_table_log2(uint32_t L, uint32_t R) {
-  // >= 2x the maximal number of distinct candidates (load factor <= 1/2), >= 2^10
-  uint64_t need = 2ull * L * R;
-  uint32_t lg = 10;
+  uint64_t need = 2ull * L * R;  // worst case: every candidate distinct, load factor 1/2
+  uint32_t lg = 11;
   while ((1ull << lg) < need) ++lg;
   return lg;
 }
 
-size_t query_smem_bytes(uint32_t table_log2, uint32_t k) {
-  const size_t S = (size_t)1 << table_log2;
-  uint32_t kp2 = 1;
-  while (kp2 < k) kp2 <<= 1;
-  return kp2 * 8 + S * 4 + S * 2 + S * 4 + 0;  // hist appended separately
+size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k) {
+  const uint32_t hist_len = (L + 1) > 256 ? L + 1 : 256;
+  const uint32_t lg = table_log2 < 11 ? 11 : table_log2;
+  return class_smem(lg, L, k, hist_len);
 }
 
-int launch_query(const QueryArgs& a, cudaStream_t s) {
+size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * kClasses + kClasses); }
+
+int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (a.nq == 0) return 0;
+  uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
+  uint32_t* counts = lists + a.nq * kClasses;
+  cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kClasses, s);
+  const uint64_t warps = (a.nq + 31) / 32;
+  uint64_t blocks = (warps + 7) / 8;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, lists, counts, a.err);
   const uint32_t hist_len = (a.L + 1) > 256 ? a.L + 1 : 256;
-  const size_t smem = query_smem_bytes(a.table_log2, a.k) + hist_len * 4;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return 0;  // the launch below then fails and the caller reports it
-    attr = smem;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kQThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = 148ull * per_sm;
-  if (grid > a.nq) grid = a.nq;
-  k_query<<<(unsigned)grid, kQThreads, smem, s>>>(a, hist_len);
-  return 1;
+  int n = 1;
+  n += launch_class<11, 128>(a, lists, counts + 0, hist_len, s);
+  if (a.table_log2 >= 12) n += launch_class<13, 256>(a, lists + a.nq, counts + 1, hist_len, s);
+  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 2 * a.nq, counts + 2, hist_len, s);
+  return n;
 }
 
 }  // namespace flash
