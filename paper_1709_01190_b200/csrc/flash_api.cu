@@ -98,6 +98,7 @@ struct flash_index {
   bool have_tables = false;
   uint64_t kept_ub = 0;     // host upper bound on kept ids
   uint64_t n_inserted = 0;  // rows passed to insert (host count)
+  uint64_t max_id = 0;      // largest id inserted so far (host count)
   // scratch
   DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
@@ -230,6 +231,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   h->have_tables = true;
   h->kept_ub = kept_cap;
   h->n_inserted += n;
+  if ((uint64_t)id_base + n - 1 > h->max_id) h->max_id = (uint64_t)id_base + n - 1;
   return FLASH_OK;
 }
 
@@ -260,6 +262,7 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   a.out_counts = out_counts;
   a.err = h->err;
   a.table_log2 = h->table_log2;
+  a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
   h->launches += launch_query(a, h->qscratch.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
@@ -522,6 +525,7 @@ flash_status flash_clear(flash_index* h, void* stream) {
   h->have_tables = false;
   h->kept_ub = 0;
   h->n_inserted = 0;
+  h->max_id = 0;
   return FLASH_OK;
 }
 

@@ -113,6 +113,7 @@ struct QueryArgs {
   uint32_t* out_counts;
   unsigned long long* err;
   uint32_t table_log2;      // worst-case count-table slots = 2^table_log2 (from L*R)
+  int packed;               // every inserted id < 2^24-1 and L <= 255: u32 (id, count) entries
 };
 // scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
 int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s);

@@ -5,9 +5,10 @@
 //   load factor <= 1/2), so most queries run with a small shared-memory footprint and
 //   many CTAs per SM.
 // k_query<LOG2S, NT>: one CTA owns one query at a time (persistent over its class list):
-//   Q1 gather   warp 0 scans the L bucket sizes into prefix offsets; every thread then
-//               walks flattened candidate positions p (binary search of the owning table,
-//               4 loads in flight per thread), reading ids[goff[t*range+a_t] + ...].
+//   Q1 gather   warp 0 scans the L bucket sizes into prefix offsets; each warp then walks
+//               its own contiguous chunk of the flattened candidate positions p (4 loads in
+//               flight per lane, table index advanced monotonically), reading
+//               ids[goff[t*range+a_t] + ...].
 //   Q2 count    each id goes into a shared-memory open-addressing table (u32 keys, u16
 //               counts updated through their u32 word): CAS on a new key, RED.ADD on its
 //               count; new slots are appended (warp-aggregated) to a list so later passes
@@ -15,10 +16,11 @@
 //               R#11).  The excluded id (self in the k-NN graph, R#14) is skipped.
 //   Q3 top-k    counts are <= L: a count histogram gives the threshold count c* (warp-
 //               parallel suffix search); the ids tied at c* are cut at the need-th smallest
-//               id by an 8-bit radix select starting at the top set bit of the largest
-//               candidate id, stopping as soon as a digit bucket is taken whole (ties by
-//               ascending id, R#12).  The <= k survivors are placed by rank (count desc,
-//               id asc) and written, padded with (EMPTY, 0) (R#13).
+//               id by a radix select (digits of <= 10 bits from the top set bit of the
+//               largest candidate id), stopping as soon as a digit bucket is taken whole
+//               (ties by ascending id, R#12).  The <= k survivors are sorted by (count desc,
+//               id asc) in one warp's registers (bitonic) and written, padded with
+//               (EMPTY, 0) (R#13).  The collect pass also resets the touched table slots.
 #include "flash_internal.cuh"
 
 namespace flash {
@@ -35,8 +37,10 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
   return m;
 }
 
-// Query size classes: count-table slots 2^11, 2^13, 2^14 for M <= 1024, 4096, 8192.
-constexpr int kClasses = 3;
+// Query size classes by M (candidates): <= 1536 and <= 3072 run one query per warp with
+// 2^11 / 2^12 count slots (load <= 3/4); <= 4096 and <= 8192 one query per CTA with
+// 2^13 / 2^14 slots (the CTA kernels also serve k > 256).
+constexpr int kClasses = 4;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              uint32_t L, uint32_t range, uint32_t* __restrict__ lists,
@@ -57,7 +61,7 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
         }
       }
     }
-    const int cls = M <= 1024 ? 0 : (M <= 4096 ? 1 : 2);
+    const int cls = M <= 1536 ? 0 : (M <= 3072 ? 1 : (M <= 4096 ? 2 : 3));
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) {
       const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
@@ -68,6 +72,67 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
       if ((m >> lane) & 1) lists[(uint64_t)c * nq + b + __popc(m & lanemask_lt_q())] = (uint32_t)q;
     }
   }
+}
+
+// Sort KP*32 keys (outbuf[0..nout), padded with ~0) ascending in registers of one warp
+// (element e = r*32 + lane) and write the first nout as (id, count).
+template <int KP>
+__device__ __forceinline__ void warp_sort_out(const uint64_t* outbuf, uint32_t nout, uint32_t* oid,
+                                              uint32_t* ocnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  constexpr uint32_t n = KP * 32;
+  uint64_t v[KP];
+#pragma unroll
+  for (int r = 0; r < KP; ++r) {
+    const uint32_t e = r * 32 + lane;
+    v[r] = e < nout ? outbuf[e] : ~0ull;
+  }
+#pragma unroll
+  for (uint32_t kk = 2; kk <= n; kk <<= 1) {
+#pragma unroll
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const uint32_t rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < KP; ++r) {
+          if ((r & rj) == 0) {
+            const uint32_t e = r * 32 + lane;
+            const bool up = (e & kk) == 0;
+            const uint64_t x = v[r], y = v[r | rj];
+            if ((x > y) == up) {
+              v[r] = y;
+              v[r | rj] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < KP; ++r) {
+          const uint32_t e = r * 32 + lane;
+          const uint64_t other = __shfl_xor_sync(kFullMask, v[r], j);
+          const bool up = (e & kk) == 0;
+          const bool lower = (lane & j) == 0;
+          v[r] = (lower == up) ? (v[r] < other ? v[r] : other) : (v[r] > other ? v[r] : other);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < KP; ++r) {
+    const uint32_t e = r * 32 + lane;
+    if (e < nout) {
+      oid[e] = (uint32_t)v[r];
+      ocnt[e] = 0xFFFFu - (uint32_t)(v[r] >> 32);
+    }
+  }
+}
+
+__host__ __device__ inline size_t warp_slice_bytes(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
+  uint32_t kp2 = 1;
+  while (kp2 < k) kp2 <<= 1;
+  const size_t S = (size_t)1 << log2s;
+  size_t b = (size_t)kp2 * 8 + (size_t)L * 8 + S * 4 + (size_t)(L + 1) * 4 + (size_t)hist_len * 4 + S * 2 + S * 2;
+  return (b + 15) & ~(size_t)15;
 }
 
 struct QueryShared {
@@ -143,52 +208,65 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
     __syncthreads();
     const uint32_t M = sh.M;
 
-    // ---- Q2: gather + count ----
+    // ---- Q2: gather + count; warp w walks its own contiguous chunk of the M positions,
+    //      4 x 32 positions per step, advancing each lane's table index monotonically ----
     uint32_t mymax = 0;
-    for (uint32_t p0 = warp * 32; p0 < M; p0 += 4 * NT) {
-      uint32_t idv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t p = p0 + u * NT + lane;
-        idv[u] = kEmpty;
-        if (p < M) {
-          uint32_t lo = 0, hi = L - 1;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (pref[mid] <= p) lo = mid; else hi = mid - 1;
-          }
-          idv[u] = a.ids[base[lo] + p];
+    {
+      constexpr uint32_t NWARP = NT / 32;
+      const uint32_t chunk = ((M + NWARP * 128 - 1) / (NWARP * 128)) * 128;
+      const uint32_t pbeg = warp * chunk;
+      const uint32_t pend = M < pbeg + chunk ? M : pbeg + chunk;
+      uint32_t t = 0;
+      if (pbeg + lane < pend) {
+        const uint32_t p = pbeg + lane;
+        uint32_t lo = 0, hi = L - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (pref[mid] <= p) lo = mid; else hi = mid - 1;
         }
+        t = lo;
       }
+      for (uint32_t p0 = pbeg; p0 < pend; p0 += 128) {
+        uint32_t idv[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t id = idv[u];
-        uint32_t newslot = 0xFFFFFFFFu;
-        if (id != kEmpty && id != excl) {
-          mymax = id > mymax ? id : mymax;
-          uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
-          while (true) {
-            uint32_t cur = keys[slot];
-            if (cur == kEmpty) {
-              cur = atomicCAS(&keys[slot], kEmpty, id);
-              if (cur == kEmpty) {
-                newslot = slot;
-                cur = id;
-              }
-            }
-            if (cur == id) {
-              atomicAdd(&cnt32[slot >> 1], 1u << ((slot & 1) * 16));
-              break;
-            }
-            slot = (slot + 1) & MASK;
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t p = p0 + u * 32 + lane;
+          idv[u] = kEmpty;
+          if (p < pend) {
+            while (pref[t + 1] <= p) ++t;
+            idv[u] = a.ids[base[t] + p];
           }
         }
-        const uint32_t m = __ballot_sync(kFullMask, newslot != 0xFFFFFFFFu);
-        if (m) {
-          uint32_t b = 0;
-          if (lane == 0) b = atomicAdd(&sh.nlist, __popc(m));
-          b = __shfl_sync(kFullMask, b, 0);
-          if (newslot != 0xFFFFFFFFu) list[b + __popc(m & lanemask_lt_q())] = (uint16_t)newslot;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          uint32_t newslot = 0xFFFFFFFFu;
+          if (id != kEmpty && id != excl) {
+            mymax = id > mymax ? id : mymax;
+            uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
+            while (true) {
+              uint32_t cur = keys[slot];
+              if (cur == kEmpty) {
+                cur = atomicCAS(&keys[slot], kEmpty, id);
+                if (cur == kEmpty) {
+                  newslot = slot;
+                  cur = id;
+                }
+              }
+              if (cur == id) {
+                atomicAdd(&cnt32[slot >> 1], 1u << ((slot & 1) * 16));
+                break;
+              }
+              slot = (slot + 1) & MASK;
+            }
+          }
+          const uint32_t m = __ballot_sync(kFullMask, newslot != 0xFFFFFFFFu);
+          if (m) {
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(&sh.nlist, __popc(m));
+            b = __shfl_sync(kFullMask, b, 0);
+            if (newslot != 0xFFFFFFFFu) list[b + __popc(m & lanemask_lt_q())] = (uint16_t)newslot;
+          }
         }
       }
     }
@@ -259,17 +337,19 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
     __syncthreads();
     const uint32_t cstar = sh.cstar;
 
-    // ---- Q3c: the need-th smallest id among those tied at c* ----
+    // ---- Q3c: the need-th smallest id among those tied at c* (radix select, digits of
+    //      up to 10 bits from the top set bit; stops when a digit bucket is taken whole) ----
     if (cstar > 0 && sh.need < sh.ties) {
       const uint32_t hb = 31 - __clz(sh.maxid | 1u);
-      int32_t shift = (int32_t)hb - 7 > 0 ? (int32_t)hb - 7 : 0;
-      uint32_t width = hb + 1 - (uint32_t)shift;
+      uint32_t width = hb + 1 < 10 ? hb + 1 : 10;
+      int32_t shift = (int32_t)(hb + 1 - width);
       uint32_t pmask = 0;
       while (true) {
-        for (uint32_t d = tid; d < 256; d += NT) hist[d] = 0;
+        const uint32_t nbins = 1u << width;
+        const uint32_t dmask = nbins - 1;
+        for (uint32_t d = tid; d < nbins; d += NT) hist[d] = 0;
         __syncthreads();
         const uint32_t prefix = sh.prefix;
-        const uint32_t dmask = (1u << width) - 1;
         for (uint32_t j = tid; j < D; j += NT) {
           const uint32_t slot = list[j];
           const uint32_t id = keys[slot];
@@ -277,9 +357,11 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         }
         __syncthreads();
         if (warp == 0) {
+          const uint32_t per = (nbins + 31) >> 5;
+          const uint32_t d0 = lane * per < nbins ? lane * per : nbins;
+          const uint32_t d1 = d0 + per < nbins ? d0 + per : nbins;
           uint32_t sum = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) sum += hist[lane * 8 + i];
+          for (uint32_t d = d0; d < d1; ++d) sum += hist[d];
           uint32_t x = sum;
 #pragma unroll
           for (uint32_t o = 1; o < 32; o <<= 1) {
@@ -291,8 +373,8 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
           const uint32_t hit = __ballot_sync(kFullMask, before < need && x >= need);
           const uint32_t src = __ffs(hit) - 1;
           if (lane == src) {
-            uint32_t cum = before, d = lane * 8;
-            for (int i = 0; i < 8; ++i, ++d) {
+            uint32_t cum = before, d = d0;
+            for (; d + 1 < d1; ++d) {
               if (cum + hist[d] >= need) break;
               cum += hist[d];
             }
@@ -308,14 +390,14 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         }
         __syncthreads();
         if (sh.done) break;
-        pmask |= ((1u << width) - 1u) << shift;
-        width = shift >= 8 ? 8u : (uint32_t)shift;
+        pmask |= dmask << shift;
+        width = shift >= 10 ? 10u : (uint32_t)shift;
         shift -= (int32_t)width;
       }
     }
     const uint32_t theta = sh.theta;
 
-    // ---- Q3d: collect <= k survivors, place them by rank ----
+    // ---- Q3d: collect <= k survivors (and reset the touched table state) ----
     for (uint32_t j0 = warp * 32; j0 < D; j0 += NT) {
       const uint32_t j = j0 + lane;
       bool keep = false;
@@ -326,6 +408,8 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         const uint32_t id = keys[slot];
         keep = c > cstar || (c == cstar && id <= theta);
         key = ((uint64_t)(0xFFFFu - c) << 32) | id;
+        keys[slot] = kEmpty;
+        cnt[slot] = 0;
       }
       const uint32_t m = __ballot_sync(kFullMask, keep);
       if (m) {
@@ -335,17 +419,18 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         if (keep) outbuf[b + __popc(m & lanemask_lt_q())] = key;
       }
     }
+    for (uint32_t j = tid; j < hist_len; j += NT) hist[j] = 0;
     __syncthreads();
     const uint32_t nout = sh.nout;
     uint32_t* oid = a.out_ids + q * k;
     uint32_t* ocnt = a.out_counts + q * k;
+    // ---- Q3e: order by (count desc, id asc): one warp, keys in registers ----
     if (kp2 <= 256) {
-      for (uint32_t j = tid; j < nout; j += NT) {
-        const uint64_t key = outbuf[j];
-        uint32_t rank = 0;
-        for (uint32_t i = 0; i < nout; ++i) rank += outbuf[i] < key;
-        oid[rank] = (uint32_t)key;
-        ocnt[rank] = 0xFFFFu - (uint32_t)(key >> 32);
+      if (warp == 0) {
+        if (kp2 <= 32) warp_sort_out<1>(outbuf, nout, oid, ocnt);
+        else if (kp2 == 64) warp_sort_out<2>(outbuf, nout, oid, ocnt);
+        else if (kp2 == 128) warp_sort_out<4>(outbuf, nout, oid, ocnt);
+        else warp_sort_out<8>(outbuf, nout, oid, ocnt);
       }
     } else {
       for (uint32_t j = nout + tid; j < kp2; j += NT) outbuf[j] = ~0ull;
@@ -373,19 +458,378 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
       oid[j] = kEmpty;
       ocnt[j] = 0;
     }
-
-    // ---- reset the touched state ----
-    for (uint32_t j = tid; j < D; j += NT) {
-      const uint32_t slot = list[j];
-      keys[slot] = kEmpty;
-      cnt[slot] = 0;
-    }
-    for (uint32_t j = tid; j < hist_len; j += NT) hist[j] = 0;
     __syncthreads();
     if (tid == 0) {
       sh.nlist = 0;
       sh.maxid = 0;
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Warp-per-query path (k <= 256): one warp owns one query at a time, no CTA barriers.
+// Count table entries pack (id, count) in one word: u32 = id<<8 | count when every id
+// is < 2^24-1 and L <= 255 (webspam, url, tiny), else u64 = id<<32 | count.  The table
+// is scanned directly (vector loads) instead of keeping a distinct-slot list, which
+// keeps the per-warp footprint at ~S words so ~20 warps fit per SM.
+// ---------------------------------------------------------------------------
+template <typename E>
+struct Ent;
+template <>
+struct Ent<uint32_t> {
+  using V = uint4;  // 4 entries per vector load
+  static constexpr int kPerVec = 4;
+  static constexpr uint32_t kE = 0xFFFFFFFFu;
+  __device__ static uint32_t make(uint32_t id) { return (id << 8) | 1u; }
+  __device__ static uint32_t id(uint32_t e) { return e >> 8; }
+  __device__ static uint32_t count(uint32_t e) { return e & 0xFFu; }
+  __device__ static uint32_t key(uint32_t e) { return ((255u - (e & 0xFFu)) << 24) | (e >> 8); }
+  __device__ static uint32_t key_id(uint32_t k) { return k & 0xFFFFFFu; }
+  __device__ static uint32_t key_count(uint32_t k) { return 255u - (k >> 24); }
+  __device__ static void get(const V& v, uint32_t* e) { e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w; }
+  __device__ static V empty_vec() { return make_uint4(kE, kE, kE, kE); }
+};
+template <>
+struct Ent<unsigned long long> {
+  using V = ulonglong2;
+  static constexpr int kPerVec = 2;
+  static constexpr unsigned long long kE = ~0ull;
+  __device__ static unsigned long long make(uint32_t id) { return ((unsigned long long)id << 32) | 1ull; }
+  __device__ static uint32_t id(unsigned long long e) { return (uint32_t)(e >> 32); }
+  __device__ static uint32_t count(unsigned long long e) { return (uint32_t)e; }
+  __device__ static unsigned long long key(unsigned long long e) {
+    return ((unsigned long long)(0xFFFFu - (uint32_t)e) << 32) | (e >> 32);
+  }
+  __device__ static uint32_t key_id(unsigned long long k) { return (uint32_t)k; }
+  __device__ static uint32_t key_count(unsigned long long k) { return 0xFFFFu - (uint32_t)(k >> 32); }
+  __device__ static void get(const V& v, unsigned long long* e) { e[0] = v.x; e[1] = v.y; }
+  __device__ static V empty_vec() { return make_ulonglong2(kE, kE); }
+};
+
+// Sort KP*32 keys (buf[0..n), padded with ~0) ascending in one warp's registers
+// (element e = r*32 + lane) and write the first n as (id, count).
+template <int KP, typename E>
+__device__ __forceinline__ void warp_sort_keys(const E* buf, uint32_t n, uint32_t* oid, uint32_t* ocnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  constexpr uint32_t N = KP * 32;
+  E v[KP];
+#pragma unroll
+  for (int r = 0; r < KP; ++r) {
+    const uint32_t e = r * 32 + lane;
+    v[r] = e < n ? buf[e] : (E)~(E)0;
+  }
+#pragma unroll
+  for (uint32_t kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const uint32_t rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < KP; ++r) {
+          if ((r & rj) == 0) {
+            const bool up = ((r * 32 + lane) & kk) == 0;
+            const E x = v[r], y = v[r | rj];
+            if ((x > y) == up) {
+              v[r] = y;
+              v[r | rj] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < KP; ++r) {
+          const E other = __shfl_xor_sync(kFullMask, v[r], j);
+          const bool keep_min = (((r * 32 + lane) & kk) == 0) == ((lane & j) == 0);
+          v[r] = keep_min ? (v[r] < other ? v[r] : other) : (v[r] > other ? v[r] : other);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < KP; ++r) {
+    const uint32_t e = r * 32 + lane;
+    if (e < n) {
+      oid[e] = Ent<E>::key_id(v[r]);
+      ocnt[e] = Ent<E>::key_count(v[r]);
+    }
+  }
+}
+
+__host__ __device__ inline size_t warp2_slice_bytes(uint32_t log2s, uint32_t entry_bytes, uint32_t L, uint32_t k) {
+  uint32_t kp2 = 32;
+  while (kp2 < k) kp2 <<= 1;
+  const size_t S = (size_t)1 << log2s;
+  size_t b = S * entry_bytes + (size_t)kp2 * entry_bytes + (size_t)L * 8 + (size_t)(L + 1) * 4 +
+             (size_t)(L + 1) * 4 + 256 * 4;
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int LOG2S, typename E>
+__global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t* __restrict__ qlist,
+                                                   const uint32_t* __restrict__ qcount) {
+  using T = Ent<E>;
+  using V = typename T::V;
+  constexpr uint32_t S = 1u << LOG2S;
+  constexpr uint32_t MASK = S - 1;
+  constexpr uint32_t NV = S / T::kPerVec;  // vectors per table
+  extern __shared__ __align__(16) uint8_t smw[];
+  const uint32_t L = a.L, k = a.k;
+  uint32_t kp2 = 32;
+  while (kp2 < k) kp2 <<= 1;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* my = smw + warp2_slice_bytes(LOG2S, sizeof(E), L, k) * wib;
+  E* tab = reinterpret_cast<E*>(my);                            // [S] count table
+  uint32_t* tie = reinterpret_cast<uint32_t*>(my);              // tie ids, compacted over tab
+  E* outbuf = tab + S;                                           // [kp2]
+  uint64_t* base = reinterpret_cast<uint64_t*>(outbuf + kp2);   // [L]
+  uint32_t* pref = reinterpret_cast<uint32_t*>(base + L);       // [L+1]
+  uint32_t* hcnt = pref + L + 1;                                 // [L+1] count histogram
+  uint32_t* hrad = hcnt + L + 1;                                 // [256] radix digits
+  V* tabv = reinterpret_cast<V*>(tab);
+
+  for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
+  for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+  __syncwarp();
+
+  const uint32_t nq = *qcount;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t it = gw; it < nq; it += nw) {
+    const uint64_t q = qlist[it];
+    const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
+
+    // ---- Q1: bucket segments -> prefix offsets ----
+    uint32_t M = 0;
+    for (uint32_t t0 = 0; t0 < L; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      uint32_t sz = 0;
+      uint64_t st = 0;
+      if (t < L) {
+        const uint32_t ad = a.addrs[q * L + t];
+        if (ad < a.range) {
+          const uint64_t i = (uint64_t)t * a.range + ad;
+          st = a.goff[i];
+          sz = (uint32_t)(a.goff[i + 1] - st);
+        }
+      }
+      uint32_t x = sz;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+      }
+      if (t < L) {
+        pref[t] = M + x - sz;
+        base[t] = st - (M + x - sz);
+      }
+      M += __shfl_sync(kFullMask, x, 31);
+    }
+    if (lane == 0) pref[L] = M;
+    __syncwarp();
+
+    // ---- Q2: gather + count, keeping the count histogram current.  Positions p0+lane
+    //      of a 32-wide round belong to table tcur + #{table starts in (p0, p]}: the
+    //      starts inside the round come from one ballot. ----
+    uint32_t tcur = 0, mymax = 0, D = 0;
+    for (uint32_t p0 = 0; p0 < M; p0 += 128) {
+      uint32_t idv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r0 = p0 + u * 32;
+        const uint32_t p = r0 + lane;
+        idv[u] = kEmpty;
+        if (r0 < M) {
+          while (pref[tcur + 1] <= r0) ++tcur;  // warp-uniform; usually 0-1 steps
+          const uint32_t tj = tcur + 1 + lane;
+          const uint32_t bj = tj <= L ? pref[tj] : 0xFFFFFFFFu;
+          const uint32_t inround = __ballot_sync(kFullMask, bj < r0 + 32);
+          uint32_t t = tcur;
+          if (inround == kFullMask) {  // > 31 table starts in one round (many empty buckets)
+            while (p < M && pref[t + 1] <= p) ++t;
+          } else {
+            uint32_t mbits = inround;
+            while (mbits) {
+              const uint32_t j = __ffs(mbits) - 1;
+              mbits &= mbits - 1;
+              t += __shfl_sync(kFullMask, bj, j) <= p;
+            }
+          }
+          if (p < M) idv[u] = a.ids[base[t] + p];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t id = idv[u];
+        bool fresh = false;
+        if (id != kEmpty && id != excl) {
+          mymax = id > mymax ? id : mymax;
+          uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
+          while (true) {
+            E cur = tab[slot];
+            if (cur == T::kE) {
+              cur = atomicCAS(&tab[slot], T::kE, T::make(id));
+              if (cur == T::kE) {
+                fresh = true;
+                break;
+              }
+            }
+            if (T::id(cur) == id) {
+              const uint32_t c = T::count(atomicAdd(&tab[slot], (E)1));  // c -> c+1
+              atomicSub(&hcnt[c < L ? c : L], 1u);
+              atomicAdd(&hcnt[c + 1 < L ? c + 1 : L], 1u);
+              break;
+            }
+            slot = (slot + 1) & MASK;
+          }
+        }
+        const uint32_t nf = __popc(__ballot_sync(kFullMask, fresh));
+        if (lane == 0 && nf) atomicAdd(&hcnt[1], nf);
+        D += nf;
+      }
+    }
+#pragma unroll
+    for (uint32_t o = 16; o > 0; o >>= 1) {
+      const uint32_t y = __shfl_xor_sync(kFullMask, mymax, o);
+      mymax = y > mymax ? y : mymax;
+    }
+    __syncwarp();
+
+    // ---- Q3a: threshold count c* from the histogram ----
+    uint32_t cstar = 0, need = 0, ties = 0;
+    if (D > k) {
+      const uint32_t cs = (L + 31) / 32;
+      const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
+      const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
+      uint32_t sum = 0;
+      for (int32_t c = hi; c >= lo; --c) sum += hcnt[c];
+      uint32_t x = sum;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t before = x - sum;
+      const uint32_t hit = __ballot_sync(kFullMask, before < k && x >= k);
+      const uint32_t src = __ffs(hit) - 1;
+      if (lane == src) {
+        uint32_t cum = before;
+        for (int32_t c = hi; c >= lo; --c) {
+          if (cum + hcnt[c] >= k) {
+            cstar = (uint32_t)c;
+            need = k - cum;
+            ties = hcnt[c];
+            break;
+          }
+          cum += hcnt[c];
+        }
+      }
+      cstar = __shfl_sync(kFullMask, cstar, src);
+      need = __shfl_sync(kFullMask, need, src);
+      ties = __shfl_sync(kFullMask, ties, src);
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+    const bool cut = cstar > 0 && need < ties;  // the c* ties must be cut by id
+
+    // ---- Q3b: one pass over the table: counts above c* (and all ties when no cut is
+    //      needed) go to the output buffer; the tied ids are compacted in place to the
+    //      front of the table (writes never pass the current read position) ----
+    uint32_t nout = 0, ntie = 0;
+    for (uint32_t v0 = 0; v0 < NV; v0 += 32) {
+      E e[T::kPerVec];
+      T::get(tabv[v0 + lane], e);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < T::kPerVec; ++i) {
+        const uint32_t c = e[i] != T::kE ? T::count(e[i]) : 0u;
+        const bool out = c > cstar || (c == cstar && c > 0 && !cut);
+        const bool tied = cut && c == cstar;
+        const uint32_t mo = __ballot_sync(kFullMask, out);
+        const uint32_t mt = __ballot_sync(kFullMask, tied);
+        if (out) outbuf[nout + __popc(mo & lanemask_lt_q())] = T::key(e[i]);
+        if (tied) tie[ntie + __popc(mt & lanemask_lt_q())] = T::id(e[i]);
+        nout += __popc(mo);
+        ntie += __popc(mt);
+      }
+    }
+    __syncwarp();
+
+    // ---- Q3c: keep the `need` smallest tied ids (radix select over the compacted ties,
+    //      8-bit digits from the top set bit, stops when a digit bucket is taken whole) ----
+    if (cut) {
+      const uint32_t hb = 31 - __clz(mymax | 1u);
+      uint32_t width = hb + 1 < 8 ? hb + 1 : 8;
+      int32_t shift = (int32_t)(hb + 1 - width);
+      uint32_t pmask = 0, prefix = 0, theta = 0;
+      while (true) {
+        for (uint32_t d = lane; d < 256; d += 32) hrad[d] = 0;
+        __syncwarp();
+        const uint32_t dmask = (1u << width) - 1;
+        for (uint32_t j = lane; j < ntie; j += 32) {
+          const uint32_t id = tie[j];
+          if ((id & pmask) == prefix) atomicAdd(&hrad[(id >> shift) & dmask], 1u);
+        }
+        __syncwarp();
+        uint32_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sum += hrad[lane * 8 + i];
+        uint32_t x = sum;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t before = x - sum;
+        const uint32_t hit = __ballot_sync(kFullMask, before < need && x >= need);
+        const uint32_t src = __ffs(hit) - 1;
+        uint32_t d = 0, cum = 0, hd = 0;
+        if (lane == src) {
+          cum = before;
+          d = lane * 8;
+          for (int i = 0; i < 7; ++i, ++d) {
+            if (cum + hrad[d] >= need) break;
+            cum += hrad[d];
+          }
+          hd = hrad[d];
+        }
+        d = __shfl_sync(kFullMask, d, src);
+        cum = __shfl_sync(kFullMask, cum, src);
+        hd = __shfl_sync(kFullMask, hd, src);
+        __syncwarp();
+        need -= cum;
+        prefix |= d << shift;
+        if (hd == need || shift == 0) {
+          theta = prefix | ((1u << shift) - 1u);
+          break;
+        }
+        pmask |= dmask << shift;
+        width = shift >= 8 ? 8u : (uint32_t)shift;
+        shift -= (int32_t)width;
+      }
+      for (uint32_t j0 = 0; j0 < ntie; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint32_t id = j < ntie ? tie[j] : 0xFFFFFFFFu;
+        const bool keep = j < ntie && id <= theta;
+        const uint32_t m = __ballot_sync(kFullMask, keep);
+        if (keep) outbuf[nout + __popc(m & lanemask_lt_q())] = T::key(T::make(id) - 1 + cstar);
+        nout += __popc(m);
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
+
+    // ---- Q3d: order by (count desc, id asc), write, pad ----
+    uint32_t* oid = a.out_ids + q * k;
+    uint32_t* ocnt = a.out_counts + q * k;
+    if (kp2 == 32) warp_sort_keys<1, E>(outbuf, nout, oid, ocnt);
+    else if (kp2 == 64) warp_sort_keys<2, E>(outbuf, nout, oid, ocnt);
+    else if (kp2 == 128) warp_sort_keys<4, E>(outbuf, nout, oid, ocnt);
+    else warp_sort_keys<8, E>(outbuf, nout, oid, ocnt);
+    for (uint32_t j = nout + lane; j < k; j += 32) {
+      oid[j] = kEmpty;
+      ocnt[j] = 0;
+    }
+    __syncwarp();
   }
 }
 
@@ -416,6 +860,27 @@ int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count
   return 1;
 }
 
+template <int LOG2S, typename E>
+int launch_warp_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+  constexpr int kWarps = 4;
+  const size_t smem = warp2_slice_bytes(LOG2S, sizeof(E), a.L, a.k) * kWarps;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_query_warp<LOG2S, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return 0;
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_warp<LOG2S, E>, 32 * kWarps, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = 148ull * per_sm;
+  const uint64_t need = (a.nq + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
+  k_query_warp<LOG2S, E><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count);
+  return 1;
+}
+
 }  // namespace
 
 uint32_t query_table_log2(uint32_t L, uint32_t R) {
@@ -426,7 +891,7 @@ uint32_t query_table_log2(uint32_t L, uint32_t R) {
 }
 
 size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k) {
-  const uint32_t hist_len = (L + 1) > 256 ? L + 1 : 256;
+  const uint32_t hist_len = (L + 1) > 1024 ? L + 1 : 1024;
   const uint32_t lg = table_log2 < 11 ? 11 : table_log2;
   return class_smem(lg, L, k, hist_len);
 }
@@ -442,11 +907,20 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   uint64_t blocks = (warps + 7) / 8;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, lists, counts, a.err);
-  const uint32_t hist_len = (a.L + 1) > 256 ? a.L + 1 : 256;
+  const uint32_t hist_len = (a.L + 1) > 1024 ? a.L + 1 : 1024;
   int n = 1;
-  n += launch_class<11, 128>(a, lists, counts + 0, hist_len, s);
-  if (a.table_log2 >= 12) n += launch_class<13, 256>(a, lists + a.nq, counts + 1, hist_len, s);
-  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 2 * a.nq, counts + 2, hist_len, s);
+  if (a.k <= 256 && a.packed) {  // one query per warp, (id, count) packed in u32
+    n += launch_warp_class<11, uint32_t>(a, lists, counts + 0, s);
+    if (a.table_log2 >= 12) n += launch_warp_class<12, uint32_t>(a, lists + a.nq, counts + 1, s);
+  } else if (a.k <= 256) {   // one query per warp, u64 entries
+    n += launch_warp_class<11, unsigned long long>(a, lists, counts + 0, s);
+    if (a.table_log2 >= 12) n += launch_warp_class<12, unsigned long long>(a, lists + a.nq, counts + 1, s);
+  } else {
+    n += launch_class<11, 128>(a, lists, counts + 0, hist_len, s);
+    if (a.table_log2 >= 12) n += launch_class<12, 128>(a, lists + a.nq, counts + 1, hist_len, s);
+  }
+  if (a.table_log2 >= 13) n += launch_class<13, 256>(a, lists + 2 * a.nq, counts + 2, hist_len, s);
+  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 3 * a.nq, counts + 3, hist_len, s);
   return n;
 }
 
