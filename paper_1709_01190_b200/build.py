@@ -16,7 +16,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 SO = os.path.join(PKG, "libflash.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["doph.cu", "build.cu", "query.cu", "flash_api.cu"]
+SOURCES = ["doph.cu", "build.cu", "query.cu", "query_merge.cu", "flash_api.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -31,6 +31,20 @@ def _stale(target: str, deps: list[str]) -> bool:
         return True
     t = os.path.getmtime(target)
     return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_variant(name: str, defines: list[str]) -> str:
+    """A diagnostic build (e.g. libflash_qprof.so with -DFLASH_QPROF); never loaded by the product."""
+    out = os.path.join(PKG, f"libflash_{name}.so")
+    objdir = os.path.join(ROOT, "build", f"obj_{name}")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
+        subprocess.check_call([NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", o])
+        objs.append(o)
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs])
+    return out
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -63,5 +77,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    if "--qprof" in sys.argv:
+        print(build_variant("qprof", ["FLASH_QPROF"]))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(SO)

@@ -28,6 +28,20 @@ namespace {
 
 constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
+#ifdef FLASH_QPROF  // phase-cycle instrumentation of k_query_warp (tools/qprof.py; never in the product build)
+__device__ unsigned long long g_qprof[8];
+#define QPROF_MARK(i)                                                   \
+  do {                                                                  \
+    const long long now_ = clock64();                                   \
+    if (lane == 0) atomicAdd(&g_qprof[i], (unsigned long long)(now_ - qp_last)); \
+    qp_last = now_;                                                     \
+  } while (0)
+#else
+#define QPROF_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t pow2_ceil_q(uint32_t x) {
   return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
 }
@@ -478,8 +492,9 @@ template <typename E>
 struct Ent;
 template <>
 struct Ent<uint32_t> {
-  using V = uint4;  // 4 entries per vector load
+  using V = uint4;  // 4 entries per vector load / hash group
   static constexpr int kPerVec = 4;
+  static constexpr int kLog2Per = 2;
   static constexpr uint32_t kE = 0xFFFFFFFFu;
   __device__ static uint32_t make(uint32_t id) { return (id << 8) | 1u; }
   __device__ static uint32_t id(uint32_t e) { return e >> 8; }
@@ -494,6 +509,7 @@ template <>
 struct Ent<unsigned long long> {
   using V = ulonglong2;
   static constexpr int kPerVec = 2;
+  static constexpr int kLog2Per = 1;
   static constexpr unsigned long long kE = ~0ull;
   __device__ static unsigned long long make(uint32_t id) { return ((unsigned long long)id << 32) | 1ull; }
   __device__ static uint32_t id(unsigned long long e) { return (uint32_t)(e >> 32); }
@@ -556,50 +572,67 @@ __device__ __forceinline__ void warp_sort_keys(const E* buf, uint32_t n, uint32_
   }
 }
 
+// Per-warp shared-memory slice: count table (S entries), output staging (kp2 keys),
+// per-non-empty-table bases (L x u64), run-start bitmap (MCAP/32 + 1 words), count
+// histogram (L+1) and radix digits (256).
 __host__ __device__ inline size_t warp2_slice_bytes(uint32_t log2s, uint32_t entry_bytes, uint32_t L, uint32_t k) {
   uint32_t kp2 = 32;
   while (kp2 < k) kp2 <<= 1;
   const size_t S = (size_t)1 << log2s;
-  size_t b = S * entry_bytes + (size_t)kp2 * entry_bytes + (size_t)L * 8 + (size_t)(L + 1) * 4 +
+  const size_t mcap = S * 3 / 4;  // class bound on M
+  size_t b = S * entry_bytes + (size_t)kp2 * entry_bytes + (size_t)L * 8 + (mcap / 32 + 2) * 4 +
              (size_t)(L + 1) * 4 + 256 * 4;
   return (b + 15) & ~(size_t)15;
 }
 
-template <int LOG2S, typename E>
+__device__ __forceinline__ uint32_t lanemask_le_q() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+
+template <int LOG2S, typename E, int KP>
 __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t* __restrict__ qlist,
                                                    const uint32_t* __restrict__ qcount) {
   using T = Ent<E>;
   using V = typename T::V;
   constexpr uint32_t S = 1u << LOG2S;
-  constexpr uint32_t MASK = S - 1;
-  constexpr uint32_t NV = S / T::kPerVec;  // vectors per table
+  constexpr uint32_t NV = S / T::kPerVec;  // vectors (= hash groups) per table
+  constexpr uint32_t GMASK = NV - 1;
+  constexpr uint32_t MCAP = S * 3 / 4;
+  constexpr uint32_t NBW = MCAP / 32 + 2;  // bitmap words
   extern __shared__ __align__(16) uint8_t smw[];
   const uint32_t L = a.L, k = a.k;
-  uint32_t kp2 = 32;
-  while (kp2 < k) kp2 <<= 1;
+  constexpr uint32_t kp2 = KP * 32;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t* my = smw + warp2_slice_bytes(LOG2S, sizeof(E), L, k) * wib;
   E* tab = reinterpret_cast<E*>(my);                            // [S] count table
   uint32_t* tie = reinterpret_cast<uint32_t*>(my);              // tie ids, compacted over tab
   E* outbuf = tab + S;                                           // [kp2]
-  uint64_t* base = reinterpret_cast<uint64_t*>(outbuf + kp2);   // [L]
-  uint32_t* pref = reinterpret_cast<uint32_t*>(base + L);       // [L+1]
-  uint32_t* hcnt = pref + L + 1;                                 // [L+1] count histogram
+  uint64_t* nbase = reinterpret_cast<uint64_t*>(outbuf + kp2);  // [L] base of i-th non-empty bucket
+  uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);      // [NBW] bucket-start bitmap
+  uint32_t* hcnt = bmap + NBW;                                   // [L+1] count histogram
   uint32_t* hrad = hcnt + L + 1;                                 // [256] radix digits
   V* tabv = reinterpret_cast<V*>(tab);
+  const uint32_t* __restrict__ gids = a.ids;
 
   for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
   for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+  for (uint32_t j = lane; j < NBW; j += 32) bmap[j] = 0;
   __syncwarp();
 
   const uint32_t nq = *qcount;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
   for (uint32_t it = gw; it < nq; it += nw) {
+#ifdef FLASH_QPROF
+    long long qp_last = clock64();
+#endif
     const uint64_t q = qlist[it];
     const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
 
-    // ---- Q1: bucket segments -> prefix offsets ----
-    uint32_t M = 0;
+    // ---- Q1: the non-empty buckets, in table order: their start positions (bitmap over
+    //      the flattened candidate positions) and bases (global index - position) ----
+    uint32_t M = 0, nne = 0;
     for (uint32_t t0 = 0; t0 < L; t0 += 32) {
       const uint32_t t = t0 + lane;
       uint32_t sz = 0;
@@ -618,44 +651,33 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
         const uint32_t y = __shfl_up_sync(kFullMask, x, o);
         if (lane >= o) x += y;
       }
-      if (t < L) {
-        pref[t] = M + x - sz;
-        base[t] = st - (M + x - sz);
+      const uint32_t pos = M + x - sz;
+      const uint32_t ne = __ballot_sync(kFullMask, sz > 0);
+      if (sz > 0) {
+        nbase[nne + __popc(ne & lanemask_lt_q())] = st - pos;
+        atomicOr(&bmap[pos >> 5], 1u << (pos & 31));
       }
+      nne += __popc(ne);
       M += __shfl_sync(kFullMask, x, 31);
     }
-    if (lane == 0) pref[L] = M;
     __syncwarp();
+    QPROF_MARK(0);
 
-    // ---- Q2: gather + count, keeping the count histogram current.  Positions p0+lane
-    //      of a 32-wide round belong to table tcur + #{table starts in (p0, p]}: the
-    //      starts inside the round come from one ballot. ----
-    uint32_t tcur = 0, mymax = 0, D = 0;
-    for (uint32_t p0 = 0; p0 < M; p0 += 128) {
+    // ---- Q2: gather + count.  Position p belongs to the (#starts <= p)-th non-empty
+    //      bucket: one bitmap word and a popc per 32 positions.  The count table is
+    //      bucketized: an id hashes to a 16-byte group of slots that fill left to right,
+    //      so one vector load answers "present / where to insert". ----
+    uint32_t before = 0, mymax = 0, D = 0;
+    for (uint32_t r0 = 0; r0 < M; r0 += 128) {
       uint32_t idv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t r0 = p0 + u * 32;
-        const uint32_t p = r0 + lane;
-        idv[u] = kEmpty;
-        if (r0 < M) {
-          while (pref[tcur + 1] <= r0) ++tcur;  // warp-uniform; usually 0-1 steps
-          const uint32_t tj = tcur + 1 + lane;
-          const uint32_t bj = tj <= L ? pref[tj] : 0xFFFFFFFFu;
-          const uint32_t inround = __ballot_sync(kFullMask, bj < r0 + 32);
-          uint32_t t = tcur;
-          if (inround == kFullMask) {  // > 31 table starts in one round (many empty buckets)
-            while (p < M && pref[t + 1] <= p) ++t;
-          } else {
-            uint32_t mbits = inround;
-            while (mbits) {
-              const uint32_t j = __ffs(mbits) - 1;
-              mbits &= mbits - 1;
-              t += __shfl_sync(kFullMask, bj, j) <= p;
-            }
-          }
-          if (p < M) idv[u] = a.ids[base[t] + p];
-        }
+        const uint32_t w0 = (r0 >> 5) + u;
+        const uint32_t w = bmap[w0];
+        const uint32_t p = r0 + u * 32 + lane;
+        const uint32_t ti = before + __popc(w & lanemask_le_q()) - 1;
+        idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
+        before += __popc(w);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -663,23 +685,32 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
         bool fresh = false;
         if (id != kEmpty && id != excl) {
           mymax = id > mymax ? id : mymax;
-          uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
+          uint32_t g = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
           while (true) {
-            E cur = tab[slot];
-            if (cur == T::kE) {
-              cur = atomicCAS(&tab[slot], T::kE, T::make(id));
-              if (cur == T::kE) {
+            E e[T::kPerVec];
+            T::get(tabv[g], e);
+            int hit = -1, emp = -1;
+#pragma unroll
+            for (int i = T::kPerVec - 1; i >= 0; --i) {
+              if (e[i] == T::kE) emp = i;
+              else if (T::id(e[i]) == id) hit = i;
+            }
+            if (hit < 0 && emp >= 0) {
+              const E old = atomicCAS(&tab[g * T::kPerVec + emp], T::kE, T::make(id));
+              if (old == T::kE) {
                 fresh = true;
                 break;
               }
+              if (T::id(old) != id) continue;  // lost the slot to another id: re-read the group
+              hit = emp;
             }
-            if (T::id(cur) == id) {
-              const uint32_t c = T::count(atomicAdd(&tab[slot], (E)1));  // c -> c+1
+            if (hit >= 0) {
+              const uint32_t c = T::count(atomicAdd(&tab[g * T::kPerVec + hit], (E)1));  // c -> c+1
               atomicSub(&hcnt[c < L ? c : L], 1u);
               atomicAdd(&hcnt[c + 1 < L ? c + 1 : L], 1u);
               break;
             }
-            slot = (slot + 1) & MASK;
+            g = (g + 1) & GMASK;  // group full: next group
           }
         }
         const uint32_t nf = __popc(__ballot_sync(kFullMask, fresh));
@@ -692,7 +723,9 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
       const uint32_t y = __shfl_xor_sync(kFullMask, mymax, o);
       mymax = y > mymax ? y : mymax;
     }
+    for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
     __syncwarp();
+    QPROF_MARK(1);
 
     // ---- Q3a: threshold count c* from the histogram ----
     uint32_t cstar = 0, need = 0, ties = 0;
@@ -708,11 +741,11 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
         const uint32_t y = __shfl_up_sync(kFullMask, x, o);
         if (lane >= o) x += y;
       }
-      const uint32_t before = x - sum;
-      const uint32_t hit = __ballot_sync(kFullMask, before < k && x >= k);
+      const uint32_t bef = x - sum;
+      const uint32_t hit = __ballot_sync(kFullMask, bef < k && x >= k);
       const uint32_t src = __ffs(hit) - 1;
       if (lane == src) {
-        uint32_t cum = before;
+        uint32_t cum = bef;
         for (int32_t c = hi; c >= lo; --c) {
           if (cum + hcnt[c] >= k) {
             cstar = (uint32_t)c;
@@ -730,29 +763,43 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
     __syncwarp();
     for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
     const bool cut = cstar > 0 && need < ties;  // the c* ties must be cut by id
+    QPROF_MARK(2);
 
     // ---- Q3b: one pass over the table: counts above c* (and all ties when no cut is
     //      needed) go to the output buffer; the tied ids are compacted in place to the
-    //      front of the table (writes never pass the current read position) ----
+    //      front of the table (writes never pass the current read position).  Each lane
+    //      classifies its vector, one packed warp scan gives both write offsets. ----
     uint32_t nout = 0, ntie = 0;
     for (uint32_t v0 = 0; v0 < NV; v0 += 32) {
       E e[T::kPerVec];
       T::get(tabv[v0 + lane], e);
-      __syncwarp();
+      uint32_t om = 0, tm = 0;  // per-entry flags
 #pragma unroll
       for (int i = 0; i < T::kPerVec; ++i) {
         const uint32_t c = e[i] != T::kE ? T::count(e[i]) : 0u;
-        const bool out = c > cstar || (c == cstar && c > 0 && !cut);
-        const bool tied = cut && c == cstar;
-        const uint32_t mo = __ballot_sync(kFullMask, out);
-        const uint32_t mt = __ballot_sync(kFullMask, tied);
-        if (out) outbuf[nout + __popc(mo & lanemask_lt_q())] = T::key(e[i]);
-        if (tied) tie[ntie + __popc(mt & lanemask_lt_q())] = T::id(e[i]);
-        nout += __popc(mo);
-        ntie += __popc(mt);
+        if (c > cstar || (c == cstar && c > 0 && !cut)) om |= 1u << i;
+        if (cut && c == cstar) tm |= 1u << i;
       }
+      const uint32_t packed = __popc(om) | (__popc(tm) << 16);
+      uint32_t x = packed;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t tot = __shfl_sync(kFullMask, x, 31);
+      uint32_t po = nout + ((x - packed) & 0xFFFFu), pt = ntie + ((x - packed) >> 16);
+      __syncwarp();  // every lane has read its vector before any tie id overwrites it
+#pragma unroll
+      for (int i = 0; i < T::kPerVec; ++i) {
+        if (om & (1u << i)) outbuf[po++] = T::key(e[i]);
+        if (tm & (1u << i)) tie[pt++] = T::id(e[i]);
+      }
+      nout += tot & 0xFFFFu;
+      ntie += tot >> 16;
     }
     __syncwarp();
+    QPROF_MARK(3);
 
     // ---- Q3c: keep the `need` smallest tied ids (radix select over the compacted ties,
     //      8-bit digits from the top set bit, stops when a digit bucket is taken whole) ----
@@ -779,12 +826,12 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
           const uint32_t y = __shfl_up_sync(kFullMask, x, o);
           if (lane >= o) x += y;
         }
-        const uint32_t before = x - sum;
-        const uint32_t hit = __ballot_sync(kFullMask, before < need && x >= need);
+        const uint32_t bef = x - sum;
+        const uint32_t hit = __ballot_sync(kFullMask, bef < need && x >= need);
         const uint32_t src = __ffs(hit) - 1;
         uint32_t d = 0, cum = 0, hd = 0;
         if (lane == src) {
-          cum = before;
+          cum = bef;
           d = lane * 8;
           for (int i = 0; i < 7; ++i, ++d) {
             if (cum + hrad[d] >= need) break;
@@ -816,20 +863,21 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
       }
     }
     __syncwarp();
+    QPROF_MARK(4);
     for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
+    QPROF_MARK(5);
 
     // ---- Q3d: order by (count desc, id asc), write, pad ----
     uint32_t* oid = a.out_ids + q * k;
     uint32_t* ocnt = a.out_counts + q * k;
-    if (kp2 == 32) warp_sort_keys<1, E>(outbuf, nout, oid, ocnt);
-    else if (kp2 == 64) warp_sort_keys<2, E>(outbuf, nout, oid, ocnt);
-    else if (kp2 == 128) warp_sort_keys<4, E>(outbuf, nout, oid, ocnt);
-    else warp_sort_keys<8, E>(outbuf, nout, oid, ocnt);
+    __syncwarp();
+    warp_sort_keys<KP, E>(outbuf, nout, oid, ocnt);
     for (uint32_t j = nout + lane; j < k; j += 32) {
       oid[j] = kEmpty;
       ocnt[j] = 0;
     }
     __syncwarp();
+    QPROF_MARK(6);
   }
 }
 
@@ -860,25 +908,33 @@ int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count
   return 1;
 }
 
-template <int LOG2S, typename E>
-int launch_warp_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+template <int LOG2S, typename E, int KP>
+int launch_warp_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
   constexpr int kWarps = 4;
   const size_t smem = warp2_slice_bytes(LOG2S, sizeof(E), a.L, a.k) * kWarps;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query_warp<LOG2S, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(k_query_warp<LOG2S, E, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return 0;
     attr = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_warp<LOG2S, E>, 32 * kWarps, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_warp<LOG2S, E, KP>, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = 148ull * per_sm;
   const uint64_t need = (a.nq + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
-  k_query_warp<LOG2S, E><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count);
+  k_query_warp<LOG2S, E, KP><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count);
   return 1;
+}
+
+template <int LOG2S, typename E>
+int launch_warp_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+  if (a.k <= 32) return launch_warp_t<LOG2S, E, 1>(a, list, count, s);
+  if (a.k <= 64) return launch_warp_t<LOG2S, E, 2>(a, list, count, s);
+  if (a.k <= 128) return launch_warp_t<LOG2S, E, 4>(a, list, count, s);
+  return launch_warp_t<LOG2S, E, 8>(a, list, count, s);
 }
 
 }  // namespace
@@ -912,7 +968,7 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (a.k <= 256 && a.packed) {  // one query per warp, (id, count) packed in u32
     n += launch_warp_class<11, uint32_t>(a, lists, counts + 0, s);
     if (a.table_log2 >= 12) n += launch_warp_class<12, uint32_t>(a, lists + a.nq, counts + 1, s);
-  } else if (a.k <= 256) {   // one query per warp, u64 entries
+  } else if (a.k <= 256) {  // one query per warp, u64 entries
     n += launch_warp_class<11, unsigned long long>(a, lists, counts + 0, s);
     if (a.table_log2 >= 12) n += launch_warp_class<12, unsigned long long>(a, lists + a.nq, counts + 1, s);
   } else {
@@ -925,3 +981,14 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
 }
 
 }  // namespace flash
+
+#ifdef FLASH_QPROF
+extern "C" int flash_debug_qprof(unsigned long long out[8], int reset) {
+  if (cudaMemcpyFromSymbol(out, flash::g_qprof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(flash::g_qprof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
