@@ -10,10 +10,11 @@
 // scatter is erased by the per-bucket (prio, id) selection and the final id sort.
 //
 // Kernels: k_count (B1 histogram) -> k_pool_sizes -> 2 scans -> k_fill_old / k_fill_new
-// (scatter every member into a bucket-contiguous pool) -> k_select_warp (one warp per
-// bucket: warp-shuffle sort for |S| <= 32, else a priority-threshold filter to ~R+6sqrt(R)
-// survivors then a shared-memory bitonic sort) -> k_select_big (one CTA per leftover
-// bucket: exact radix select on the priority, any size).
+// (scatter every member into a bucket-contiguous pool) -> k_select_small (one warp per
+// bucket with <= 32 members, keys in registers) -> k_select_warp (one warp per bucket
+// with 33..2048 members: priority-threshold filter to ~R+6sqrt(R) survivors, shared-
+// memory bitonic sort) -> k_select_big (one CTA per larger or leftover bucket: the same
+// filter with the whole CTA, exact radix select on the priority as the fallback).
 #include <cub/device/device_scan.cuh>
 
 #include "flash_internal.cuh"
@@ -46,6 +47,21 @@ __device__ __forceinline__ uint64_t warp_sort32(uint64_t key) {
       const bool up = (lane & k) == 0;
       const bool lower = (lane & j) == 0;
       key = (lower == up) ? (key < other ? key : other) : (key > other ? key : other);
+    }
+  }
+  return key;
+}
+
+// Ascending bitonic sort of one u32 key per lane.
+__device__ __forceinline__ uint32_t warp_sort32_u32(uint32_t key) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t other = __shfl_xor_sync(kFull, key, j);
+      const bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
+      key = keep_min ? min(key, other) : max(key, other);
     }
   }
   return key;
@@ -147,39 +163,60 @@ __device__ __forceinline__ void push_big(uint32_t i, uint32_t* big_list, uint32_
   if ((threadIdx.x & 31) == 0) big_list[atomicAdd(big_count, 1u)] = i;
 }
 
-// B2, common case: one warp per bucket.
+// B2, buckets with <= 32 members (the vast majority): one warp per bucket, keys in
+// registers, no shared memory (full occupancy).  Larger buckets are listed for
+// k_select_warp (or the exact CTA path when FLASH_DEBUG_FORCE_BIG is set).
+__global__ void __launch_bounds__(256)
+k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
+               const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
+               const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
+               uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
+               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb; i += nw) {
+    const uint64_t p0 = pool_off[i];
+    const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
+    if (m == 0) continue;
+    if (m > 32) {  // > 2048 members: the CTA path streams them with 256 threads
+      if (force_big || m > 2048) push_big(i, big_list, big_count);
+      else push_big(i, mid_list, mid_count);
+      continue;
+    }
+    const uint32_t keep = m < R ? m : R;
+    uint32_t* out = ids_out + goff[i];
+    uint32_t id = lane < m ? pool[p0 + lane] : kEmpty;
+    if (m > R) {  // bottom-R by (prio, id)
+      const uint32_t t = i / range, b = i - t * range;
+      const uint64_t tb = prio_bucket_key(keys, t, b);
+      uint64_t key = lane < m ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
+      key = warp_sort32(key);
+      id = lane < keep ? (uint32_t)key : kEmpty;
+    }
+    id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
+    if (lane < keep) out[lane] = id;
+  }
+}
+
+// B2, buckets with > 32 members: one warp per listed bucket.
 __global__ void __launch_bounds__(kSelThreads)
-k_select_warp(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
-              const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
-              const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
-              uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+k_select_warp(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restrict__ mid_list,
+              const uint32_t* __restrict__ mid_count, const uint64_t* __restrict__ pool_off,
+              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
+              uint32_t* __restrict__ ids_out, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
   extern __shared__ uint64_t sel_smem[];
   const uint32_t lane = threadIdx.x & 31;
   uint64_t* buf = sel_smem + (size_t)(threadIdx.x >> 5) * kWarpCap;
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb; i += nw) {
+  const uint32_t nmid = *mid_count;
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nmid; it += nw) {
+    const uint32_t i = mid_list[it];
     const uint64_t p0 = pool_off[i];
     const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
     if (m == 0) continue;
     const uint32_t keep = m < R ? m : R;
     uint32_t* out = ids_out + goff[i];
     const uint32_t t = i / range, b = i - t * range;
-
-    if (m <= 32 && !force_big) {
-      uint32_t id = lane < m ? pool[p0 + lane] : kEmpty;
-      uint64_t key;
-      if (m > R) {  // bottom-R by (prio, id)
-        const uint64_t tb = prio_bucket_key(keys, t, b);
-        key = lane < m ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
-        key = warp_sort32(key);
-        id = (uint32_t)key;
-      }
-      key = lane < keep ? (uint64_t)id : ~0ull;
-      key = warp_sort32(key);  // ascending id
-      if (lane < keep) out[lane] = (uint32_t)key;
-      continue;
-    }
-    if (force_big) { push_big(i, big_list, big_count); continue; }
 
     if (m <= R) {  // keep every member; sort ids
       if (m > kWarpCap) { push_big(i, big_list, big_count); continue; }
@@ -233,15 +270,18 @@ k_select_warp(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_
   }
 }
 
-// B2, exact path for any bucket size (R <= kBigCap): radix select of the keep-th smallest
-// (prio, id) key, 8 bits at a time, then gather and id-sort.
+// B2, large buckets (and anything the warp path could not finish): one CTA per bucket.
+// First a priority-threshold filter with the whole CTA (4 loads in flight per thread)
+// keeps ~R + 6 sqrt(R) + 16 candidates in shared memory; if at least `keep` and at most
+// kBigCap survive, a CTA bitonic sort by (prio, id) picks the bottom-R.  Otherwise an
+// exact radix select of the keep-th smallest (prio, id), 8 bits at a time, decides.
 __global__ void __launch_bounds__(kSelThreads)
-k_select_big(uint32_t range, uint32_t R, HashKeys keys, const uint64_t* __restrict__ pool_off,
+k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const uint64_t* __restrict__ pool_off,
              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
              uint32_t* __restrict__ ids_out, const uint32_t* __restrict__ big_list,
              const uint32_t* __restrict__ big_count) {
   __shared__ uint32_t hist[256];
-  __shared__ uint32_t buf[kBigCap];
+  __shared__ uint64_t kbuf[kBigCap];
   __shared__ uint32_t s_prefix, s_need, s_ties, s_n;
   const uint32_t nbig = *big_count;
   for (uint32_t it = blockIdx.x; it < nbig; it += gridDim.x) {
@@ -253,9 +293,58 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, const uint64_t* __restri
     const uint32_t t = i / range, b = i - t * range;
     const uint64_t tb = prio_bucket_key(keys, t, b);
 
-    uint32_t pstar = 0xFFFFFFFFu, theta = 0xFFFFFFFFu;
-    if (m > R) {
-      // pass A: keep-th smallest priority value pstar, and its rank among equal priorities
+    if (m <= R) {  // every member is kept (m <= R <= kBigCap): sort the ids
+      const uint32_t n2 = pow2_ceil(m);
+      for (uint32_t j = threadIdx.x; j < n2; j += blockDim.x) kbuf[j] = j < m ? (uint64_t)pool[p0 + j] : ~0ull;
+      __syncthreads();
+      block_bitonic(kbuf, n2);
+      for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) out[j] = (uint32_t)kbuf[j];
+      __syncthreads();
+      continue;
+    }
+
+    // ---- threshold filter ----
+    const double expect = (double)R + 6.0 * sqrt((double)R) + 16.0;
+    const uint64_t tau = expect >= (double)m ? (1ull << 32) : (uint64_t)ceil(expect / (double)m * 4294967296.0);
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (uint32_t j0 = threadIdx.x; j0 < m; j0 += 4 * blockDim.x) {
+      uint32_t idv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * blockDim.x;
+        idv[u] = j < m ? pool[p0 + j] : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u * blockDim.x < m) {
+          const uint32_t pr = prio_of(tb, idv[u]);
+          if ((uint64_t)pr < tau) {
+            const uint32_t pos = atomicAdd(&s_n, 1u);
+            if (pos < kBigCap) kbuf[pos] = ((uint64_t)pr << 32) | idv[u];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t cnt = s_n;
+    if (cnt >= keep && cnt <= kBigCap && !exact_only) {
+      const uint32_t n2 = pow2_ceil(cnt);
+      for (uint32_t j = cnt + threadIdx.x; j < n2; j += blockDim.x) kbuf[j] = ~0ull;
+      __syncthreads();
+      block_bitonic(kbuf, n2);  // by (prio, id)
+      const uint32_t n3 = pow2_ceil(keep);
+      for (uint32_t j = threadIdx.x; j < n3; j += blockDim.x) kbuf[j] = j < keep ? (kbuf[j] & 0xFFFFFFFFull) : ~0ull;
+      __syncthreads();
+      block_bitonic(kbuf, n3);  // kept ids ascending
+      for (uint32_t j = threadIdx.x; j < keep; j += blockDim.x) out[j] = (uint32_t)kbuf[j];
+      __syncthreads();
+      continue;
+    }
+
+    // ---- exact fallback: radix select on the priority, then on the id among ties ----
+    uint32_t pstar, theta = 0xFFFFFFFFu;
+    {
       uint32_t prefix = 0, pmask = 0, need = keep, ties = 0;
       for (int shift = 24; shift >= 0; shift -= 8) {
         for (uint32_t d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
@@ -284,15 +373,13 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, const uint64_t* __restri
       }
       pstar = prefix;
       if (need < ties) {
-        // pass B: need-th smallest id among priorities equal to pstar
         uint32_t iprefix = 0, imask = 0;
         for (int shift = 24; shift >= 0; shift -= 8) {
           for (uint32_t d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
           __syncthreads();
           for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
             const uint32_t id = pool[p0 + j];
-            if (prio_of(tb, id) == pstar && (id & imask) == iprefix)
-              atomicAdd(&hist[(id >> shift) & 255u], 1u);
+            if (prio_of(tb, id) == pstar && (id & imask) == iprefix) atomicAdd(&hist[(id >> shift) & 255u], 1u);
           }
           __syncthreads();
           if (threadIdx.x == 0) {
@@ -313,24 +400,19 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, const uint64_t* __restri
         theta = iprefix;
       }
     }
-    // gather the kept ids
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
       const uint32_t id = pool[p0 + j];
-      bool k = true;
-      if (m > R) {
-        const uint32_t pr = prio_of(tb, id);
-        k = pr < pstar || (pr == pstar && id <= theta);
-      }
-      if (k) buf[atomicAdd(&s_n, 1u)] = id;
+      const uint32_t pr = prio_of(tb, id);
+      if (pr < pstar || (pr == pstar && id <= theta)) kbuf[atomicAdd(&s_n, 1u)] = id;
     }
     __syncthreads();
     const uint32_t n2 = pow2_ceil(keep);
-    for (uint32_t j = keep + threadIdx.x; j < n2; j += blockDim.x) buf[j] = 0xFFFFFFFFu;
+    for (uint32_t j = keep + threadIdx.x; j < n2; j += blockDim.x) kbuf[j] = ~0ull;
     __syncthreads();
-    block_bitonic(buf, n2);
-    for (uint32_t j = threadIdx.x; j < keep; j += blockDim.x) out[j] = buf[j];
+    block_bitonic(kbuf, n2);
+    for (uint32_t j = threadIdx.x; j < keep; j += blockDim.x) out[j] = (uint32_t)kbuf[j];
     __syncthreads();
   }
 }
@@ -350,7 +432,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < 148ull * 32 ? (a.n + 7) / 8 : 148ull * 32);
   const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
-  cudaMemsetAsync(a.big_count, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(a.big_count, 0, 2 * sizeof(uint32_t), s);  // big + mid list counters
   if (a.n) {
     k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.L, a.range, a.cursor, a.err);
     launches++;
@@ -377,14 +459,21 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_select_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
     attr = true;
   }
-  const int force_big = getenv("FLASH_DEBUG_FORCE_BIG") ? 1 : 0;
-  const unsigned sel_blocks = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 24 ? ((uint64_t)nb + 7) / 8 : 148ull * 24);
-  k_select_warp<<<sel_blocks, kSelThreads, sel_smem, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off,
-                                                          a.pool, a.goff_new, a.ids_new, a.big_list,
-                                                          a.big_count);
-  k_select_big<<<148 * 2, kSelThreads, 0, s>>>(a.range, a.R, a.keys, a.pool_off, a.pool, a.goff_new,
-                                              a.ids_new, a.big_list, a.big_count);
+  // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
+  // =2: and the CTA path skips its filter (exact radix select).  Tests only.
+  const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");
+  const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
+  uint32_t* mid_list = a.cursor;  // free once k_fill_new is done
+  uint32_t* mid_count = a.big_count + 1;
+  const unsigned small_blocks = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 64 ? ((uint64_t)nb + 7) / 8 : 148ull * 64);
+  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
+                                             a.ids_new, mid_list, mid_count, a.big_list, a.big_count);
+  k_select_warp<<<148 * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
+                                                      a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;
+  k_select_big<<<148 * 2, kSelThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
+                                              a.ids_new, a.big_list, a.big_count);
+  launches += 1;
   return launches;
 }
 

@@ -63,13 +63,26 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
     const int64_t head = min(end, e + (int64_t)(((16u - mis) & 15u) >> 2));
     if (e + (int64_t)lane < head) bin_min(v, B, keys, ld_stream(col_idx + e + lane));
     e = head;
-    const int64_t vec_end = e + ((end - e) & ~(int64_t)127);  // whole 512-B warp tiles
-    for (; e < vec_end; e += 128) {
+    const int64_t vec_end2 = e + ((end - e) & ~(int64_t)255);  // pairs of 512-B warp tiles
+    for (; e < vec_end2; e += 256) {  // two 16-B loads in flight per lane
+      const uint4 q0 = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e) + lane);
+      const uint4 q1 = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e + 128) + lane);
+      bin_min(v, B, keys, q0.x);
+      bin_min(v, B, keys, q0.y);
+      bin_min(v, B, keys, q0.z);
+      bin_min(v, B, keys, q0.w);
+      bin_min(v, B, keys, q1.x);
+      bin_min(v, B, keys, q1.y);
+      bin_min(v, B, keys, q1.z);
+      bin_min(v, B, keys, q1.w);
+    }
+    if (end - e >= 128) {  // one more whole tile
       const uint4 q = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e) + lane);
       bin_min(v, B, keys, q.x);
       bin_min(v, B, keys, q.y);
       bin_min(v, B, keys, q.z);
       bin_min(v, B, keys, q.w);
+      e += 128;
     }
     for (e += lane; e < end; e += 32) bin_min(v, B, keys, ld_stream(col_idx + e));
     __syncwarp();
@@ -131,8 +144,8 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  uint64_t blocks = (n_rows + wpb - 1) / wpb;
-  const uint64_t cap = 148ull * 64;
+  uint64_t blocks = (n_rows + wpb - 1) / wpb;  // one warp per row: the block scheduler balances
+  const uint64_t cap = 0x7FFFFFFFull;             // the skewed row lengths
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return 0;
   k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,

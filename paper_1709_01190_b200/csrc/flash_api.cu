@@ -197,7 +197,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
   TRY(ensure(h->pool, sizeof(uint32_t) * pool_cap));
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * kept_cap));
-  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 1)));
+  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 2)));
   TRY(ensure(h->scan_tmp, build_scan_tmp_bytes(nb)));
 
   Phase ph(h, 1, s);

@@ -92,7 +92,7 @@ struct BuildArgs {
   uint32_t* pool;             // [pool capacity]
   uint32_t* ids_new;          // [kept capacity]
   uint32_t* big_list;         // [nb] bucket indices for the CTA path
-  uint32_t* big_count;        // [1]
+  uint32_t* big_count;        // [2]: CTA-path list count, warp-path (mid) list count
   unsigned long long* err;    // device error counter
   void* scan_tmp;
   size_t scan_tmp_bytes;

@@ -111,6 +111,8 @@ BUILD_CASES = [
     ("range1_R128", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 3, 128, 1),
     ("range1_R2000_big", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 2, 2000, 1),
     ("range1_R4096_m_le_R", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=3000)), 1, 2, 4096, 1),
+    ("range1_R4096_m5000_overflow", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=5000)), 1, 2, 4096, 1),
+    ("range2_R100_m2500_cta", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=5000)), 1, 2, 100, 2),
     ("webspam_slice", lambda: shape_slice("webspam", 1500), 4, 50, 128, 1 << 10),
     ("url_slice", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 12),
 ]
@@ -130,10 +132,12 @@ def test_tables_bit_exact(name, make, K, L, R, rng):
         assert idx.errors() == 0
 
 
-def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch):
-    """FLASH_DEBUG_FORCE_BIG routes every bucket with > 32 members through the exact
-    radix-select CTA kernel (normally only reached by rare threshold misses)."""
-    monkeypatch.setenv("FLASH_DEBUG_FORCE_BIG", "1")
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch, mode):
+    """FLASH_DEBUG_FORCE_BIG=1 routes every bucket with > 32 members through the CTA
+    kernel; =2 also skips its threshold filter so the exact radix select (normally only
+    reached by rare threshold misses) decides every bucket."""
+    monkeypatch.setenv("FLASH_DEBUG_FORCE_BIG", mode)
     for make, K, L, R, rng in [(skew_csr, 2, 6, 8, 64),
                                (lambda: shape_slice("webspam", 1500), 4, 50, 128, 256),
                                (lambda: synth.generate(synth.SHAPES["tiny"].with_(N=2000)), 1, 2, 300, 1)]:
