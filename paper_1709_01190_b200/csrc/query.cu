@@ -573,15 +573,16 @@ __device__ __forceinline__ void warp_sort_keys(const E* buf, uint32_t n, uint32_
 }
 
 // Per-warp shared-memory slice: count table (S entries), output staging (kp2 keys),
-// per-non-empty-table bases (L x u64), run-start bitmap (MCAP/32 + 1 words), count
-// histogram (L+1) and radix digits (256).
+// per-non-empty-table bases (L x u64), run-start bitmap (MCAP/32 + 2 words) and count
+// histogram (L+1).  The 256 radix digits use the table's last 1 KB: during the tie
+// select the table only holds the compacted ties (<= MCAP = 3S/4 ids) at its front.
 __host__ __device__ inline size_t warp2_slice_bytes(uint32_t log2s, uint32_t entry_bytes, uint32_t L, uint32_t k) {
   uint32_t kp2 = 32;
   while (kp2 < k) kp2 <<= 1;
   const size_t S = (size_t)1 << log2s;
   const size_t mcap = S * 3 / 4;  // class bound on M
   size_t b = S * entry_bytes + (size_t)kp2 * entry_bytes + (size_t)L * 8 + (mcap / 32 + 2) * 4 +
-             (size_t)(L + 1) * 4 + 256 * 4;
+             (size_t)(L + 1) * 4;  // radix digits live in the table's free tail (see k_query_warp)
   return (b + 15) & ~(size_t)15;
 }
 
@@ -612,7 +613,8 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
   uint64_t* nbase = reinterpret_cast<uint64_t*>(outbuf + kp2);  // [L] base of i-th non-empty bucket
   uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);      // [NBW] bucket-start bitmap
   uint32_t* hcnt = bmap + NBW;                                   // [L+1] count histogram
-  uint32_t* hrad = hcnt + L + 1;                                 // [256] radix digits
+  uint32_t* hrad = reinterpret_cast<uint32_t*>(tab + S) - 256;  // [256] radix digits (table tail)
+  static_assert(MCAP * 4 + 256 * 4 <= S * sizeof(E), "tie ids and radix digits must fit the table");
   V* tabv = reinterpret_cast<V*>(tab);
   const uint32_t* __restrict__ gids = a.ids;
 
@@ -666,8 +668,52 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
     // ---- Q2: gather + count.  Position p belongs to the (#starts <= p)-th non-empty
     //      bucket: one bitmap word and a popc per 32 positions.  The count table is
     //      bucketized: an id hashes to a 16-byte group of slots that fill left to right,
-    //      so one vector load answers "present / where to insert". ----
-    uint32_t before = 0, mymax = 0, D = 0;
+    //      so one vector load answers "present / where to insert".  The main loop makes
+    //      exactly one probe per candidate (4 group loads in flight per lane); the few
+    //      candidates whose first group is full, or whose slot was just taken by another
+    //      id, are queued and inserted by the full probe loop (insert_slow).  An id is
+    //      always either in its first group or that group is full, so both paths agree. ----
+    uint32_t before = 0, mymax = 0, D = 0, qn = 0;
+    uint32_t* queue = reinterpret_cast<uint32_t*>(outbuf);  // free until Q3b
+    constexpr uint32_t QCAP = kp2 * sizeof(E) / 4;
+    auto bump = [&](uint32_t c) {  // an existing entry went from count c to c+1
+      atomicSub(&hcnt[c < L ? c : L], 1u);
+      atomicAdd(&hcnt[c + 1 < L ? c + 1 : L], 1u);
+    };
+    auto insert_slow = [&](uint32_t id) -> bool {  // full linear probe over groups
+      uint32_t g = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
+      while (true) {
+        E e[T::kPerVec];
+        T::get(tabv[g], e);
+        int hit = -1, emp = -1;
+#pragma unroll
+        for (int i = T::kPerVec - 1; i >= 0; --i) {
+          if (e[i] == T::kE) emp = i;
+          else if (T::id(e[i]) == id) hit = i;
+        }
+        if (hit < 0 && emp >= 0) {
+          const E old = atomicCAS(&tab[g * T::kPerVec + emp], T::kE, T::make(id));
+          if (old == T::kE) return true;
+          if (T::id(old) != id) continue;  // lost the slot to another id: re-read the group
+          hit = emp;
+        }
+        if (hit >= 0) {
+          bump(T::count(atomicAdd(&tab[g * T::kPerVec + hit], (E)1)));
+          return false;
+        }
+        g = (g + 1) & GMASK;  // group full: next group
+      }
+    };
+    auto flush = [&]() {
+      for (uint32_t j0 = 0; j0 < qn; j0 += 32) {
+        const bool f = (j0 + lane < qn) && insert_slow(queue[j0 + lane]);
+        const uint32_t nf = __popc(__ballot_sync(kFullMask, f));
+        if (lane == 0 && nf) atomicAdd(&hcnt[1], nf);
+        D += nf;
+      }
+      qn = 0;
+      __syncwarp();
+    };
     for (uint32_t r0 = 0; r0 < M; r0 += 128) {
       uint32_t idv[4];
 #pragma unroll
@@ -679,45 +725,50 @@ __global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t*
         idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
         before += __popc(w);
       }
+      uint32_t gv[4];
+      V ev[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t id = idv[u] != excl ? idv[u] : kEmpty;
+        idv[u] = id;
+        mymax = (id != kEmpty && id > mymax) ? id : mymax;
+        gv[u] = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
+        if (id != kEmpty) ev[u] = tabv[gv[u]];  // the group as of this step (re-checked by CAS)
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint32_t id = idv[u];
-        bool fresh = false;
-        if (id != kEmpty && id != excl) {
-          mymax = id > mymax ? id : mymax;
-          uint32_t g = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
-          while (true) {
-            E e[T::kPerVec];
-            T::get(tabv[g], e);
-            int hit = -1, emp = -1;
+        bool fresh = false, defer = false;
+        if (id != kEmpty) {
+          E e[T::kPerVec];
+          T::get(ev[u], e);
+          int hit = -1, emp = -1;
 #pragma unroll
-            for (int i = T::kPerVec - 1; i >= 0; --i) {
-              if (e[i] == T::kE) emp = i;
-              else if (T::id(e[i]) == id) hit = i;
-            }
-            if (hit < 0 && emp >= 0) {
-              const E old = atomicCAS(&tab[g * T::kPerVec + emp], T::kE, T::make(id));
-              if (old == T::kE) {
-                fresh = true;
-                break;
-              }
-              if (T::id(old) != id) continue;  // lost the slot to another id: re-read the group
-              hit = emp;
-            }
-            if (hit >= 0) {
-              const uint32_t c = T::count(atomicAdd(&tab[g * T::kPerVec + hit], (E)1));  // c -> c+1
-              atomicSub(&hcnt[c < L ? c : L], 1u);
-              atomicAdd(&hcnt[c + 1 < L ? c + 1 : L], 1u);
-              break;
-            }
-            g = (g + 1) & GMASK;  // group full: next group
+          for (int i = T::kPerVec - 1; i >= 0; --i) {
+            if (e[i] == T::kE) emp = i;
+            else if (T::id(e[i]) == id) hit = i;
           }
+          const uint32_t base_slot = gv[u] * T::kPerVec;
+          if (hit < 0 && emp >= 0) {
+            const E old = atomicCAS(&tab[base_slot + emp], T::kE, T::make(id));
+            if (old == T::kE) fresh = true;
+            else if (T::id(old) == id) hit = emp;
+            else defer = true;
+          } else if (hit < 0) {
+            defer = true;  // first group full
+          }
+          if (hit >= 0) bump(T::count(atomicAdd(&tab[base_slot + hit], (E)1)));
         }
         const uint32_t nf = __popc(__ballot_sync(kFullMask, fresh));
         if (lane == 0 && nf) atomicAdd(&hcnt[1], nf);
         D += nf;
+        const uint32_t dm = __ballot_sync(kFullMask, defer);
+        if (defer) queue[qn + __popc(dm & lanemask_lt_q())] = id;
+        qn += __popc(dm);
+        if (qn + 32 > QCAP) flush();
       }
     }
+    flush();
 #pragma unroll
     for (uint32_t o = 16; o > 0; o >>= 1) {
       const uint32_t y = __shfl_xor_sync(kFullMask, mymax, o);
