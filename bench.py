@@ -15,9 +15,10 @@ flash_knn_graph_host (pinned host CSR in, host top-k out, copies inside the time
 region).  N>1: one rank per GPU (torchrun), replicated tables (paper_1709_01190_b200
 /dist.py), strong scaling of the fixed graph.
 
-The reference arm (--impl reference) times the CPU oracle (oracle/) as it stands on
-the host cores, on a bounded sample of the same workload (hash + build of every row,
-top-k for a row sample, extrapolated per query); it is a deliberately slow baseline.
+The reference arm (--impl reference) and `cpu_baseline` time the CPU oracle (oracle/)
+as it stands on the host cores (OpenMP, all cores) on the same workload: hash + build
+of every row and top-k for --ref-sample rows (default: all rows, i.e. the whole graph;
+a smaller sample is extrapolated per query).  It is a deliberately slow baseline.
 """
 from __future__ import annotations
 
@@ -39,7 +40,11 @@ import synth  # noqa: E402
 K, L, R, RANGE, SEED, TOPK = 4, 50, 128, 1 << 15, 0x5EED0002, 128
 METRIC = "webspam-shaped k-NN graph time (s), queries/s, hash nnz/s at 1/2/4/8 B200"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+# Shared-memory RMW throughput measured on this pool's B200 (profiles/r01_microbench_smem.txt:
+# RED.S.ADD on random addresses, 8.76 lane-ops/clk/SM at 1.9 GHz x 148 SMs): the ceiling
+# for the count step, which needs at least one shared-memory RMW per candidate.
+SMEM_RMW_PEAK = 8.76 * 148 * 1.9e9
 
 
 def log(*a):
@@ -263,30 +268,34 @@ def run_ours(args):
         query_ms = per_step["query"]
         build_ms = per_step["build"]
         dominant = max(("hash", hash_ms), ("build", build_ms), ("query", query_ms), key=lambda x: x[1])[0]
-        traffic = None
+        traffic = {}
         try:
             with open(TRAFFIC_PATH) as f:
-                traffic = json.load(f)
+                for d in json.load(f):
+                    traffic.setdefault(d["kernel"].split("::")[-1].split("<")[0], d.get("dram_traffic_bytes"))
         except Exception:
             pass
         if dominant == "query" and n_cand is not None:
-            qbytes = 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local
-            roof = {"kernel": "k_query", "bound": "hbm", "achieved": qbytes / (query_ms * 1e-3) / 1e9,
-                    "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
-                    "traffic": (traffic or {}).get("k_query"), "algorithmic_bytes": qbytes,
-                    "candidates": n_cand}
+            # the count kernel is bound by per-candidate shared-memory work, not by HBM
+            roof = {"kernel": "k_query_warp", "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
+                    "peak": SMEM_RMW_PEAK, "unit": "candidate-updates/s", "peak_kind": "measured (smem RMW microbench)",
+                    "traffic": traffic.get("k_query_warp"), "candidates": n_cand,
+                    "hbm_view": {"algorithmic_bytes": 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local,
+                                 "achieved_GBps": (4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local)
+                                 / (query_ms * 1e-3) / 1e9}}
         elif dominant == "build":
             bbytes = 8 * L * n_local * 2 + 12 * L * n_local
             roof = {"kernel": "build (k_count..k_select_big)", "bound": "hbm",
                     "achieved": bbytes / (build_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                    "peak_kind": peak_kind, "traffic": (traffic or {}).get("build"), "algorithmic_bytes": bbytes}
+                    "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": bbytes}
         else:
             roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
                     "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
-                    "traffic": (traffic or {}).get("k_doph"), "algorithmic_bytes": hash_bytes}
+                    "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
+        hash_roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
+                     "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        hash_roof = {"achieved_GBps": hash_bytes / (hash_ms * 1e-3) / 1e9,
-                     "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak}
         value = shape.N / (ms_step * 1e-3)
         h2d = 8 * (n_local + 1) + 4 * nnz_local
         d2h = 8 * n_local * TOPK
@@ -378,7 +387,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-sample", type=int, default=20000, help="oracle query sample (rows)")
+    ap.add_argument("--ref-sample", type=int, default=350000, help="oracle query sample (rows; all = full graph)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
