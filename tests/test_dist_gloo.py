@@ -1,0 +1,116 @@
+"""Multi-process (world_size 2 and 3, gloo on CPU) check of the multi-GPU orchestration
+in paper_1709_01190_b200/dist.py: row sharding, the address all-gather, global ids and
+self-exclusion.  The per-rank compute is stood in for by the CPU oracle (tests only);
+on GPUs the same orchestration drives libflash.so over NCCL.  The distributed graph
+must equal the single-process oracle graph row for row (identity at every GPU count)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_1709_01190_b200 import dist as fdist
+
+CFG = dict(K=4, L=16, R=8, range_=256, seed=0xD157, k=10)
+
+
+class OracleIndex:
+    """CPU stand-in with the FlashIndex methods dist.py uses (hash / insert / query)."""
+
+    def __init__(self, K, L, R, range_, seed):
+        self.K, self.L, self.R, self.range, self.seed = K, L, R, range_, seed
+        self.T = None
+
+    def hash_addrs(self, row_ptr, col_idx):
+        rp = row_ptr.numpy()
+        col = col_idx.numpy().view(np.uint32)
+        codes = oracle.doph(self.K, self.L, self.seed, rp, col)
+        return torch.from_numpy(oracle.addresses(self.K, self.L, self.range, self.seed, codes).view(np.int32))
+
+    def insert_addrs(self, addrs, id_base):
+        a = addrs.numpy().view(np.uint32)
+        ids = (np.arange(a.shape[0], dtype=np.int64) + id_base).astype(np.uint32)
+        self.T = oracle.build(self.L, self.R, self.range, self.seed, a, ids)
+
+    def query_addrs(self, addrs, k, exclude):
+        ids, cnt = oracle.query(self.T, addrs.numpy().view(np.uint32), k,
+                                exclude=exclude.numpy().astype(np.int64).astype(np.uint32))
+        return torch.from_numpy(ids.view(np.int32)), torch.from_numpy(cnt.view(np.int32))
+
+
+def _shape():
+    return synth.SHAPES["tiny"].with_(N=700, seed=11)
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shape = _shape()
+        lens = np.diff(synth.generate(shape)[0])
+        bounds = fdist.shard_bounds(lens, world)
+        rp, col = synth.generate(shape, rows=(bounds[rank], bounds[rank + 1]))
+        idx = OracleIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"])
+        ids, cnt = fdist.knn_graph_replicated(idx, torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)),
+                                              CFG["k"], bounds, rank)
+        np.save(os.path.join(out_dir, f"ids_{rank}.npy"), ids.numpy())
+        np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), cnt.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_graph_equals_single_process(tmp_path, world):
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    shape = _shape()
+    rp, col = synth.generate(shape)
+    want_ids, want_cnt = oracle.knn_graph(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"], rp, col,
+                                          CFG["k"])
+    got_ids = np.concatenate([np.load(tmp_path / f"ids_{r}.npy") for r in range(world)]).view(np.uint32)
+    got_cnt = np.concatenate([np.load(tmp_path / f"cnt_{r}.npy") for r in range(world)]).view(np.uint32)
+    assert np.array_equal(got_ids, want_ids)
+    assert np.array_equal(got_cnt, want_cnt)
+
+
+def test_shard_bounds_balance_nnz_and_cover_all_rows():
+    lens = np.random.default_rng(0).integers(1, 5000, size=10_001)
+    for world in (1, 2, 3, 8):
+        b = fdist.shard_bounds(lens, world)
+        assert b[0] == 0 and b[-1] == lens.size and all(x <= y for x, y in zip(b, b[1:]))
+        tot = lens.sum()
+        for g in range(world):
+            share = lens[b[g]:b[g + 1]].sum()
+            assert abs(share - tot / world) <= lens.max()
+
+
+def test_all_gather_rows_handles_uneven_shards(tmp_path):
+    port = _free_port()
+    mp.spawn(_gather_worker, args=(port, str(tmp_path)), nprocs=2, join=True)
+    got = np.load(tmp_path / "g0.npy")
+    assert got.tolist() == [[0, 0], [0, 1], [0, 2], [1, 0]]
+
+
+def _gather_worker(rank, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        counts = [3, 1]
+        local = torch.tensor([[rank, i] for i in range(counts[rank])], dtype=torch.int32)
+        out = fdist.all_gather_rows(local, counts)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "g0.npy"), out.numpy())
+    finally:
+        dist.destroy_process_group()
