@@ -16,7 +16,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 SO = os.path.join(PKG, "libflash.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["doph.cu", "build.cu", "query.cu", "query_merge.cu", "flash_api.cu"]
+SOURCES = ["doph.cu", "build.cu", "query.cu", "query_sort.cu", "flash_api.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -77,8 +77,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    if "--qprof" in sys.argv:
-        print(build_variant("qprof", ["FLASH_QPROF"]))
-    else:
-        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-        print(SO)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(SO)

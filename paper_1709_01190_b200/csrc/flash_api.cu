@@ -263,6 +263,7 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   a.err = h->err;
   a.table_log2 = h->table_log2;
   a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
+  a.max_id = (uint32_t)h->max_id;
   h->launches += launch_query(a, h->qscratch.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;

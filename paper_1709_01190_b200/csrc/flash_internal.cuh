@@ -114,13 +114,14 @@ struct QueryArgs {
   unsigned long long* err;
   uint32_t table_log2;      // worst-case count-table slots = 2^table_log2 (from L*R)
   int packed;               // every inserted id < 2^24-1 and L <= 255: u32 (id, count) entries
+  uint32_t max_id;          // largest id inserted (the sort kernel's digit range)
 };
 // scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
 int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s);
 size_t query_scratch_bytes(uint64_t nq);
-// merge-based warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
-int launch_query_merge(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
-                       cudaStream_t s);
+// radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
+int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
+                      cudaStream_t s);
 size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k);
 uint32_t query_table_log2(uint32_t L, uint32_t R);
 

@@ -1,9 +1,9 @@
 // query.cu — Q1-Q3: the querying phase (Alg. 3) on sm_100a.
 //
 // k_query_plan: one lane per query sums the sizes M of its L addressed buckets and
-//   files the query into a size class (count-table capacity 2^11 / 2^13 / 2^14 slots,
-//   load factor <= 1/2), so most queries run with a small shared-memory footprint and
-//   many CTAs per SM.
+//   files the query into a size class: M <= 1024 / 1536 / 3072 go to the warp-per-query
+//   radix-partition kernel (query_sort.cu), larger M to the CTA kernel below (count
+//   table of 2^13 / 2^14 slots, load factor <= 1/2).
 // k_query<LOG2S, NT>: one CTA owns one query at a time (persistent over its class list):
 //   Q1 gather   warp 0 scans the L bucket sizes into prefix offsets; each warp then walks
 //               its own contiguous chunk of the flattened candidate positions p (4 loads in
@@ -28,19 +28,6 @@ namespace {
 
 constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
-#ifdef FLASH_QPROF  // phase-cycle instrumentation of k_query_warp (tools/qprof.py; never in the product build)
-__device__ unsigned long long g_qprof[8];
-#define QPROF_MARK(i)                                                   \
-  do {                                                                  \
-    const long long now_ = clock64();                                   \
-    if (lane == 0) atomicAdd(&g_qprof[i], (unsigned long long)(now_ - qp_last)); \
-    qp_last = now_;                                                     \
-  } while (0)
-#else
-#define QPROF_MARK(i) \
-  do {                \
-  } while (0)
-#endif
 
 __device__ __forceinline__ uint32_t pow2_ceil_q(uint32_t x) {
   return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
@@ -51,10 +38,10 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
   return m;
 }
 
-// Query size classes by M (candidates): <= 1536 and <= 3072 run one query per warp with
-// 2^11 / 2^12 count slots (load <= 3/4); <= 4096 and <= 8192 one query per CTA with
-// 2^13 / 2^14 slots (the CTA kernels also serve k > 256).
-constexpr int kClasses = 4;
+// Query size classes by M (candidates): <= 1024, <= 1536 and <= 3072 run one query per
+// warp (query_sort.cu; smaller classes use less shared memory, so more warps per SM);
+// <= 4096 and <= 8192 run one query per CTA with 2^13 / 2^14 count slots (below).
+constexpr int kClasses = 5;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              uint32_t L, uint32_t range, uint32_t* __restrict__ lists,
@@ -75,7 +62,7 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
         }
       }
     }
-    const int cls = M <= 1536 ? 0 : (M <= 3072 ? 1 : (M <= 4096 ? 2 : 3));
+    const int cls = M <= 1024 ? 0 : (M <= 1536 ? 1 : (M <= 3072 ? 2 : (M <= 4096 ? 3 : 4)));
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) {
       const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
@@ -141,13 +128,6 @@ __device__ __forceinline__ void warp_sort_out(const uint64_t* outbuf, uint32_t n
   }
 }
 
-__host__ __device__ inline size_t warp_slice_bytes(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
-  uint32_t kp2 = 1;
-  while (kp2 < k) kp2 <<= 1;
-  const size_t S = (size_t)1 << log2s;
-  size_t b = (size_t)kp2 * 8 + (size_t)L * 8 + S * 4 + (size_t)(L + 1) * 4 + (size_t)hist_len * 4 + S * 2 + S * 2;
-  return (b + 15) & ~(size_t)15;
-}
 
 struct QueryShared {
   uint32_t M, nlist, nout, cstar, need, ties, theta, maxid, done, prefix;
@@ -481,457 +461,6 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
 }
 
 
-// ---------------------------------------------------------------------------
-// Warp-per-query path (k <= 256): one warp owns one query at a time, no CTA barriers.
-// Count table entries pack (id, count) in one word: u32 = id<<8 | count when every id
-// is < 2^24-1 and L <= 255 (webspam, url, tiny), else u64 = id<<32 | count.  The table
-// is scanned directly (vector loads) instead of keeping a distinct-slot list, which
-// keeps the per-warp footprint at ~S words so ~20 warps fit per SM.
-// ---------------------------------------------------------------------------
-template <typename E>
-struct Ent;
-template <>
-struct Ent<uint32_t> {
-  using V = uint4;  // 4 entries per vector load / hash group
-  static constexpr int kPerVec = 4;
-  static constexpr int kLog2Per = 2;
-  static constexpr uint32_t kE = 0xFFFFFFFFu;
-  __device__ static uint32_t make(uint32_t id) { return (id << 8) | 1u; }
-  __device__ static uint32_t id(uint32_t e) { return e >> 8; }
-  __device__ static uint32_t count(uint32_t e) { return e & 0xFFu; }
-  __device__ static uint32_t key(uint32_t e) { return ((255u - (e & 0xFFu)) << 24) | (e >> 8); }
-  __device__ static uint32_t key_id(uint32_t k) { return k & 0xFFFFFFu; }
-  __device__ static uint32_t key_count(uint32_t k) { return 255u - (k >> 24); }
-  __device__ static void get(const V& v, uint32_t* e) { e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w; }
-  __device__ static V empty_vec() { return make_uint4(kE, kE, kE, kE); }
-};
-template <>
-struct Ent<unsigned long long> {
-  using V = ulonglong2;
-  static constexpr int kPerVec = 2;
-  static constexpr int kLog2Per = 1;
-  static constexpr unsigned long long kE = ~0ull;
-  __device__ static unsigned long long make(uint32_t id) { return ((unsigned long long)id << 32) | 1ull; }
-  __device__ static uint32_t id(unsigned long long e) { return (uint32_t)(e >> 32); }
-  __device__ static uint32_t count(unsigned long long e) { return (uint32_t)e; }
-  __device__ static unsigned long long key(unsigned long long e) {
-    return ((unsigned long long)(0xFFFFu - (uint32_t)e) << 32) | (e >> 32);
-  }
-  __device__ static uint32_t key_id(unsigned long long k) { return (uint32_t)k; }
-  __device__ static uint32_t key_count(unsigned long long k) { return 0xFFFFu - (uint32_t)(k >> 32); }
-  __device__ static void get(const V& v, unsigned long long* e) { e[0] = v.x; e[1] = v.y; }
-  __device__ static V empty_vec() { return make_ulonglong2(kE, kE); }
-};
-
-// Sort KP*32 keys (buf[0..n), padded with ~0) ascending in one warp's registers
-// (element e = r*32 + lane) and write the first n as (id, count).
-template <int KP, typename E>
-__device__ __forceinline__ void warp_sort_keys(const E* buf, uint32_t n, uint32_t* oid, uint32_t* ocnt) {
-  const uint32_t lane = threadIdx.x & 31;
-  constexpr uint32_t N = KP * 32;
-  E v[KP];
-#pragma unroll
-  for (int r = 0; r < KP; ++r) {
-    const uint32_t e = r * 32 + lane;
-    v[r] = e < n ? buf[e] : (E)~(E)0;
-  }
-#pragma unroll
-  for (uint32_t kk = 2; kk <= N; kk <<= 1) {
-#pragma unroll
-    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= 32) {
-        const uint32_t rj = j >> 5;
-#pragma unroll
-        for (int r = 0; r < KP; ++r) {
-          if ((r & rj) == 0) {
-            const bool up = ((r * 32 + lane) & kk) == 0;
-            const E x = v[r], y = v[r | rj];
-            if ((x > y) == up) {
-              v[r] = y;
-              v[r | rj] = x;
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < KP; ++r) {
-          const E other = __shfl_xor_sync(kFullMask, v[r], j);
-          const bool keep_min = (((r * 32 + lane) & kk) == 0) == ((lane & j) == 0);
-          v[r] = keep_min ? (v[r] < other ? v[r] : other) : (v[r] > other ? v[r] : other);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < KP; ++r) {
-    const uint32_t e = r * 32 + lane;
-    if (e < n) {
-      oid[e] = Ent<E>::key_id(v[r]);
-      ocnt[e] = Ent<E>::key_count(v[r]);
-    }
-  }
-}
-
-// Per-warp shared-memory slice: count table (S entries), output staging (kp2 keys),
-// per-non-empty-table bases (L x u64), run-start bitmap (MCAP/32 + 2 words) and count
-// histogram (L+1).  The 256 radix digits use the table's last 1 KB: during the tie
-// select the table only holds the compacted ties (<= MCAP = 3S/4 ids) at its front.
-__host__ __device__ inline size_t warp2_slice_bytes(uint32_t log2s, uint32_t entry_bytes, uint32_t L, uint32_t k) {
-  uint32_t kp2 = 32;
-  while (kp2 < k) kp2 <<= 1;
-  const size_t S = (size_t)1 << log2s;
-  const size_t mcap = S * 3 / 4;  // class bound on M
-  size_t b = S * entry_bytes + (size_t)kp2 * entry_bytes + (size_t)L * 8 + (mcap / 32 + 2) * 4 +
-             (size_t)(L + 1) * 4;  // radix digits live in the table's free tail (see k_query_warp)
-  return (b + 15) & ~(size_t)15;
-}
-
-__device__ __forceinline__ uint32_t lanemask_le_q() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
-  return m;
-}
-
-template <int LOG2S, typename E, int KP>
-__global__ void __launch_bounds__(128) k_query_warp(QueryArgs a, const uint32_t* __restrict__ qlist,
-                                                   const uint32_t* __restrict__ qcount) {
-  using T = Ent<E>;
-  using V = typename T::V;
-  constexpr uint32_t S = 1u << LOG2S;
-  constexpr uint32_t NV = S / T::kPerVec;  // vectors (= hash groups) per table
-  constexpr uint32_t GMASK = NV - 1;
-  constexpr uint32_t MCAP = S * 3 / 4;
-  constexpr uint32_t NBW = MCAP / 32 + 2;  // bitmap words
-  extern __shared__ __align__(16) uint8_t smw[];
-  const uint32_t L = a.L, k = a.k;
-  constexpr uint32_t kp2 = KP * 32;
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t* my = smw + warp2_slice_bytes(LOG2S, sizeof(E), L, k) * wib;
-  E* tab = reinterpret_cast<E*>(my);                            // [S] count table
-  uint32_t* tie = reinterpret_cast<uint32_t*>(my);              // tie ids, compacted over tab
-  E* outbuf = tab + S;                                           // [kp2]
-  uint64_t* nbase = reinterpret_cast<uint64_t*>(outbuf + kp2);  // [L] base of i-th non-empty bucket
-  uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);      // [NBW] bucket-start bitmap
-  uint32_t* hcnt = bmap + NBW;                                   // [L+1] count histogram
-  uint32_t* hrad = reinterpret_cast<uint32_t*>(tab + S) - 256;  // [256] radix digits (table tail)
-  static_assert(MCAP * 4 + 256 * 4 <= S * sizeof(E), "tie ids and radix digits must fit the table");
-  V* tabv = reinterpret_cast<V*>(tab);
-  const uint32_t* __restrict__ gids = a.ids;
-
-  for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
-  for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
-  for (uint32_t j = lane; j < NBW; j += 32) bmap[j] = 0;
-  __syncwarp();
-
-  const uint32_t nq = *qcount;
-  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t it = gw; it < nq; it += nw) {
-#ifdef FLASH_QPROF
-    long long qp_last = clock64();
-#endif
-    const uint64_t q = qlist[it];
-    const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
-
-    // ---- Q1: the non-empty buckets, in table order: their start positions (bitmap over
-    //      the flattened candidate positions) and bases (global index - position) ----
-    uint32_t M = 0, nne = 0;
-    for (uint32_t t0 = 0; t0 < L; t0 += 32) {
-      const uint32_t t = t0 + lane;
-      uint32_t sz = 0;
-      uint64_t st = 0;
-      if (t < L) {
-        const uint32_t ad = a.addrs[q * L + t];
-        if (ad < a.range) {
-          const uint64_t i = (uint64_t)t * a.range + ad;
-          st = a.goff[i];
-          sz = (uint32_t)(a.goff[i + 1] - st);
-        }
-      }
-      uint32_t x = sz;
-#pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-        if (lane >= o) x += y;
-      }
-      const uint32_t pos = M + x - sz;
-      const uint32_t ne = __ballot_sync(kFullMask, sz > 0);
-      if (sz > 0) {
-        nbase[nne + __popc(ne & lanemask_lt_q())] = st - pos;
-        atomicOr(&bmap[pos >> 5], 1u << (pos & 31));
-      }
-      nne += __popc(ne);
-      M += __shfl_sync(kFullMask, x, 31);
-    }
-    __syncwarp();
-    QPROF_MARK(0);
-
-    // ---- Q2: gather + count.  Position p belongs to the (#starts <= p)-th non-empty
-    //      bucket: one bitmap word and a popc per 32 positions.  The count table is
-    //      bucketized: an id hashes to a 16-byte group of slots that fill left to right,
-    //      so one vector load answers "present / where to insert".  The main loop makes
-    //      exactly one probe per candidate (4 group loads in flight per lane); the few
-    //      candidates whose first group is full, or whose slot was just taken by another
-    //      id, are queued and inserted by the full probe loop (insert_slow).  An id is
-    //      always either in its first group or that group is full, so both paths agree. ----
-    uint32_t before = 0, mymax = 0, D = 0, qn = 0;
-    uint32_t* queue = reinterpret_cast<uint32_t*>(outbuf);  // free until Q3b
-    constexpr uint32_t QCAP = kp2 * sizeof(E) / 4;
-    auto bump = [&](uint32_t c) {  // an existing entry went from count c to c+1
-      atomicSub(&hcnt[c < L ? c : L], 1u);
-      atomicAdd(&hcnt[c + 1 < L ? c + 1 : L], 1u);
-    };
-    auto insert_slow = [&](uint32_t id) -> bool {  // full linear probe over groups
-      uint32_t g = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
-      while (true) {
-        E e[T::kPerVec];
-        T::get(tabv[g], e);
-        int hit = -1, emp = -1;
-#pragma unroll
-        for (int i = T::kPerVec - 1; i >= 0; --i) {
-          if (e[i] == T::kE) emp = i;
-          else if (T::id(e[i]) == id) hit = i;
-        }
-        if (hit < 0 && emp >= 0) {
-          const E old = atomicCAS(&tab[g * T::kPerVec + emp], T::kE, T::make(id));
-          if (old == T::kE) return true;
-          if (T::id(old) != id) continue;  // lost the slot to another id: re-read the group
-          hit = emp;
-        }
-        if (hit >= 0) {
-          bump(T::count(atomicAdd(&tab[g * T::kPerVec + hit], (E)1)));
-          return false;
-        }
-        g = (g + 1) & GMASK;  // group full: next group
-      }
-    };
-    auto flush = [&]() {
-      for (uint32_t j0 = 0; j0 < qn; j0 += 32) {
-        const bool f = (j0 + lane < qn) && insert_slow(queue[j0 + lane]);
-        const uint32_t nf = __popc(__ballot_sync(kFullMask, f));
-        if (lane == 0 && nf) atomicAdd(&hcnt[1], nf);
-        D += nf;
-      }
-      qn = 0;
-      __syncwarp();
-    };
-    for (uint32_t r0 = 0; r0 < M; r0 += 128) {
-      uint32_t idv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t w0 = (r0 >> 5) + u;
-        const uint32_t w = bmap[w0];
-        const uint32_t p = r0 + u * 32 + lane;
-        const uint32_t ti = before + __popc(w & lanemask_le_q()) - 1;
-        idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
-        before += __popc(w);
-      }
-      uint32_t gv[4];
-      V ev[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t id = idv[u] != excl ? idv[u] : kEmpty;
-        idv[u] = id;
-        mymax = (id != kEmpty && id > mymax) ? id : mymax;
-        gv[u] = (id * 0x9E3779B1u) >> (32 - (LOG2S - T::kLog2Per));
-        if (id != kEmpty) ev[u] = tabv[gv[u]];  // the group as of this step (re-checked by CAS)
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t id = idv[u];
-        bool fresh = false, defer = false;
-        if (id != kEmpty) {
-          E e[T::kPerVec];
-          T::get(ev[u], e);
-          int hit = -1, emp = -1;
-#pragma unroll
-          for (int i = T::kPerVec - 1; i >= 0; --i) {
-            if (e[i] == T::kE) emp = i;
-            else if (T::id(e[i]) == id) hit = i;
-          }
-          const uint32_t base_slot = gv[u] * T::kPerVec;
-          if (hit < 0 && emp >= 0) {
-            const E old = atomicCAS(&tab[base_slot + emp], T::kE, T::make(id));
-            if (old == T::kE) fresh = true;
-            else if (T::id(old) == id) hit = emp;
-            else defer = true;
-          } else if (hit < 0) {
-            defer = true;  // first group full
-          }
-          if (hit >= 0) bump(T::count(atomicAdd(&tab[base_slot + hit], (E)1)));
-        }
-        const uint32_t nf = __popc(__ballot_sync(kFullMask, fresh));
-        if (lane == 0 && nf) atomicAdd(&hcnt[1], nf);
-        D += nf;
-        const uint32_t dm = __ballot_sync(kFullMask, defer);
-        if (defer) queue[qn + __popc(dm & lanemask_lt_q())] = id;
-        qn += __popc(dm);
-        if (qn + 32 > QCAP) flush();
-      }
-    }
-    flush();
-#pragma unroll
-    for (uint32_t o = 16; o > 0; o >>= 1) {
-      const uint32_t y = __shfl_xor_sync(kFullMask, mymax, o);
-      mymax = y > mymax ? y : mymax;
-    }
-    for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
-    __syncwarp();
-    QPROF_MARK(1);
-
-    // ---- Q3a: threshold count c* from the histogram ----
-    uint32_t cstar = 0, need = 0, ties = 0;
-    if (D > k) {
-      const uint32_t cs = (L + 31) / 32;
-      const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
-      const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
-      uint32_t sum = 0;
-      for (int32_t c = hi; c >= lo; --c) sum += hcnt[c];
-      uint32_t x = sum;
-#pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-        if (lane >= o) x += y;
-      }
-      const uint32_t bef = x - sum;
-      const uint32_t hit = __ballot_sync(kFullMask, bef < k && x >= k);
-      const uint32_t src = __ffs(hit) - 1;
-      if (lane == src) {
-        uint32_t cum = bef;
-        for (int32_t c = hi; c >= lo; --c) {
-          if (cum + hcnt[c] >= k) {
-            cstar = (uint32_t)c;
-            need = k - cum;
-            ties = hcnt[c];
-            break;
-          }
-          cum += hcnt[c];
-        }
-      }
-      cstar = __shfl_sync(kFullMask, cstar, src);
-      need = __shfl_sync(kFullMask, need, src);
-      ties = __shfl_sync(kFullMask, ties, src);
-    }
-    __syncwarp();
-    for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
-    const bool cut = cstar > 0 && need < ties;  // the c* ties must be cut by id
-    QPROF_MARK(2);
-
-    // ---- Q3b: one pass over the table: counts above c* (and all ties when no cut is
-    //      needed) go to the output buffer; the tied ids are compacted in place to the
-    //      front of the table (writes never pass the current read position).  Each lane
-    //      classifies its vector, one packed warp scan gives both write offsets. ----
-    uint32_t nout = 0, ntie = 0;
-    for (uint32_t v0 = 0; v0 < NV; v0 += 32) {
-      E e[T::kPerVec];
-      T::get(tabv[v0 + lane], e);
-      uint32_t om = 0, tm = 0;  // per-entry flags
-#pragma unroll
-      for (int i = 0; i < T::kPerVec; ++i) {
-        const uint32_t c = e[i] != T::kE ? T::count(e[i]) : 0u;
-        if (c > cstar || (c == cstar && c > 0 && !cut)) om |= 1u << i;
-        if (cut && c == cstar) tm |= 1u << i;
-      }
-      const uint32_t packed = __popc(om) | (__popc(tm) << 16);
-      uint32_t x = packed;
-#pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-        if (lane >= o) x += y;
-      }
-      const uint32_t tot = __shfl_sync(kFullMask, x, 31);
-      uint32_t po = nout + ((x - packed) & 0xFFFFu), pt = ntie + ((x - packed) >> 16);
-      __syncwarp();  // every lane has read its vector before any tie id overwrites it
-#pragma unroll
-      for (int i = 0; i < T::kPerVec; ++i) {
-        if (om & (1u << i)) outbuf[po++] = T::key(e[i]);
-        if (tm & (1u << i)) tie[pt++] = T::id(e[i]);
-      }
-      nout += tot & 0xFFFFu;
-      ntie += tot >> 16;
-    }
-    __syncwarp();
-    QPROF_MARK(3);
-
-    // ---- Q3c: keep the `need` smallest tied ids (radix select over the compacted ties,
-    //      8-bit digits from the top set bit, stops when a digit bucket is taken whole) ----
-    if (cut) {
-      const uint32_t hb = 31 - __clz(mymax | 1u);
-      uint32_t width = hb + 1 < 8 ? hb + 1 : 8;
-      int32_t shift = (int32_t)(hb + 1 - width);
-      uint32_t pmask = 0, prefix = 0, theta = 0;
-      while (true) {
-        for (uint32_t d = lane; d < 256; d += 32) hrad[d] = 0;
-        __syncwarp();
-        const uint32_t dmask = (1u << width) - 1;
-        for (uint32_t j = lane; j < ntie; j += 32) {
-          const uint32_t id = tie[j];
-          if ((id & pmask) == prefix) atomicAdd(&hrad[(id >> shift) & dmask], 1u);
-        }
-        __syncwarp();
-        uint32_t sum = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sum += hrad[lane * 8 + i];
-        uint32_t x = sum;
-#pragma unroll
-        for (uint32_t o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-          if (lane >= o) x += y;
-        }
-        const uint32_t bef = x - sum;
-        const uint32_t hit = __ballot_sync(kFullMask, bef < need && x >= need);
-        const uint32_t src = __ffs(hit) - 1;
-        uint32_t d = 0, cum = 0, hd = 0;
-        if (lane == src) {
-          cum = bef;
-          d = lane * 8;
-          for (int i = 0; i < 7; ++i, ++d) {
-            if (cum + hrad[d] >= need) break;
-            cum += hrad[d];
-          }
-          hd = hrad[d];
-        }
-        d = __shfl_sync(kFullMask, d, src);
-        cum = __shfl_sync(kFullMask, cum, src);
-        hd = __shfl_sync(kFullMask, hd, src);
-        __syncwarp();
-        need -= cum;
-        prefix |= d << shift;
-        if (hd == need || shift == 0) {
-          theta = prefix | ((1u << shift) - 1u);
-          break;
-        }
-        pmask |= dmask << shift;
-        width = shift >= 8 ? 8u : (uint32_t)shift;
-        shift -= (int32_t)width;
-      }
-      for (uint32_t j0 = 0; j0 < ntie; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const uint32_t id = j < ntie ? tie[j] : 0xFFFFFFFFu;
-        const bool keep = j < ntie && id <= theta;
-        const uint32_t m = __ballot_sync(kFullMask, keep);
-        if (keep) outbuf[nout + __popc(m & lanemask_lt_q())] = T::key(T::make(id) - 1 + cstar);
-        nout += __popc(m);
-      }
-    }
-    __syncwarp();
-    QPROF_MARK(4);
-    for (uint32_t j = lane; j < NV; j += 32) tabv[j] = T::empty_vec();
-    QPROF_MARK(5);
-
-    // ---- Q3d: order by (count desc, id asc), write, pad ----
-    uint32_t* oid = a.out_ids + q * k;
-    uint32_t* ocnt = a.out_counts + q * k;
-    __syncwarp();
-    warp_sort_keys<KP, E>(outbuf, nout, oid, ocnt);
-    for (uint32_t j = nout + lane; j < k; j += 32) {
-      oid[j] = kEmpty;
-      ocnt[j] = 0;
-    }
-    __syncwarp();
-    QPROF_MARK(6);
-  }
-}
-
 size_t class_smem(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
   uint32_t kp2 = 1;
   while (kp2 < k) kp2 <<= 1;
@@ -957,35 +486,6 @@ int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count
   if (grid > a.nq) grid = a.nq;
   k_query<LOG2S, NT><<<(unsigned)grid, NT, smem, s>>>(a, list, count, hist_len);
   return 1;
-}
-
-template <int LOG2S, typename E, int KP>
-int launch_warp_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
-  constexpr int kWarps = 4;
-  const size_t smem = warp2_slice_bytes(LOG2S, sizeof(E), a.L, a.k) * kWarps;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query_warp<LOG2S, E, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return 0;
-    attr = smem;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_warp<LOG2S, E, KP>, 32 * kWarps, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = 148ull * per_sm;
-  const uint64_t need = (a.nq + kWarps - 1) / kWarps;
-  if (grid > need) grid = need;
-  k_query_warp<LOG2S, E, KP><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count);
-  return 1;
-}
-
-template <int LOG2S, typename E>
-int launch_warp_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
-  if (a.k <= 32) return launch_warp_t<LOG2S, E, 1>(a, list, count, s);
-  if (a.k <= 64) return launch_warp_t<LOG2S, E, 2>(a, list, count, s);
-  if (a.k <= 128) return launch_warp_t<LOG2S, E, 4>(a, list, count, s);
-  return launch_warp_t<LOG2S, E, 8>(a, list, count, s);
 }
 
 }  // namespace
@@ -1016,30 +516,15 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, lists, counts, a.err);
   const uint32_t hist_len = (a.L + 1) > 1024 ? a.L + 1 : 1024;
   int n = 1;
-  if (a.k <= 256 && a.packed) {  // one query per warp, (id, count) packed in u32
-    n += launch_warp_class<11, uint32_t>(a, lists, counts + 0, s);
-    if (a.table_log2 >= 12) n += launch_warp_class<12, uint32_t>(a, lists + a.nq, counts + 1, s);
-  } else if (a.k <= 256) {  // one query per warp, u64 entries
-    n += launch_warp_class<11, unsigned long long>(a, lists, counts + 0, s);
-    if (a.table_log2 >= 12) n += launch_warp_class<12, unsigned long long>(a, lists + a.nq, counts + 1, s);
-  } else {
-    n += launch_class<11, 128>(a, lists, counts + 0, hist_len, s);
-    if (a.table_log2 >= 12) n += launch_class<12, 128>(a, lists + a.nq, counts + 1, hist_len, s);
-  }
-  if (a.table_log2 >= 13) n += launch_class<13, 256>(a, lists + 2 * a.nq, counts + 2, hist_len, s);
-  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 3 * a.nq, counts + 3, hist_len, s);
+  // one query per warp: radix-partition sort of the candidates (query_sort.cu)
+  n += launch_query_sort(a, 1024, lists, counts + 0, s);
+  if (a.table_log2 >= 12) n += launch_query_sort(a, 1536, lists + a.nq, counts + 1, s);
+  if (a.table_log2 >= 12) n += launch_query_sort(a, 3072, lists + 2 * a.nq, counts + 2, s);
+  // one query per CTA with a shared-memory hash count table (this file)
+  if (a.table_log2 >= 13) n += launch_class<13, 256>(a, lists + 3 * a.nq, counts + 3, hist_len, s);
+  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 4 * a.nq, counts + 4, hist_len, s);
   return n;
 }
 
 }  // namespace flash
 
-#ifdef FLASH_QPROF
-extern "C" int flash_debug_qprof(unsigned long long out[8], int reset) {
-  if (cudaMemcpyFromSymbol(out, flash::g_qprof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
-  if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(flash::g_qprof, z, sizeof z);
-  }
-  return 0;
-}
-#endif

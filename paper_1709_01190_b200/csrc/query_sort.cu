@@ -1,0 +1,366 @@
+// query_sort.cu — Q1-Q3 by radix partition: one warp owns one query at a time (sm_100a).
+//
+// COUNTFREQUENCY (Alg. 3) needs equal candidate ids brought together.  The
+// L addressed buckets hold M ~ 1K ids, so a warp sorts them in shared memory:
+//   Q1 gather   the non-empty buckets of the query are located by a bitmap over the
+//               flattened candidate positions (one word + popc per 32 positions).
+//   Q2 sort     pass A counts the candidates per digit (the top 10 significant bits of
+//               the id range), a warp scan turns counts into bin offsets, pass B gathers
+//               again and scatters each id into its bin; each lane then insertion-sorts
+//               the 32 bins it owns (a bin spans a narrow id range, so inversions are
+//               few).  The array is now sorted by id.
+//   Q3 count    run lengths of equal ids are the full multiplicities (R#11), found with
+//   + top-k     a ballot of run starts per 32 elements; a histogram of the counts (<= L)
+//               gives the threshold count c*; because the distinct ids come in ascending
+//               order, the ids tied at c* that survive are the first `need` of them (ties
+//               by ascending id, R#12); ids with count > c* go to per-count output cursors
+//               (higher counts first, ids ascending within a count), the ties after them.
+//               No final sort is needed.  Pads are (EMPTY, 0) (R#13).  The excluded id
+//               (self, R#14) is dropped at the gather.
+// No hash table, no probing, no CAS: two shared-memory atomics per candidate.
+#include "flash_internal.cuh"
+
+namespace flash {
+namespace {
+
+constexpr uint32_t kFullS = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t lanemask_lt_s() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t lanemask_le_s() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+
+__host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins, uint32_t L) {
+  size_t b = (size_t)mcap * 4            // ids, sorted in place by bin
+             + (size_t)(kBins > mcap ? kBins : mcap) * 2  // u16 bin counters, later distinct counts
+             + (size_t)L * 8              // base of each non-empty bucket
+             + ((size_t)mcap / 32 + 2) * 4  // bucket-start bitmap
+             + (size_t)(L + 1) * 4;       // count histogram
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int MCAP, int BINS_LOG2>
+__global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t* __restrict__ qlist,
+                                                   const uint32_t* __restrict__ qcount, uint32_t shift) {
+  constexpr uint32_t NBW = MCAP / 32 + 2;
+  constexpr uint32_t kBins = 1u << BINS_LOG2;
+  extern __shared__ __align__(16) uint8_t sms[];
+  const uint32_t L = a.L, k = a.k;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* my = sms + sort_slice_bytes(MCAP, kBins, L) * wib;
+  uint32_t* arr = reinterpret_cast<uint32_t*>(my);                  // [MCAP]
+  uint32_t* binw = arr + MCAP;                                      // [kBins/2] packed u16
+  constexpr uint32_t CW = (kBins > MCAP ? kBins : MCAP) / 2;        // words of the u16 area
+  uint64_t* nbase = reinterpret_cast<uint64_t*>(binw + CW);         // [L]
+  uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);          // [NBW]
+  uint32_t* hcnt = bmap + NBW;                                      // [L+1]
+  const uint16_t* bin16 = reinterpret_cast<const uint16_t*>(binw);
+  const uint32_t* __restrict__ gids = a.ids;
+
+  for (uint32_t j = lane; j < kBins / 2; j += 32) binw[j] = 0;
+  for (uint32_t j = lane; j < NBW; j += 32) bmap[j] = 0;
+  for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+  __syncwarp();
+
+  const uint32_t nq = *qcount;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t it = gw; it < nq; it += nw) {
+    const uint64_t q = qlist[it];
+    const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
+
+    // ---- Q1: non-empty buckets in table order: start bitmap + bases ----
+    uint32_t M = 0, nne = 0;
+    for (uint32_t t0 = 0; t0 < L; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      uint32_t sz = 0;
+      uint64_t st = 0;
+      if (t < L) {
+        const uint32_t ad = a.addrs[q * L + t];
+        if (ad < a.range) {
+          const uint64_t i = (uint64_t)t * a.range + ad;
+          st = a.goff[i];
+          sz = (uint32_t)(a.goff[i + 1] - st);
+        }
+      }
+      uint32_t x = sz;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullS, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t pos = M + x - sz;
+      const uint32_t ne = __ballot_sync(kFullS, sz > 0);
+      if (sz > 0) {
+        nbase[nne + __popc(ne & lanemask_lt_s())] = st - pos;
+        atomicOr(&bmap[pos >> 5], 1u << (pos & 31));
+      }
+      nne += __popc(ne);
+      M += __shfl_sync(kFullS, x, 31);
+    }
+    __syncwarp();
+
+    // ---- Q2a: count candidates per digit ----
+    {
+      uint32_t before = 0;
+      for (uint32_t r0 = 0; r0 < M; r0 += 128) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w = bmap[(r0 >> 5) + u];
+          const uint32_t p = r0 + u * 32 + lane;
+          const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
+          idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
+          before += __popc(w);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          if (id != kEmpty && id != excl) {
+            const uint32_t d = (id >> shift) & (kBins - 1);
+            atomicAdd(&binw[d >> 1], 1u << ((d & 1) * 16));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // exclusive scan of the kBins counters (lane owns kBins/32 consecutive bins, 2 per word)
+    constexpr uint32_t WPL = kBins / 64;  // words per lane
+    uint32_t mtot;
+    {
+      uint32_t sum = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < WPL; ++i) {
+        const uint32_t w = binw[lane * WPL + i];
+        sum += (w & 0xFFFFu) + (w >> 16);
+      }
+      uint32_t x = sum;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullS, x, o);
+        if (lane >= o) x += y;
+      }
+      mtot = __shfl_sync(kFullS, x, 31);
+      uint32_t run = x - sum;
+#pragma unroll
+      for (uint32_t i = 0; i < WPL; ++i) {
+        const uint32_t w = binw[lane * WPL + i];
+        const uint32_t c0 = w & 0xFFFFu, c1 = w >> 16;
+        binw[lane * WPL + i] = run | ((run + c0) << 16);
+        run += c0 + c1;
+      }
+    }
+    __syncwarp();
+
+    // ---- Q2b: gather again, scatter into bins ----
+    {
+      uint32_t before = 0;
+      for (uint32_t r0 = 0; r0 < M; r0 += 128) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w = bmap[(r0 >> 5) + u];
+          const uint32_t p = r0 + u * 32 + lane;
+          const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
+          idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
+          before += __popc(w);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          if (id != kEmpty && id != excl) {
+            const uint32_t d = (id >> shift) & (kBins - 1);
+            const uint32_t old = atomicAdd(&binw[d >> 1], 1u << ((d & 1) * 16));
+            arr[(old >> ((d & 1) * 16)) & 0xFFFFu] = id;
+          }
+        }
+      }
+    }
+    for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
+    __syncwarp();
+    // bin d now ends at bin16[d]; each lane insertion-sorts the range of the kBins/32
+    // bins it owns (a bin spans 2^shift ids and holds ~M/kBins of them: few inversions)
+    {
+      constexpr uint32_t BPL = kBins / 32;
+      const uint32_t lo = lane == 0 ? 0u : bin16[lane * BPL - 1];
+      const uint32_t hi = bin16[lane * BPL + BPL - 1];
+      uint32_t prev = lo < hi ? arr[lo] : 0u;
+      for (uint32_t i = lo + 1; i < hi; ++i) {
+        const uint32_t x = arr[i];
+        if (x >= prev) {  // already in order (the common case)
+          prev = x;
+          continue;
+        }
+        uint32_t j = i;
+        while (j > lo && arr[j - 1] > x) {
+          arr[j] = arr[j - 1];
+          --j;
+        }
+        arr[j] = x;
+      }
+    }
+    __syncwarp();
+
+    // ---- Q3a: run lengths.  Distinct ids are compacted in place to arr[0..nd) (a run's
+    //      write index never exceeds its end index) with their counts in cnt16 (the bin
+    //      counters are done); the count histogram is built on the way. ----
+    uint16_t* cnt16 = reinterpret_cast<uint16_t*>(binw);
+    uint32_t nd = 0;
+    {
+      uint32_t carry = 0;  // start index of the run open at the chunk boundary
+      for (uint32_t i0 = 0; i0 < mtot; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint32_t x = i < mtot ? arr[i] : kEmpty;
+        const bool start = i < mtot && (i == 0 || arr[i - 1] != x);
+        const bool end = i < mtot && (i + 1 == mtot || arr[i + 1] != x);
+        const uint32_t sm = __ballot_sync(kFullS, start);
+        const uint32_t em = __ballot_sync(kFullS, end);
+        const uint32_t below = sm & lanemask_le_s();
+        const uint32_t st = below ? i0 + 31 - __clz(below) : carry;
+        __syncwarp();  // all reads of this chunk precede the compaction writes
+        if (end) {
+          const uint32_t c = i - st + 1;
+          const uint32_t d = nd + __popc(em & lanemask_lt_s());
+          arr[d] = x;
+          cnt16[d] = (uint16_t)c;
+          atomicAdd(&hcnt[c < L ? c : L], 1u);
+        }
+        nd += __popc(em);
+        if (sm) carry = i0 + 31 - __clz(sm);
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+
+    // ---- Q3b: threshold count c*, how many ties to keep, how many counts above c*; the
+    //      histogram becomes the output cursor of each count above c* (higher counts first) ----
+    uint32_t cstar = 0, need = 0xFFFFFFFFu, nhi = nd;
+    {
+      const uint32_t cs = (L + 31) / 32;
+      const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
+      const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
+      uint32_t sum = 0;
+      for (int32_t c = hi; c >= lo; --c) sum += hcnt[c];
+      uint32_t x = sum;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullS, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t bef = x - sum;
+      if (nd > k) {
+        const uint32_t hit = __ballot_sync(kFullS, bef < k && x >= k);
+        const uint32_t src = __ffs(hit) - 1;
+        if (lane == src) {
+          uint32_t cum = bef;
+          for (int32_t c = hi; c >= lo; --c) {
+            if (cum + hcnt[c] >= k) {
+              cstar = (uint32_t)c;
+              need = k - cum;
+              nhi = cum;
+              break;
+            }
+            cum += hcnt[c];
+          }
+        }
+        cstar = __shfl_sync(kFullS, cstar, src);
+        need = __shfl_sync(kFullS, need, src);
+        nhi = __shfl_sync(kFullS, nhi, src);
+      }
+      __syncwarp();
+      uint32_t cur = bef;  // exclusive prefix in descending count order
+      for (int32_t c = hi; c >= lo; --c) {
+        const uint32_t h = hcnt[c];
+        hcnt[c] = cur;
+        cur += h;
+      }
+    }
+    __syncwarp();
+
+    // ---- Q3c: one pass over the distinct ids in ascending order: a count above c* is
+    //      written at its count's cursor (so equal counts stay in id order); the first
+    //      `need` ids tied at c* follow all of them ----
+    uint32_t* oid = a.out_ids + q * k;
+    uint32_t* ocnt = a.out_counts + q * k;
+    uint32_t nh = 0, nt = 0;
+    for (uint32_t d0 = 0; d0 < nd && (nt < need || nh < nhi); d0 += 32) {
+      const uint32_t d = d0 + lane;
+      const uint32_t c = d < nd ? cnt16[d] : 0u;
+      const uint32_t x = d < nd ? arr[d] : 0u;
+      const bool up = c > cstar;
+      const bool tie = cstar > 0 && c == cstar;
+      uint32_t um = __ballot_sync(kFullS, up);
+      nh += __popc(um);
+      while (um) {  // one group per distinct count in this chunk (usually 0-2)
+        const uint32_t c0 = __shfl_sync(kFullS, c, __ffs(um) - 1);
+        const uint32_t m = __ballot_sync(kFullS, up && c == c0);
+        const uint32_t base = hcnt[c0 < L ? c0 : L];
+        if (up && c == c0) {
+          const uint32_t pos = base + __popc(m & lanemask_lt_s());
+          oid[pos] = x;
+          ocnt[pos] = c;
+        }
+        __syncwarp();
+        if (lane == 0) hcnt[c0 < L ? c0 : L] = base + __popc(m);
+        __syncwarp();
+        um &= ~m;
+      }
+      const uint32_t mt = __ballot_sync(kFullS, tie);
+      const uint32_t rank = nt + __popc(mt & lanemask_lt_s());
+      if (tie && rank < need) {
+        oid[nhi + rank] = x;
+        ocnt[nhi + rank] = c;
+      }
+      nt += __popc(mt);
+    }
+    __syncwarp();
+    if (nt > need) nt = need;
+    for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+    for (uint32_t j = lane; j < kBins / 2; j += 32) binw[j] = 0;
+    for (uint32_t j = nhi + nt + lane; j < k; j += 32) {
+      oid[j] = kEmpty;
+      ocnt[j] = 0;
+    }
+    __syncwarp();
+  }
+}
+
+template <int MCAP, int BL>
+int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+  constexpr int kWarps = 4;
+  // digit = the top BL bits of the id range [0, max_id]
+  const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
+  const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
+  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L) * kWarps;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_query_sort<MCAP, BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return 0;
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL>, 32 * kWarps, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = 148ull * per_sm;
+  const uint64_t need = (a.nq + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
+  k_query_sort<MCAP, BL><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count, shift);
+  return 1;
+}
+
+}  // namespace
+
+int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
+                      cudaStream_t s) {
+  if (mcap <= 1024) return launch_sort_t<1024, 10>(a, list, count, s);
+  if (mcap <= 1536) return launch_sort_t<1536, 11>(a, list, count, s);
+  return launch_sort_t<3072, 11>(a, list, count, s);
+}
+
+}  // namespace flash
