@@ -108,6 +108,7 @@ struct flash_index {
   cudaEvent_t order_ev = nullptr;
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> copy_events;
+
   // profiling
   int profiling = 0;
   std::vector<PendingPhase> pending;
@@ -331,6 +332,7 @@ void flash_destroy(flash_index* h) {
     cudaEventDestroy(p.b);
   }
   for (auto e : h->copy_events) cudaEventDestroy(e);
+
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   cudaFree(h->arrivals);
   cudaFree(h->err);

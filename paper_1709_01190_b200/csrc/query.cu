@@ -38,10 +38,15 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
   return m;
 }
 
-// Query size classes by M (candidates): <= 1024, <= 1536 and <= 3072 run one query per
-// warp (query_sort.cu; smaller classes use less shared memory, so more warps per SM);
-// <= 4096 and <= 8192 run one query per CTA with 2^13 / 2^14 count slots (below).
-constexpr int kClasses = 5;
+// Query size classes by M (candidates): the first kSortClasses run one query per warp
+// (query_sort.cu; a smaller class uses less shared memory per warp, so more warps per
+// SM); M <= 4096 and <= 8192 run one query per CTA with 2^13 / 2^14 count slots (below).
+constexpr int kSortClasses = 6;
+__host__ __device__ constexpr uint32_t class_max(int c) {
+  return c == 0 ? 768u : c == 1 ? 1024u : c == 2 ? 1280u : c == 3 ? 1536u : c == 4 ? 2048u
+         : c == 5 ? 3072u : c == 6 ? 4096u : 8192u;
+}
+constexpr int kClasses = kSortClasses + 2;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              uint32_t L, uint32_t range, uint32_t* __restrict__ lists,
@@ -62,7 +67,8 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
         }
       }
     }
-    const int cls = M <= 1024 ? 0 : (M <= 1536 ? 1 : (M <= 3072 ? 2 : (M <= 4096 ? 3 : 4)));
+    int cls = 0;
+    while (cls < kClasses - 1 && M > class_max(cls)) ++cls;
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) {
       const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
@@ -515,14 +521,18 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, lists, counts, a.err);
   const uint32_t hist_len = (a.L + 1) > 1024 ? a.L + 1 : 1024;
+  // The class kernels are persistent over their device-side query lists and run back to
+  // back on the caller's stream (measured: overlapping them on side streams is slower,
+  // since kernels with different shared-memory footprints then share the SMs).
+  const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
   int n = 1;
-  // one query per warp: radix-partition sort of the candidates (query_sort.cu)
-  n += launch_query_sort(a, 1024, lists, counts + 0, s);
-  if (a.table_log2 >= 12) n += launch_query_sort(a, 1536, lists + a.nq, counts + 1, s);
-  if (a.table_log2 >= 12) n += launch_query_sort(a, 3072, lists + 2 * a.nq, counts + 2, s);
-  // one query per CTA with a shared-memory hash count table (this file)
-  if (a.table_log2 >= 13) n += launch_class<13, 256>(a, lists + 3 * a.nq, counts + 3, hist_len, s);
-  if (a.table_log2 >= 14) n += launch_class<14, 256>(a, lists + 4 * a.nq, counts + 4, hist_len, s);
+  for (int c = 0; c < kClasses; ++c) {
+    if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
+    const uint32_t* lc = lists + (uint64_t)c * a.nq;
+    if (c < kSortClasses) n += launch_query_sort(a, class_max(c), lc, counts + c, s);
+    else if (c == kSortClasses) n += launch_class<13, 256>(a, lc, counts + c, hist_len, s);
+    else n += launch_class<14, 256>(a, lc, counts + c, hist_len, s);
+  }
   return n;
 }
 

@@ -358,8 +358,11 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
 
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
                       cudaStream_t s) {
+  if (mcap <= 768) return launch_sort_t<768, 10>(a, list, count, s);
   if (mcap <= 1024) return launch_sort_t<1024, 10>(a, list, count, s);
+  if (mcap <= 1280) return launch_sort_t<1280, 10>(a, list, count, s);
   if (mcap <= 1536) return launch_sort_t<1536, 11>(a, list, count, s);
+  if (mcap <= 2048) return launch_sort_t<2048, 11>(a, list, count, s);
   return launch_sort_t<3072, 11>(a, list, count, s);
 }
 
