@@ -183,25 +183,29 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     }
     for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
     __syncwarp();
-    // bin d now ends at bin16[d]; each lane insertion-sorts the range of the kBins/32
-    // bins it owns (a bin spans 2^shift ids and holds ~M/kBins of them: few inversions)
+    // bin d now ends at bin16[d]; each lane sorts the range of the kBins/32 bins it owns.
+    // A bin spans 2^shift ids and holds ~M/kBins of them, so the range is nearly sorted:
+    // bubble passes (no inner loop, hence no divergence) until no lane swaps.
     {
       constexpr uint32_t BPL = kBins / 32;
       const uint32_t lo = lane == 0 ? 0u : bin16[lane * BPL - 1];
       const uint32_t hi = bin16[lane * BPL + BPL - 1];
-      uint32_t prev = lo < hi ? arr[lo] : 0u;
-      for (uint32_t i = lo + 1; i < hi; ++i) {
-        const uint32_t x = arr[i];
-        if (x >= prev) {  // already in order (the common case)
-          prev = x;
-          continue;
+      bool swapped = hi > lo + 1;
+      while (__any_sync(kFullS, swapped)) {
+        swapped = false;
+        if (hi > lo + 1) {
+          uint32_t big = arr[lo];  // the largest value seen in this pass
+          for (uint32_t i = lo + 1; i < hi; ++i) {
+            const uint32_t x = arr[i];
+            if (big > x) {
+              arr[i - 1] = x;
+              arr[i] = big;
+              swapped = true;
+            } else {
+              big = x;
+            }
+          }
         }
-        uint32_t j = i;
-        while (j > lo && arr[j - 1] > x) {
-          arr[j] = arr[j - 1];
-          --j;
-        }
-        arr[j] = x;
       }
     }
     __syncwarp();
