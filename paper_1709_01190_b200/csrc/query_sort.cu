@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         uint32_t idv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t w = bmap[(r0 >> 5) + u];
+          const uint32_t w = r0 + u * 32 < M ? bmap[(r0 >> 5) + u] : 0u;  // stay inside the slice
           const uint32_t p = r0 + u * 32 + lane;
           const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
           idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         uint32_t idv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t w = bmap[(r0 >> 5) + u];
+          const uint32_t w = r0 + u * 32 < M ? bmap[(r0 >> 5) + u] : 0u;  // stay inside the slice
           const uint32_t p = r0 + u * 32 + lane;
           const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
           idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         }
       }
     }
+    __syncwarp();  // every lane is done reading the bitmap (independent thread scheduling)
     for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
     __syncwarp();
     // bin d now ends at bin16[d]; each lane sorts the range of the kBins/32 bins it owns.

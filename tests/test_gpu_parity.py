@@ -304,3 +304,19 @@ def test_full_webspam_graph_sampled_parity():
     o_ids, o_cnt = oracle.query(T, o_addrs[sample], k, exclude=sample.astype(np.uint32))
     assert np.array_equal(flash.as_u32(g_ids)[sample], o_ids)
     assert np.array_equal(flash.as_u32(g_cnt)[sample], o_cnt)
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool):
+    """compute-sanitizer finds no memory errors / shared-memory races on small graphs
+    (tools/sanitize_run.py: tiny, webspam, url shapes plus the edge-case rows)."""
+    import shutil
+    import subprocess
+    import sys
+
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(root, "tools", "sanitize_run.py")],
+                       capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
