@@ -13,7 +13,8 @@ R=128, range=2^15, k=128 (synthetic, synth/ seed 2).
 device-timed with CUDA events, max over ranks.  `e2e` = the same metric through
 flash_knn_graph_host (pinned host CSR in, host top-k out, copies inside the timed
 region).  N>1: one rank per GPU (torchrun), replicated tables (paper_1709_01190_b200
-/dist.py), strong scaling of the fixed graph.
+/dist.py knn_graph_sharded_build: row-sharded hash and query, table-sharded build,
+built tables all-gathered), strong scaling of the fixed graph.
 
 The reference arm (--impl reference) and `cpu_baseline` time the CPU oracle (oracle/)
 as it stands on the host cores (OpenMP, all cores) on the same workload: hash + build
@@ -72,7 +73,8 @@ def workload_config(shape, nnz, args):
         "workload": "webspam-shaped approximate k-NN graph from scratch (hash + build + query every row)",
         "N": shape.N, "D": shape.D, "nnz": int(nnz), "nnz_per_row": round(nnz / shape.N, 1),
         "K": K, "L": L, "R": R, "range": RANGE, "k": TOPK, "seed": SEED,
-        "parallelism": f"replicated-tables x{args.gpus}" if args.gpus > 1 else "1 GPU",
+        "parallelism": (f"rows x{args.gpus} (hash, query); tables x{args.gpus} (build); "
+                        "all-gather addresses + built tables") if args.gpus > 1 else "1 GPU",
         "l2_policy": "inputs larger than L2 (col_idx 5.2 GB vs 126 MB L2); no flush",
     }
 
@@ -163,9 +165,17 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # FLASH_BENCH_ONE_GPU=1 (debug only): every rank on cuda:0 over gloo, to exercise the
+    # multi-rank path on a 1-GPU box; its timings mean nothing.
+    one_gpu = os.environ.get("FLASH_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = synth.SHAPES["webspam"]
     t0 = time.time()
     all_lens = np.empty(shape.N, dtype=np.int64)
@@ -191,7 +201,7 @@ def run_ours(args):
         if world == 1:
             flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, TOPK, out_ids, out_cnt)
             return out_ids, out_cnt
-        return fdist.knn_graph_replicated(idx, d_rp, d_col, TOPK, bounds, rank)
+        return fdist.knn_graph_sharded_build(idx, d_rp, d_col, TOPK, bounds, rank)
 
     for _ in range(args.warmup):
         step()
@@ -238,7 +248,7 @@ def run_ours(args):
         else:
             d_rp2 = h_rp_local.to(dev, non_blocking=True)
             d_col2 = h_col.to(dev, non_blocking=True)
-            ids_, cnt_ = fdist.knn_graph_replicated(idx, d_rp2, d_col2, TOPK, bounds, rank)
+            ids_, cnt_ = fdist.knn_graph_sharded_build(idx, d_rp2, d_col2, TOPK, bounds, rank)
             h_ids.copy_(ids_, non_blocking=True)
             h_cnt.copy_(cnt_, non_blocking=True)
             torch.cuda.synchronize()
@@ -255,7 +265,7 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     addrs_np = flash.as_u32(idx.hash_addrs(d_rp, d_col))
-    n_cand = query_work(lambda t: idx.table(t), addrs_np) if world == 1 else None
+    n_cand = query_work(lambda t: idx.table(t), addrs_np)  # this rank's queries
 
     result = None
     if rank == 0:

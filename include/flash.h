@@ -86,6 +86,29 @@ flash_status flash_insert(flash_index *h, const int64_t *row_ptr, const uint32_t
 flash_status flash_insert_addrs(flash_index *h, const uint32_t *addrs, uint64_t n_rows,
                                 uint32_t id_base, void *stream);
 
+/* flash_insert_addrs restricted to tables [t_begin, t_end): the rows' addresses for
+ * other tables are ignored and those tables keep their content.  The multi-GPU graph
+ * (paper_1709_01190_b200/dist.py) builds each GPU's table window with this and then
+ * assembles the full tables on every GPU (flash_table_arrays / flash_import_tables).
+ * The tables of a window are exactly those a full insert would build (bottom-R is
+ * per-bucket; the priority uses the global table index). */
+flash_status flash_insert_addrs_window(flash_index *h, const uint32_t *addrs, uint64_t n_rows,
+                                       uint32_t id_base, uint32_t t_begin, uint32_t t_end,
+                                       void *stream);
+
+/* Device pointers to the whole index: goff [L*range+1] (uint64 absolute offsets: table t,
+ * bucket b holds ids[goff[t*range+b] .. goff[t*range+b+1])), ids [*n_ids], arrivals
+ * [L*range].  Synchronizes the handle's last stream.  Valid until the next insert,
+ * import, clear or destroy.  Before any insert: FLASH_ESTATE. */
+flash_status flash_table_arrays(const flash_index *h, const uint64_t **goff, const uint32_t **ids,
+                                const uint32_t **arrivals, uint64_t *n_ids);
+
+/* Replace the index content with copies of device arrays in flash_table_arrays' layout
+ * (arrivals may be NULL: zeros).  max_id: the largest id the tables hold (ids are
+ * 0..max_id in a k-NN graph).  Stream-ordered. */
+flash_status flash_import_tables(flash_index *h, const uint64_t *goff, const uint32_t *ids, uint64_t n_ids,
+                                 const uint32_t *arrivals, uint32_t max_id, void *stream);
+
 /* Querying phase (Alg. 3) for n_q CSR query rows: aggregate the L addressed
  * buckets, count each candidate's multiplicity (full count, R#11), drop exclude[q] (if
  * exclude != NULL, R#14), order by (count desc, id asc) (R#12), keep k, pad with

@@ -185,7 +185,8 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
 }
 
 flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
-                             cudaStream_t s) {
+                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX) {
+  if (t1 > h->L) t1 = h->L;
   const uint64_t nb = (uint64_t)h->L * h->range;
   const uint64_t pool_cap = h->kept_ub + n * h->L;
   const uint64_t kept_cap = pool_cap < nb * h->R ? pool_cap : nb * h->R;
@@ -210,6 +211,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.L = h->L;
   a.R = h->R;
   a.range = h->range;
+  a.t0 = t0;
+  a.t1 = t1;
   a.keys = h->keys;
   a.goff_old = h->have_tables ? h->goff[h->cur].as<uint64_t>() : nullptr;
   a.ids_old = h->have_tables ? h->ids[h->cur].as<uint32_t>() : nullptr;
@@ -368,6 +371,62 @@ flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t 
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
   return do_insert_addrs(h, addrs, n_rows, id_base, s);
+}
+
+flash_status flash_insert_addrs_window(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
+                                       uint32_t t_begin, uint32_t t_end, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (t_begin > t_end || t_end > h->L) return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(addrs);
+  if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
+    return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  return do_insert_addrs(h, addrs, n_rows, id_base, s, t_begin, t_end);
+}
+
+flash_status flash_table_arrays(const flash_index* hc, const uint64_t** goff, const uint32_t** ids,
+                                const uint32_t** arrivals, uint64_t* n_ids) {
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  if (!h->have_tables) return fail(FLASH_ESTATE, "nothing inserted yet");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+  const uint64_t* g = h->goff[h->cur].as<uint64_t>();
+  uint64_t total = 0;
+  CUDA_TRY(cudaMemcpy(&total, g + (uint64_t)h->L * h->range, sizeof total, cudaMemcpyDeviceToHost));
+  if (goff) *goff = g;
+  if (ids) *ids = h->ids[h->cur].as<uint32_t>();
+  if (arrivals) *arrivals = h->arrivals;
+  if (n_ids) *n_ids = total;
+  return FLASH_OK;
+}
+
+flash_status flash_import_tables(flash_index* h, const uint64_t* goff, const uint32_t* ids, uint64_t n_ids,
+                                 const uint32_t* arrivals, uint32_t max_id, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  REQUIRE_DEV(goff);
+  if (n_ids) REQUIRE_DEV(ids);
+  if (arrivals) REQUIRE_DEV(arrivals);
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  const uint64_t nb = (uint64_t)h->L * h->range;
+  const int nxt = h->have_tables ? 1 - h->cur : h->cur;
+  TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
+  TRY(ensure(h->ids[nxt], sizeof(uint32_t) * (n_ids ? n_ids : 1)));
+  CUDA_TRY(cudaMemcpyAsync(h->goff[nxt].p, goff, sizeof(uint64_t) * (nb + 1), cudaMemcpyDeviceToDevice, s));
+  if (n_ids) CUDA_TRY(cudaMemcpyAsync(h->ids[nxt].p, ids, sizeof(uint32_t) * n_ids, cudaMemcpyDeviceToDevice, s));
+  if (arrivals)
+    CUDA_TRY(cudaMemcpyAsync(h->arrivals, arrivals, sizeof(uint32_t) * nb, cudaMemcpyDeviceToDevice, s));
+  else
+    CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * nb, s));
+  h->cur = nxt;
+  h->have_tables = true;
+  h->kept_ub = n_ids;
+  h->max_id = max_id;
+  h->n_inserted = (uint64_t)max_id + 1;
+  return FLASH_OK;
 }
 
 flash_status flash_insert(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,

@@ -78,6 +78,7 @@ struct BuildArgs {
   uint64_t n;
   uint32_t id_base;
   uint32_t L, R, range;
+  uint32_t t0, t1;  // only tables [t0, t1) receive the new rows (others keep their content)
   HashKeys keys;
   // old tables (null when empty)
   const uint64_t* goff_old;  // [nb+1]

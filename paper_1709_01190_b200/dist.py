@@ -59,3 +59,67 @@ def knn_graph_replicated(index, row_ptr_local, col_idx_local, k: int, bounds: li
     excl = torch.arange(bounds[rank], bounds[rank] + n_local, dtype=torch.int64,
                         device=addrs_local.device).to(torch.int32)
     return index.query_addrs(addrs_local, k, excl)                         # Q1-Q3, own rows
+
+
+def table_window(L: int, world: int, rank: int) -> tuple[int, int]:
+    """Tables [floor(rank*L/world), floor((rank+1)*L/world)) are built by `rank` (R#22 of
+    SURVEY §8(c): floor-block partition; results do not depend on it)."""
+    return (L * rank) // world, (L * (rank + 1)) // world
+
+
+def _gather_var(x: torch.Tensor, sizes: list[int], group=None) -> list[torch.Tensor]:
+    """All-gather 1-D tensors of per-rank length sizes[g] (padded to the max)."""
+    world = len(sizes)
+    m = max(max(sizes), 1)
+    pad = torch.zeros(m, dtype=x.dtype, device=x.device)
+    pad[: x.numel()] = x
+    out = torch.empty(world * m, dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return [out[g * m: g * m + sizes[g]] for g in range(world)]
+
+
+def knn_graph_sharded_build(index, row_ptr_local, col_idx_local, k: int, bounds: list[int], rank: int,
+                            group=None):
+    """Multi-GPU k-NN graph with the table build sharded across GPUs:
+
+    1. rank g hashes its row shard (H1-H3, all L tables);
+    2. X1: the addresses of every row are all-gathered (N*L*4 bytes);
+    3. rank g builds only its table window [t0, t1) over all N rows (B1-B2; bottom-R is
+       per bucket and keyed by the global table index, so a window equals the
+       corresponding tables of a full build);
+    4. X2: the built windows (bucket offsets + kept ids) are all-gathered, and every rank
+       imports the full, identical tables;
+    5. rank g answers its own rows (Q1-Q3) with exclude = global row id.
+    Results are byte-identical to the 1-GPU graph."""
+    world = len(bounds) - 1
+    counts = [bounds[g + 1] - bounds[g] for g in range(world)]
+    n_local = counts[rank]
+    n_total = bounds[-1]
+    L, R = index.L, index.range
+    addrs_local = index.hash_addrs(row_ptr_local, col_idx_local)               # H1-H3
+    addrs_all = all_gather_rows(addrs_local, counts, group)                     # X1
+    t0, t1 = table_window(L, world, rank)
+    index.insert_addrs_window(addrs_all, 0, t0, t1)                            # B1-B2 (own tables)
+    goff, ids, arr = index.table_arrays()
+    lo, hi = int(goff[t0 * R].item()), int(goff[t1 * R].item())
+    rel = goff[t0 * R: t1 * R + 1] - lo                                         # window offsets
+    my_ids = ids[lo:hi]
+    wsizes = [(table_window(L, world, g)[1] - table_window(L, world, g)[0]) * R + 1 for g in range(world)]
+    nsz = torch.tensor([hi - lo], dtype=torch.int64, device=goff.device)
+    allsz = torch.empty(world, dtype=torch.int64, device=goff.device)
+    dist.all_gather_into_tensor(allsz, nsz, group=group)
+    isizes = [int(v) for v in allsz.tolist()]
+    rels = _gather_var(rel, wsizes, group)                                      # X2
+    idss = _gather_var(my_ids, isizes, group)
+    dist.all_reduce(arr, op=dist.ReduceOp.SUM, group=group)                     # disjoint windows
+    parts, base = [], 0
+    for g in range(world):
+        parts.append(rels[g][:-1] + base)
+        base += isizes[g]
+    parts.append(torch.tensor([base], dtype=torch.int64, device=goff.device))
+    full_goff = torch.cat(parts).contiguous()
+    full_ids = torch.cat(idss).contiguous() if base else torch.zeros(0, dtype=ids.dtype, device=ids.device)
+    index.import_tables(full_goff, full_ids, arr.contiguous(), n_total - 1)
+    excl = torch.arange(bounds[rank], bounds[rank] + n_local, dtype=torch.int64,
+                        device=addrs_local.device).to(torch.int32)
+    return index.query_addrs(addrs_local, k, excl)                             # Q1-Q3 (own rows)

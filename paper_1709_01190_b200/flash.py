@@ -30,7 +30,8 @@ _NAMES = {1: "FLASH_EINVAL", 2: "FLASH_ENOMEM", 3: "FLASH_ECUDA", 4: "FLASH_ENCC
 EXPORTS = (
     "flash_create", "flash_destroy", "flash_hash", "flash_insert", "flash_insert_addrs",
     "flash_query_topk", "flash_query_addrs", "flash_knn_graph", "flash_knn_graph_host",
-    "flash_get_table", "flash_clear", "flash_check", "flash_set_profiling", "flash_phase_ms",
+    "flash_get_table", "flash_clear", "flash_check", "flash_insert_addrs_window",
+    "flash_table_arrays", "flash_import_tables", "flash_set_profiling", "flash_phase_ms",
     "flash_launch_count", "flash_reset_counters", "flash_last_error",
 )
 
@@ -67,6 +68,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                   ctypes.POINTER(u64)]
     L.flash_check.argtypes = [vp, ctypes.POINTER(u64)]
     L.flash_clear.argtypes = [vp, vp]
+    L.flash_insert_addrs_window.argtypes = [vp, vp, u64, u32, u32, u32, vp]
+    L.flash_table_arrays.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                     ctypes.POINTER(u64)]
+    L.flash_import_tables.argtypes = [vp, vp, vp, u64, vp, u32, vp]
     L.flash_set_profiling.argtypes = [vp, i32]
     L.flash_phase_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
     L.flash_launch_count.argtypes = [vp]
@@ -185,6 +190,24 @@ def flash_get_table(h, t: int):
     return off.value, ids.value, arr.value, n.value
 
 
+def flash_insert_addrs_window(h, addrs, n_rows, id_base, t_begin, t_end, stream=None):
+    _check(load_library().flash_insert_addrs_window(h, _ptr(addrs), n_rows, id_base, t_begin, t_end,
+                                                    _stream(stream, addrs)))
+
+
+def flash_table_arrays(h):
+    """(goff, ids, arrivals) device pointers and the total number of kept ids."""
+    g, i, a = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    n = ctypes.c_uint64()
+    _check(load_library().flash_table_arrays(h, ctypes.byref(g), ctypes.byref(i), ctypes.byref(a), ctypes.byref(n)))
+    return g.value, i.value, a.value, n.value
+
+
+def flash_import_tables(h, goff, ids, n_ids, arrivals, max_id, stream=None):
+    _check(load_library().flash_import_tables(h, _ptr(goff), _ptr(ids), n_ids, _ptr(arrivals), max_id,
+                                              _stream(stream, goff)))
+
+
 def flash_clear(h, stream=None):
     _check(load_library().flash_clear(h, _stream(stream)))
 
@@ -225,15 +248,16 @@ def flash_last_error() -> str:
 class _DeviceArray:
     """Zero-copy view of library-owned device memory (CUDA array interface)."""
 
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
+    def __init__(self, ptr: int, n: int, typestr: str = "<i4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                          "version": 2, "strides": None}
 
 
-def _copy_device(ptr: int, n: int, device) -> torch.Tensor:
+def _copy_device(ptr: int, n: int, device, typestr: str = "<i4") -> torch.Tensor:
+    dt = torch.int64 if typestr == "<i8" else torch.int32
     if n == 0:
-        return torch.empty(0, dtype=torch.int32, device=device)
-    return torch.as_tensor(_DeviceArray(ptr, n), device=device).clone()
+        return torch.empty(0, dtype=dt, device=device)
+    return torch.as_tensor(_DeviceArray(ptr, n, typestr), device=device).clone()
 
 
 class FlashIndex:
@@ -308,6 +332,19 @@ class FlashIndex:
 
     def clear(self):
         flash_clear(self.h)
+
+    def insert_addrs_window(self, addrs, id_base, t_begin, t_end):
+        flash_insert_addrs_window(self.h, addrs, addrs.shape[0], id_base, t_begin, t_end)
+
+    def table_arrays(self):
+        """Copies of (goff int64 [L*range+1], ids int32 [n], arrivals int32 [L*range])."""
+        g, i, a, n = flash_table_arrays(self.h)
+        nb = self.L * self.range
+        return (_copy_device(g, nb + 1, self.device, "<i8"), _copy_device(i, n, self.device),
+                _copy_device(a, nb, self.device))
+
+    def import_tables(self, goff, ids, arrivals, max_id):
+        flash_import_tables(self.h, goff, ids if ids.numel() else None, ids.numel(), arrivals, max_id)
 
     def errors(self) -> int:
         return flash_check(self.h)

@@ -37,6 +37,37 @@ class OracleIndex:
         ids = (np.arange(a.shape[0], dtype=np.int64) + id_base).astype(np.uint32)
         self.T = oracle.build(self.L, self.R, self.range, self.seed, a, ids)
 
+    def insert_addrs_window(self, addrs, id_base, t0, t1):
+        a = addrs.numpy().view(np.uint32).copy()
+        a[:, :t0] = 0xFFFFFFFF  # other tables receive nothing
+        a[:, t1:] = 0xFFFFFFFF
+        self.insert_addrs(torch.from_numpy(a.view(np.int32)), id_base)
+
+    def table_arrays(self):
+        """Flat (goff int64 [L*range+1], ids int32, arrivals int32 [L*range]) like the C ABI."""
+        goff, ids, base = [], [], 0
+        for t in range(self.L):
+            off, kept, _ = self.T.table(t)
+            goff.append(off[:-1].astype(np.int64) + base)
+            ids.append(kept)
+            base += int(off[-1])
+        goff.append(np.array([base], np.int64))
+        return (torch.from_numpy(np.concatenate(goff)), torch.from_numpy(np.concatenate(ids).view(np.int32)),
+                torch.from_numpy(self.T.arrivals.reshape(-1).view(np.int32).copy()))
+
+    def import_tables(self, goff, ids, arrivals, max_id):
+        g = goff.numpy()
+        i = ids.numpy().view(np.uint32)
+        off = np.stack([g[t * self.range: (t + 1) * self.range + 1] - g[t * self.range]
+                        for t in range(self.L)]).astype(np.uint32)
+        stride = max(1, int(off[:, -1].max()))
+        kept = np.zeros(self.L * stride, np.uint32)
+        for t in range(self.L):
+            n = int(off[t, -1])
+            kept[t * stride: t * stride + n] = i[g[t * self.range]: g[t * self.range] + n]
+        arr = arrivals.numpy().view(np.uint32).reshape(self.L, self.range).copy()
+        self.T = oracle.Tables(self.L, self.R, self.range, arr, off, kept, stride)
+
     def query_addrs(self, addrs, k, exclude):
         ids, cnt = oracle.query(self.T, addrs.numpy().view(np.uint32), k,
                                 exclude=exclude.numpy().astype(np.int64).astype(np.uint32))
@@ -47,7 +78,7 @@ def _shape():
     return synth.SHAPES["tiny"].with_(N=700, seed=11)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, mode="replicated"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,8 +88,8 @@ def _worker(rank, world, port, out_dir):
         bounds = fdist.shard_bounds(lens, world)
         rp, col = synth.generate(shape, rows=(bounds[rank], bounds[rank + 1]))
         idx = OracleIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"])
-        ids, cnt = fdist.knn_graph_replicated(idx, torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)),
-                                              CFG["k"], bounds, rank)
+        fn = fdist.knn_graph_replicated if mode == "replicated" else fdist.knn_graph_sharded_build
+        ids, cnt = fn(idx, torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)), CFG["k"], bounds, rank)
         np.save(os.path.join(out_dir, f"ids_{rank}.npy"), ids.numpy())
         np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), cnt.numpy())
     finally:
@@ -71,9 +102,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_graph_equals_single_process(tmp_path, world):
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,mode", [(2, "replicated"), (3, "replicated"), (2, "sharded"), (3, "sharded"),
+                                        (5, "sharded")])
+def test_distributed_graph_equals_single_process(tmp_path, world, mode):
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, join=True)
     shape = _shape()
     rp, col = synth.generate(shape)
     want_ids, want_cnt = oracle.knn_graph(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"], rp, col,

@@ -320,3 +320,41 @@ def test_compute_sanitizer_clean(tool):
                         os.path.join(root, "tools", "sanitize_run.py")],
                        capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_table_windows_assemble_to_the_full_index():
+    """The multi-GPU build path on one GPU: G handles each build a table window
+    (flash_insert_addrs_window), their windows are assembled like dist.py does, imported
+    into a fresh handle (flash_import_tables), and the graph equals the oracle's."""
+    rp, col = shape_slice("webspam", 2500)
+    n = rp.size - 1
+    K, L, R, rng, seed, k = 4, 50, 128, 1 << 12, 0x5EED0002, 64
+    o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    G = 3
+    with flash.FlashIndex(K, L, R, rng, seed) as full:
+        addrs = full.hash_addrs(d_rp, d_col)
+        parts, ids_parts, arr_sum, base = [], [], None, 0
+        for g in range(G):
+            t0, t1 = (L * g) // G, (L * (g + 1)) // G
+            with flash.FlashIndex(K, L, R, rng, seed) as w:
+                w.insert_addrs_window(addrs, 0, t0, t1)
+                goff, ids, arr = w.table_arrays()
+                lo, hi = int(goff[t0 * rng]), int(goff[t1 * rng])
+                parts.append(goff[t0 * rng: t1 * rng] - lo + base)
+                ids_parts.append(ids[lo:hi])
+                arr_sum = arr if arr_sum is None else arr_sum + arr
+                base += hi - lo
+        parts.append(torch.tensor([base], dtype=torch.int64, device="cuda"))
+        with flash.FlashIndex(K, L, R, rng, seed) as imp:
+            imp.import_tables(torch.cat(parts).contiguous(), torch.cat(ids_parts).contiguous(),
+                              arr_sum.contiguous(), n - 1)
+            excl = torch.arange(n, dtype=torch.int32, device="cuda")
+            g_ids, g_cnt = imp.query_addrs(addrs, k, excl)
+            assert np.array_equal(flash.as_u32(g_ids), o_ids)
+            assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
+            T = oracle.build(L, R, rng, seed, flash.as_u32(addrs), np.arange(n, dtype=np.uint32))
+            for t in (0, 17, 49):
+                off, ids_t, arr_t = imp.table(t)
+                o_off, o_ids_t, o_arr = T.table(t)
+                assert np.array_equal(off, o_off) and np.array_equal(ids_t, o_ids_t) and np.array_equal(arr_t, o_arr)
