@@ -77,5 +77,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    if "--qprof" in sys.argv:  # diagnostic per-phase cycle counters (tools/qprof.py)
+        print(build_variant("qprof", ["FLASH_QPROF"]))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(SO)

@@ -25,6 +25,20 @@ namespace {
 
 constexpr uint32_t kFullS = 0xFFFFFFFFu;
 
+#ifdef FLASH_QPROF  // per-phase cycle counters (diagnostic builds only: build.py --qprof)
+__device__ unsigned long long g_qprof[8];
+#define QMARK(i)                                                                  \
+  do {                                                                            \
+    const long long now_ = clock64();                                             \
+    if (lane == 0) atomicAdd(&g_qprof[i], (unsigned long long)(now_ - qp_last)); \
+    qp_last = now_;                                                               \
+  } while (0)
+#else
+#define QMARK(i) \
+  do {           \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t lanemask_lt_s() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -34,6 +48,44 @@ __device__ __forceinline__ uint32_t lanemask_le_s() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
   return m;
+}
+
+// bitonic sort of E*32 keys held E per lane, key index r*32+lane (ascending)
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[E], uint32_t lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 32u * E; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {  // partner is the other register of this lane (k == 64: ascending)
+        const uint32_t a = min(v[0], v[1]), b = max(v[0], v[1]);
+        v[0] = a;
+        v[1] = b;
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const uint32_t w = __shfl_xor_sync(0xFFFFFFFFu, v[r], j);
+          const bool asc = ((lane + 32u * r) & k) == 0;
+          v[r] = (lower == asc) ? min(v[r], w) : max(v[r], w);
+        }
+      }
+    }
+  }
+}
+
+// whole-warp ascending sort of arr[lo, lo+n), n <= 64
+__device__ __forceinline__ void warp_sort_range(uint32_t* arr, uint32_t lo, uint32_t n, uint32_t lane) {
+  if (n <= 32) {
+    uint32_t v[1] = {lane < n ? arr[lo + lane] : 0xFFFFFFFFu};
+    warp_bitonic<1>(v, lane);
+    if (lane < n) arr[lo + lane] = v[0];
+  } else {
+    uint32_t v[2] = {arr[lo + lane], lane + 32 < n ? arr[lo + 32 + lane] : 0xFFFFFFFFu};
+    warp_bitonic<2>(v, lane);
+    arr[lo + lane] = v[0];
+    if (lane + 32 < n) arr[lo + 32 + lane] = v[1];
+  }
 }
 
 __host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins, uint32_t L) {
@@ -71,6 +123,9 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   const uint32_t nq = *qcount;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
   for (uint32_t it = gw; it < nq; it += nw) {
+#ifdef FLASH_QPROF
+    long long qp_last = clock64();
+#endif
     const uint64_t q = qlist[it];
     const uint32_t excl = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
 
@@ -104,6 +159,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       M += __shfl_sync(kFullS, x, 31);
     }
     __syncwarp();
+    QMARK(0);
 
     // ---- Q2a: count candidates per digit ----
     {
@@ -129,6 +185,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       }
     }
     __syncwarp();
+    QMARK(1);
     // exclusive scan of the kBins counters (lane owns kBins/32 consecutive bins, 2 per word)
     constexpr uint32_t WPL = kBins / 64;  // words per lane
     uint32_t mtot;
@@ -156,6 +213,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       }
     }
     __syncwarp();
+    QMARK(2);
 
     // ---- Q2b: gather again, scatter into bins ----
     {
@@ -184,32 +242,63 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     __syncwarp();  // every lane is done reading the bitmap (independent thread scheduling)
     for (uint32_t j = lane; j <= (M >> 5) + 1 && j < NBW; j += 32) bmap[j] = 0;
     __syncwarp();
-    // bin d now ends at bin16[d]; each lane sorts the range of the kBins/32 bins it owns.
-    // A bin spans 2^shift ids and holds ~M/kBins of them, so the range is nearly sorted:
-    // bubble passes (no inner loop, hence no divergence) until no lane swaps.
+    QMARK(3);
+    // bin d now ends at bin16[d].  A bin spans 2^shift ids and holds ~M/kBins of them,
+    // so the array is sorted except inside bins, with few inversions (~300 per query on
+    // webspam, tools/binstats.py).  Each lane insertion-sorts a contiguous run of whole
+    // bins: lane j starts at the bin holding element j*mtot/32, so the runs are balanced
+    // even when a near-duplicate's L copies make one bin large; such a bin (16..64 ids)
+    // is bitonic-sorted by the whole warp first.  The in-order scan checks four elements
+    // per step.  (Measured alternatives, all slower: bubble passes, LSD
+    // radix passes, per-bin min-extraction, a descent queue + warp bitonic sort of big
+    // bins alone, register-held ids.)
     {
-      constexpr uint32_t BPL = kBins / 32;
-      const uint32_t lo = lane == 0 ? 0u : bin16[lane * BPL - 1];
-      const uint32_t hi = bin16[lane * BPL + BPL - 1];
-      bool swapped = hi > lo + 1;
-      while (__any_sync(kFullS, swapped)) {
-        swapped = false;
-        if (hi > lo + 1) {
-          uint32_t big = arr[lo];  // the largest value seen in this pass
-          for (uint32_t i = lo + 1; i < hi; ++i) {
-            const uint32_t x = arr[i];
-            if (big > x) {
-              arr[i - 1] = x;
-              arr[i] = big;
-              swapped = true;
-            } else {
-              big = x;
-            }
+      const uint32_t p = (uint32_t)(((uint64_t)lane * mtot) >> 5);
+      uint32_t lo = 0, bsz = 0;
+      if (mtot) {
+        const uint32_t d = (arr[p] >> shift) & (kBins - 1);
+        lo = d ? bin16[d - 1] : 0u;
+        bsz = bin16[d] - lo;
+      }
+      {  // a bin of 16..64 ids found at a split point is sorted by the whole warp first
+        const uint32_t plo = __shfl_up_sync(kFullS, lo, 1);
+        uint32_t bm = __ballot_sync(kFullS, (lane == 0 || plo != lo) && bsz >= 16 && bsz <= 64);
+        while (bm) {
+          const uint32_t src = __ffs(bm) - 1;
+          warp_sort_range(arr, __shfl_sync(kFullS, lo, src), __shfl_sync(kFullS, bsz, src), lane);
+          bm &= bm - 1;
+        }
+        __syncwarp();
+      }
+      uint32_t hi = __shfl_down_sync(kFullS, lo, 1);
+      if (lane == 31) hi = mtot;
+      uint32_t prev = lo < hi ? arr[lo] : 0u;
+      uint32_t i = lo + 1;
+      while (i < hi) {
+        if (i + 3 < hi) {
+          const uint32_t x0 = arr[i], x1 = arr[i + 1], x2 = arr[i + 2], x3 = arr[i + 3];
+          if (prev <= x0 && x0 <= x1 && x1 <= x2 && x2 <= x3) {
+            prev = x3;
+            i += 4;
+            continue;
           }
         }
+        const uint32_t x = arr[i];
+        if (x >= prev) {
+          prev = x;
+        } else {
+          uint32_t j = i;
+          while (j > lo && arr[j - 1] > x) {
+            arr[j] = arr[j - 1];
+            --j;
+          }
+          arr[j] = x;
+        }
+        ++i;
       }
     }
     __syncwarp();
+    QMARK(4);
 
     // ---- Q3a: run lengths.  Distinct ids are compacted in place to arr[0..nd) (a run's
     //      write index never exceeds its end index) with their counts in cnt16 (the bin
@@ -241,6 +330,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       }
     }
     __syncwarp();
+    QMARK(5);
 
     // ---- Q3b: threshold count c*, how many ties to keep, how many counts above c*; the
     //      histogram becomes the output cursor of each count above c* (higher counts first) ----
@@ -332,6 +422,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       ocnt[j] = 0;
     }
     __syncwarp();
+    QMARK(6);
   }
 }
 
@@ -372,3 +463,14 @@ int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, c
 }
 
 }  // namespace flash
+
+#ifdef FLASH_QPROF
+extern "C" int flash_debug_qprof(unsigned long long out[8], int reset) {
+  if (cudaMemcpyFromSymbol(out, flash::g_qprof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(flash::g_qprof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
