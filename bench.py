@@ -145,15 +145,125 @@ def gen_local(shape, bounds, rank):
 
 
 def query_work(idx_tables, addrs_np):
-    """Candidates gathered per graph (sum over queries of their L bucket sizes)."""
-    total = 0
+    """Candidates gathered per query (the sum of its L bucket sizes) and the bucket-arrival
+    histogram (log2 bins) of the built tables."""
+    per_q = np.zeros(addrs_np.shape[0], dtype=np.int64)
+    hist = np.zeros(34, dtype=np.int64)
+    over_r = 0
     for t in range(L):
-        off, _, _ = idx_tables(t)
+        off, _, arr = idx_tables(t)
         sizes = np.diff(off.astype(np.int64))
         a = addrs_np[:, t]
         valid = a != 0xFFFFFFFF
-        total += int(sizes[a[valid].astype(np.int64)].sum())
-    return total
+        per_q[valid] += sizes[a[valid].astype(np.int64)]
+        arr = arr.astype(np.int64)
+        lg = np.zeros_like(arr)
+        nz = arr > 0
+        lg[nz] = np.floor(np.log2(arr[nz])).astype(np.int64) + 1
+        hist += np.bincount(lg, minlength=34)[:34]
+        over_r += int((arr > R).sum())
+    top = int(np.nonzero(hist)[0].max()) if hist.any() else 0
+    labels = ["0"] + [f"{1 << (i - 1)}-{(1 << i) - 1}" for i in range(1, top + 1)]
+    arrivals = {"buckets": int(hist.sum()), "histogram_log2": dict(zip(labels, hist[: top + 1].tolist())),
+                "frac_over_R": over_r / max(int(hist.sum()), 1)}
+    return per_q, arrivals
+
+
+def data_quality_stats(h_rp, d_col, out_ids, n_q=1000, n_pairs=100_000, seed=13):
+    """SURVEY §8(d) statistics printed beside the timing (evaluation only, outside the timed
+    region, never on the product path): nnz mean / p99, mean binary cosine over random row
+    pairs, and the graph's R@k / S@k against exact binary cosine for
+    n_q sampled rows.  Rows are treated as sets (duplicate column ids dropped).  The brute
+    force is a deduplicated CSR x dense 0/1 query-mask product (torch sparse on the GPU)."""
+    import torch
+
+    dev = d_col.device
+    rp = h_rp.numpy().astype(np.int64)
+    rp = rp - rp[0]
+    N = rp.size - 1
+    lens = np.diff(rp)
+    res = {"nnz_mean": float(lens.mean()), "nnz_p99": float(np.percentile(lens, 99))}
+    row = torch.repeat_interleave(torch.arange(N, device=dev), torch.from_numpy(lens).to(dev))
+    key = (row << 32) | (d_col.to(torch.int64) & 0xFFFFFFFF)
+    del row
+    key = torch.sort(key).values
+    keep = torch.ones(key.numel(), dtype=torch.bool, device=dev)
+    keep[1:] = key[1:] != key[:-1]
+    key = key[keep]
+    del keep
+    cnt = torch.bincount(key >> 32, minlength=N)
+    crow = torch.zeros(N + 1, dtype=torch.int64, device=dev)
+    crow[1:] = torch.cumsum(cnt, 0)
+    col = (key & 0xFFFFFFFF).to(torch.int32)
+    D = int(col.max().item()) + 1
+    rng = np.random.default_rng(seed)
+
+    # mean pairwise cosine: |a ∩ b| by looking up (b, c) for every c of row a in the sorted keys
+    pa, pb = rng.integers(0, N, n_pairs), rng.integers(0, N, n_pairs)
+    ok = pa != pb
+    pa, pb = pa[ok], pb[ok]
+    cos_sum, n_ok = 0.0, 0
+    for c0 in range(0, pa.size, 10_000):
+        a = torch.from_numpy(pa[c0:c0 + 10_000]).to(dev)
+        b = torch.from_numpy(pb[c0:c0 + 10_000]).to(dev)
+        la = cnt[a]
+        pidx = torch.repeat_interleave(torch.arange(a.numel(), device=dev), la)
+        first = torch.cumsum(la, 0) - la
+        offs = torch.arange(pidx.numel(), device=dev) - first[pidx]
+        q = (b[pidx] << 32) | (key[crow[a][pidx] + offs] & 0xFFFFFFFF)
+        pos = torch.searchsorted(key, q).clamp(max=key.numel() - 1)
+        inter = torch.bincount(pidx, weights=(key[pos] == q).double(), minlength=a.numel())
+        den = torch.sqrt(la.double() * cnt[b].double())
+        c = torch.where(den > 0, inter / den.clamp(min=1), torch.zeros_like(inter))
+        cos_sum += float(c.sum().item())
+        n_ok += a.numel()
+    res["pairwise_cosine_mean"] = cos_sum / max(n_ok, 1)
+    res["pairwise_pairs"] = n_ok
+    del key
+
+    # R@k / S@k of the reported top-k against exact cosine, n_q sampled rows
+    X = torch.sparse_csr_tensor(crow.to(torch.int32), col, torch.ones(col.numel(), device=dev),
+                                size=(N, D), check_invariants=False)
+    qs = rng.choice(N, size=min(n_q, N), replace=False)
+    B = 64
+    Qm = torch.empty((D, B), dtype=torch.float32, device=dev)
+    kmax = out_ids.shape[1]
+    ks = sorted({k for k in (1, 10, 100) if k <= kmax} | {kmax})
+    rec = {k: 0.0 for k in ks}
+    sim = {k: 0.0 for k in ks}
+    best_sum = 0.0
+    cntd = cnt.double()
+    for b0 in range(0, qs.size, B):
+        qb = torch.from_numpy(qs[b0:b0 + B]).to(dev)
+        nb = qb.numel()
+        Qm.zero_()
+        lq = cnt[qb]
+        pidx = torch.repeat_interleave(torch.arange(nb, device=dev), lq)
+        first = torch.cumsum(lq, 0) - lq
+        offs = torch.arange(pidx.numel(), device=dev) - first[pidx]
+        Qm[col[crow[qb][pidx] + offs].long(), pidx] = 1.0
+        inter = torch.sparse.mm(X, Qm)[:, :nb].double()                 # [N, nb]
+        den = torch.sqrt(cntd[:, None] * cntd[qb][None, :])
+        cos = torch.where(den > 0, inter / den.clamp(min=1), torch.zeros_like(inter))
+        cos[qb, torch.arange(nb, device=dev)] = -1.0                      # exclude self
+        best = cos.max(0).values                                          # exact 1-NN cosine
+        top = out_ids[qb].long()                                          # [nb, k]
+        valid = top >= 0
+        ct = cos.t().gather(1, top.clamp(min=0))
+        for k in ks:
+            v = valid[:, :k]
+            hit = ((ct[:, :k] >= best[:, None] - 1e-9) & v).any(1)
+            rec[k] += float(hit.double().sum().item())
+            s = torch.where(v, ct[:, :k], torch.zeros_like(ct[:, :k])).sum(1) / v.sum(1).clamp(min=1)
+            sim[k] += float(s.sum().item())
+        best_sum += float(best.sum().item())
+    n = qs.size
+    res["one_nn_cosine_mean"] = best_sum / n
+    res["quality"] = {"queries": int(n), "R@k": {str(k): rec[k] / n for k in ks},
+                      "S@k": {str(k): sim[k] / n for k in ks},
+                      "definition": "R@k: exact cosine 1-NN (any tie) in the reported top-k (P:393); "
+                                    "S@k: mean exact cosine of the reported top-k (P:395)"}
+    return res
 
 
 def run_ours(args):
@@ -265,7 +375,8 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     addrs_np = flash.as_u32(idx.hash_addrs(d_rp, d_col))
-    n_cand = query_work(lambda t: idx.table(t), addrs_np)  # this rank's queries
+    per_q, arrivals = query_work(lambda t: idx.table(t), addrs_np)  # this rank's queries
+    n_cand = int(per_q.sum())
 
     result = None
     if rank == 0:
@@ -278,18 +389,24 @@ def run_ours(args):
         query_ms = per_step["query"]
         build_ms = per_step["build"]
         dominant = max(("hash", hash_ms), ("build", build_ms), ("query", query_ms), key=lambda x: x[1])[0]
-        traffic = {}
+        traffic = {}  # ncu --set full DRAM bytes of one graph, summed per kernel name
         try:
             with open(TRAFFIC_PATH) as f:
                 for d in json.load(f):
-                    traffic.setdefault(d["kernel"].split("::")[-1].split("<")[0], d.get("dram_traffic_bytes"))
+                    nm = d["kernel"].split("::")[-1].split("<")[0]
+                    if d.get("dram_traffic_bytes") is not None:
+                        traffic[nm] = traffic.get(nm, 0.0) + d["dram_traffic_bytes"]
         except Exception:
             pass
+        q_traffic = None
+        if "k_query_sort" in traffic:
+            q_traffic = sum(traffic.get(nm, 0.0) for nm in ("k_query_plan", "k_query_sort", "k_query"))
         if dominant == "query" and n_cand is not None:
             # the count kernel is bound by per-candidate shared-memory work, not by HBM
-            roof = {"kernel": "k_query_warp", "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
+            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query for M > 3072)",
+                    "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
                     "peak": SMEM_RMW_PEAK, "unit": "candidate-updates/s", "peak_kind": "measured (smem RMW microbench)",
-                    "traffic": traffic.get("k_query_warp"), "candidates": n_cand,
+                    "traffic": q_traffic, "candidates": n_cand,
                     "hbm_view": {"algorithmic_bytes": 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local,
                                  "achieved_GBps": (4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local)
                                  / (query_ms * 1e-3) / 1e9}}
@@ -336,8 +453,13 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        if n_cand is not None:
-            result["candidates_per_query"] = n_cand / n_local
+        result["candidates_per_query"] = {"mean": n_cand / n_local, "p99": float(np.percentile(per_q, 99)),
+                                          "max": int(per_q.max())}
+        result["bucket_arrivals"] = arrivals
+        if world == 1 and not args.no_quality:
+            t0 = time.time()
+            result["data_stats"] = data_quality_stats(h_rp, d_col, out_ids, n_q=args.quality_queries)
+            log(f"data/quality stats in {time.time() - t0:.1f}s")
     idx.close()
     return result
 
@@ -399,6 +521,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--ref-sample", type=int, default=350000, help="oracle query sample (rows; all = full graph)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
+    ap.add_argument("--quality-queries", type=int, default=1000)
     args = ap.parse_args()
     if args.impl == "reference":
         res = run_reference(args)
