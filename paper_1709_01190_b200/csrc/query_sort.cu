@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   uint32_t* arr = reinterpret_cast<uint32_t*>(my);                  // [MCAP]
   uint32_t* binw = arr + MCAP;                                      // [kBins/2] packed u16
   constexpr uint32_t CW = (kBins > MCAP ? kBins : MCAP) / 2;        // words of the u16 area
-  uint64_t* nbase = reinterpret_cast<uint64_t*>(binw + CW);         // [L]
-  uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);          // [NBW]
+  // nbase[j]: address of candidate position 0 if it lay in the j-th non-empty bucket,
+  // so candidate p of that bucket is nbase[j][p] (one wide multiply-add per gather)
+  const uint32_t** nbase = reinterpret_cast<const uint32_t**>(binw + CW);  // [L]
+  uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);                 // [NBW]
   uint32_t* hcnt = bmap + NBW;                                      // [L+1]
   const uint16_t* bin16 = reinterpret_cast<const uint16_t*>(binw);
   const uint32_t* __restrict__ gids = a.ids;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       const uint32_t pos = M + x - sz;
       const uint32_t ne = __ballot_sync(kFullS, sz > 0);
       if (sz > 0) {
-        nbase[nne + __popc(ne & lanemask_lt_s())] = st - pos;
+        nbase[nne + __popc(ne & lanemask_lt_s())] = gids + (int64_t)(st - (uint64_t)pos);
         atomicOr(&bmap[pos >> 5], 1u << (pos & 31));
       }
       nne += __popc(ne);
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
           const uint32_t w = r0 + u * 32 < M ? bmap[(r0 >> 5) + u] : 0u;  // stay inside the slice
           const uint32_t p = r0 + u * 32 + lane;
           const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
-          idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
+          idv[u] = p < M ? __ldg(nbase[ti] + p) : kEmpty;
           before += __popc(w);
         }
 #pragma unroll
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
           const uint32_t w = r0 + u * 32 < M ? bmap[(r0 >> 5) + u] : 0u;  // stay inside the slice
           const uint32_t p = r0 + u * 32 + lane;
           const uint32_t ti = before + __popc(w & lanemask_le_s()) - 1;
-          idv[u] = p < M ? gids[nbase[ti] + p] : kEmpty;
+          idv[u] = p < M ? __ldg(nbase[ti] + p) : kEmpty;
           before += __popc(w);
         }
 #pragma unroll
