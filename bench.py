@@ -73,8 +73,10 @@ def workload_config(shape, nnz, args):
         "workload": "webspam-shaped approximate k-NN graph from scratch (hash + build + query every row)",
         "N": shape.N, "D": shape.D, "nnz": int(nnz), "nnz_per_row": round(nnz / shape.N, 1),
         "K": K, "L": L, "R": R, "range": RANGE, "k": TOPK, "seed": SEED,
-        "parallelism": (f"rows x{args.gpus} (hash, query); tables x{args.gpus} (build); "
-                        "all-gather addresses + built tables") if args.gpus > 1 else "1 GPU",
+        "parallelism": ((f"rows x{args.gpus} (hash, count/top-k); tables x{args.gpus} (build, gather); "
+                         "all-to-all addresses + candidates") if args.mode == "exchange" else
+                        (f"rows x{args.gpus} (hash, query); tables x{args.gpus} (build); "
+                         "all-gather addresses + built tables")) if args.gpus > 1 else "1 GPU",
         "l2_policy": "inputs larger than L2 (col_idx 5.2 GB vs 126 MB L2); no flush",
     }
 
@@ -305,13 +307,17 @@ def run_ours(args):
     out_cnt = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
     idx = flash.FlashIndex(K, L, R, RANGE, SEED)
     stream = torch.cuda.current_stream()
+    # N > 1: tables partitioned over the GPUs with the candidate all-to-all (north_star (d),
+    # default) or the sharded build + table all-gather
+    graph_fn = (fdist.knn_graph_candidate_exchange if args.mode == "exchange"
+                else fdist.knn_graph_sharded_build)
 
     def step():
         idx.clear()
         if world == 1:
             flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, TOPK, out_ids, out_cnt)
             return out_ids, out_cnt
-        return fdist.knn_graph_sharded_build(idx, d_rp, d_col, TOPK, bounds, rank)
+        return graph_fn(idx, d_rp, d_col, TOPK, bounds, rank)
 
     for _ in range(args.warmup):
         step()
@@ -358,7 +364,7 @@ def run_ours(args):
         else:
             d_rp2 = h_rp_local.to(dev, non_blocking=True)
             d_col2 = h_col.to(dev, non_blocking=True)
-            ids_, cnt_ = fdist.knn_graph_sharded_build(idx, d_rp2, d_col2, TOPK, bounds, rank)
+            ids_, cnt_ = graph_fn(idx, d_rp2, d_col2, TOPK, bounds, rank)
             h_ids.copy_(ids_, non_blocking=True)
             h_cnt.copy_(cnt_, non_blocking=True)
             torch.cuda.synchronize()
@@ -449,7 +455,7 @@ def run_ours(args):
             "e2e": {"value": shape.N / (e2e_ms_max * 1e-3), "unit": "queries/s",
                     "ms_per_step": e2e_ms_max, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "flash_knn_graph_host (pinned host buffers)" if world == 1 else
-                           "host copies + replicated-table graph"},
+                           f"host copies + dist {args.mode} graph"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -519,6 +525,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["exchange", "sharded"], default="exchange",
+                    help="N>1: candidate all-to-all over partitioned tables (north_star (d)) or "
+                         "sharded build + table all-gather")
     ap.add_argument("--ref-sample", type=int, default=350000, help="oracle query sample (rows; all = full graph)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")

@@ -137,6 +137,56 @@ flash_status flash_knn_graph_host(flash_index *h, const int64_t *row_ptr, const 
                                   uint64_t n_rows, uint32_t k, uint32_t *out_ids, uint32_t *out_counts,
                                   void *stream);
 
+/* ---- Multi-GPU candidate exchange (north_star (d)) ----------
+ * The L tables are partitioned over `world` GPUs by floor blocks: rank g owns the table
+ * window [t0(g), t1(g)) = [floor(g*L/world), floor((g+1)*L/world)).  A query's candidate
+ * multiset (Alg. 3 lines 4-7) is the union over ranks of the buckets it
+ * addresses in each window, so the owner of a query can count and select (Q2-Q3) over
+ * the per-rank lists exactly as a single GPU does over the L buckets. */
+
+/* flash_hash writing only addresses, laid out by table owner (the exchange's send layout
+ * for the address all-to-all, X1): rank g's block is [n_rows][t1(g)-t0(g)] uint32 and
+ * starts at element n_rows * t0(g) of addrs (total n_rows * L elements).  world == 1 is
+ * the plain [n_rows][L] layout.  1 <= world <= 65536. */
+flash_status flash_hash_blocked(const flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
+                                uint64_t n_rows, uint32_t world, uint32_t *addrs, void *stream);
+
+/* flash_insert_addrs_window where addrs holds only the window's columns: addrs
+ * [n_rows][t_end - t_begin], column j = table t_begin + j (the address all-to-all's
+ * receive layout).  Builds tables [t_begin, t_end) exactly as a full insert would
+ * (bottom-R is per bucket, keyed by the global table index); other tables are kept. */
+flash_status flash_insert_addrs_cols(flash_index *h, const uint32_t *addrs, uint64_t n_rows,
+                                     uint32_t id_base, uint32_t t_begin, uint32_t t_end, void *stream);
+
+/* Per-query candidate counts of the table window [t_begin, t_end) for n_q queries whose
+ * window addresses are addrs [n_q][t_end - t_begin]: sizes[q] (uint32, [n_q]) = sum of
+ * the addressed buckets' sizes; offsets (uint64, [n_q+1]) = their exclusive scan, total
+ * at offsets[n_q].  These are the per-destination sizes of the candidate all-to-all (X2).
+ * Before any insert every size is 0. */
+flash_status flash_window_sizes(const flash_index *h, const uint32_t *addrs, uint64_t n_q, uint32_t t_begin,
+                                uint32_t t_end, uint32_t *sizes, uint64_t *offsets, void *stream);
+
+/* Gather (Q1 restricted to the window): out_ids[offsets[q] .. offsets[q+1]) = the
+ * concatenation, in table order, of query q's window buckets (ascending ids within each).
+ * offsets from flash_window_sizes with the same arguments; out_ids has offsets[n_q]
+ * entries (caller-allocated). */
+flash_status flash_window_gather(const flash_index *h, const uint32_t *addrs, uint64_t n_q, uint32_t t_begin,
+                                 uint32_t t_end, const uint64_t *offsets, uint32_t *out_ids, void *stream);
+
+/* Q2-Q3 on pre-gathered candidate segments (the owner side of X2): query q's candidates
+ * are the n_seg segments (s, q), s < n_seg, stored consecutively in (s, q) order in cand:
+ * segment (s, q) has seg_sizes[s*n_q + q] ids.  Counts multiplicities (R#11), drops
+ * exclude[q] (if exclude != NULL), orders by (count desc, id asc), keeps k, pads (R#12,
+ * R#13) — the same result as flash_query_addrs when the segments are the query's
+ * buckets split by table window.  Preconditions (the exchange guarantees them): an id
+ * occurs at most once per table, so counts are <= the handle's L, and a query has at most
+ * L*R candidates (a query with more is counted in the device error counter, flash_check,
+ * and gets k pads).  max_id bounds every candidate id.  cand may be NULL when every size is
+ * 0.  1 <= n_seg <= 4096, n_q < 2^31.  The handle's tables are not used. */
+flash_status flash_count_topk(const flash_index *h, const uint32_t *cand, const uint32_t *seg_sizes,
+                              uint32_t n_seg, uint64_t n_q, uint32_t k, const uint32_t *exclude, uint32_t max_id,
+                              uint32_t *out_ids, uint32_t *out_counts, void *stream);
+
 /* Drop every inserted id (stream-ordered): the handle returns to its freshly created
  * state (arrivals zero, no tables), keeping K, L, R, range and seed. */
 flash_status flash_clear(flash_index *h, void *stream);

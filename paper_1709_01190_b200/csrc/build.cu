@@ -103,13 +103,14 @@ __device__ void block_bitonic(T* a, uint32_t n) {
 }
 
 // B1: per-bucket arrival histogram of the new rows (warp per row, lanes over tables).
-__global__ void k_count(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t range,
-                        uint32_t t0, uint32_t t1, uint32_t* __restrict__ cnt, unsigned long long* err) {
+__global__ void k_count(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t acol0,
+                        uint32_t range, uint32_t t0, uint32_t t1, uint32_t* __restrict__ cnt,
+                        unsigned long long* err) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
     for (uint32_t t = t0 + lane; t < t1; t += 32) {
-      const uint32_t a = addrs[r * L + t];
+      const uint32_t a = addrs[r * L + t - acol0];
       if (a == kEmpty) continue;
       if (a >= range) { atomicAdd(err, 1ull); continue; }
       atomicAdd(&cnt[t * range + a], 1u);
@@ -143,14 +144,15 @@ __global__ void k_fill_old(uint32_t nb, const uint64_t* __restrict__ goff_old,
   }
 }
 
-__global__ void k_fill_new(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t range,
-                           uint32_t t0, uint32_t t1, uint32_t id_base, uint32_t* __restrict__ cursor,
+__global__ void k_fill_new(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t acol0,
+                           uint32_t range, uint32_t t0, uint32_t t1, uint32_t id_base,
+                           uint32_t* __restrict__ cursor,
                            const uint64_t* __restrict__ pool_off, uint32_t* __restrict__ pool) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
     for (uint32_t t = t0 + lane; t < t1; t += 32) {
-      const uint32_t a = addrs[r * L + t];
+      const uint32_t a = addrs[r * L + t - acol0];
       if (a >= range) continue;  // EMPTY or invalid (counted by k_count)
       const uint32_t i = t * range + a;
       const uint32_t pos = atomicAdd(&cursor[i], 1u);
@@ -434,7 +436,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
   cudaMemsetAsync(a.big_count, 0, 2 * sizeof(uint32_t), s);  // big + mid list counters
   if (a.n) {
-    k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.L, a.range, a.t0, a.t1, a.cursor, a.err);
+    k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.cursor, a.err);
     launches++;
   }
   k_pool_sizes<<<nb_blocks, 256, 0, s>>>(nb, a.R, a.goff_old, a.cursor, a.arrivals, a.pool_cnt, a.keep_cnt);
@@ -450,8 +452,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     launches++;
   }
   if (a.n) {
-    k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.L, a.range, a.t0, a.t1, a.id_base, a.cursor,
-                                           a.pool_off, a.pool);
+    k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.id_base,
+                                           a.cursor, a.pool_off, a.pool);
     launches++;
   }
   static bool attr = false;

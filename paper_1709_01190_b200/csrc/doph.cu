@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
                                                    uint64_t n_rows, uint32_t K, uint32_t L,
                                                    uint32_t range, HashKeys keys,
                                                    uint32_t* __restrict__ codes,
-                                                   uint32_t* __restrict__ addrs) {
+                                                   uint32_t* __restrict__ addrs, uint32_t world) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31;
@@ -123,7 +123,13 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
           for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
           a = __umulhi(x, range);
         }
-        addrs[r * L + t] = a;
+        if (world == 1) {
+          addrs[r * L + t] = a;
+        } else {  // owner-blocked: table t goes to the block of the rank whose window holds it
+          const uint32_t g = ((t + 1) * world - 1) / L;
+          const uint32_t g0 = (g * L) / world, g1 = ((g + 1) * L) / world;
+          addrs[n_rows * g0 + r * (g1 - g0) + (t - g0)] = a;
+        }
       }
     }
     __syncwarp();
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
 template <bool C, bool A>
 int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
              uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-             cudaStream_t s) {
+             uint32_t world, cudaStream_t s) {
   const uint32_t B = K * L;
   const size_t per_warp = (size_t)2 * B * sizeof(uint32_t);
   int wpb = (int)((96 * 1024) / per_warp);
@@ -149,7 +155,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return 0;
   k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                         codes, addrs);
+                                                         codes, addrs, world);
   return 1;
 }
 
@@ -157,10 +163,11 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
 
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-                cudaStream_t s) {
-  if (codes && addrs) return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, s);
-  if (codes) return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, s);
-  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, s);
+                uint32_t world, cudaStream_t s) {
+  if (codes && addrs)
+    return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
+  if (codes) return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
+  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
 }
 
 }  // namespace flash

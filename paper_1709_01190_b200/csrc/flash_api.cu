@@ -101,6 +101,7 @@ struct flash_index {
   uint64_t max_id = 0;      // largest id inserted so far (host count)
   // scratch
   DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
+  DevBuf seg_off, xscan_tmp;  // flash_count_topk segment offsets; exchange scans
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -176,16 +177,16 @@ __global__ void k_table_off(const uint64_t* goff, uint32_t t, uint32_t range, ui
 }
 
 flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n,
-                     uint32_t* codes, uint32_t* addrs, cudaStream_t s) {
+                     uint32_t* codes, uint32_t* addrs, cudaStream_t s, uint32_t world = 1) {
   Phase ph(h, 0, s);
   const_cast<flash_index*>(h)->launches +=
-      launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, addrs, s);
+      launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, addrs, world, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }
 
 flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
-                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX) {
+                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX, bool cols = false) {
   if (t1 > h->L) t1 = h->L;
   const uint64_t nb = (uint64_t)h->L * h->range;
   const uint64_t pool_cap = h->kept_ub + n * h->L;
@@ -206,6 +207,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   BuildArgs a;
   memset(&a, 0, sizeof a);
   a.addrs = addrs;
+  a.astride = cols ? t1 - t0 : h->L;  // cols: addrs holds only the window's columns
+  a.acol0 = cols ? t0 : 0;
   a.n = n;
   a.id_base = id_base;
   a.L = h->L;
@@ -259,6 +262,8 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   a.L = h->L;
   a.range = h->range;
   a.k = k;
+  a.cmax = h->L;
+  a.direct = 0;
   a.exclude = exclude;
   a.exclude_self = exclude_self;
   a.self_base = self_base;
@@ -341,6 +346,7 @@ void flash_destroy(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
+                    &h->seg_off, &h->xscan_tmp,
                     &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
@@ -576,6 +582,125 @@ flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const 
     CUDA_TRY(cudaMemcpyAsync(out_counts, d_cnt, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
   }
   CUDA_TRY(cudaStreamSynchronize(s));
+  return FLASH_OK;
+}
+
+flash_status flash_hash_blocked(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,
+                                uint64_t n_rows, uint32_t world, uint32_t* addrs, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (world < 1 || world > 65536) return fail(FLASH_EINVAL, "world=%u outside [1, 65536]", world);
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(row_ptr);
+  REQUIRE_DEV(col_idx);
+  REQUIRE_DEV(addrs);
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  return do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s, world);
+}
+
+flash_status flash_insert_addrs_cols(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
+                                     uint32_t t_begin, uint32_t t_end, void* stream) {
+  if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (t_begin >= t_end || t_end > h->L)
+    return fail(FLASH_EINVAL, "table window [%u, %u) must be non-empty and inside [0, %u)", t_begin, t_end, h->L);
+  if (n_rows == 0) return FLASH_OK;
+  REQUIRE_DEV(addrs);
+  if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
+    return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  return do_insert_addrs(h, addrs, n_rows, id_base, s, t_begin, t_end, true);
+}
+
+flash_status flash_window_sizes(const flash_index* hc, const uint32_t* addrs, uint64_t n_q, uint32_t t_begin,
+                                uint32_t t_end, uint32_t* sizes, uint64_t* offsets, void* stream) {
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  if (t_begin > t_end || t_end > h->L)
+    return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
+  REQUIRE_DEV(offsets);
+  if (n_q) {
+    REQUIRE_DEV(sizes);
+    if (t_end > t_begin) REQUIRE_DEV(addrs);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  if (!h->have_tables || t_end == t_begin || n_q == 0) {
+    if (n_q) CUDA_TRY(cudaMemsetAsync(sizes, 0, sizeof(uint32_t) * n_q, s));
+    CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(uint64_t) * (n_q + 1), s));
+    return FLASH_OK;
+  }
+  TRY(ensure(h->xscan_tmp, scan_u32_to_u64_tmp_bytes(n_q)));
+  Phase ph(h, 2, s);
+  h->launches += launch_window_sizes(addrs, n_q, t_begin, t_end, h->range, h->goff[h->cur].as<uint64_t>(), sizes,
+                                     offsets, h->xscan_tmp.p, h->xscan_tmp.cap, h->err, s);
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
+flash_status flash_window_gather(const flash_index* hc, const uint32_t* addrs, uint64_t n_q, uint32_t t_begin,
+                                 uint32_t t_end, const uint64_t* offsets, uint32_t* out_ids, void* stream) {
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  if (t_begin > t_end || t_end > h->L)
+    return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
+  if (n_q == 0 || t_end == t_begin || !h->have_tables) return FLASH_OK;
+  REQUIRE_DEV(addrs);
+  REQUIRE_DEV(offsets);
+  REQUIRE_DEV(out_ids);
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  Phase ph(h, 2, s);
+  h->launches += launch_window_gather(addrs, n_q, t_begin, t_end, h->range, h->goff[h->cur].as<uint64_t>(),
+                                      h->ids[h->cur].as<uint32_t>(), offsets, out_ids, s);
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
+flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const uint32_t* seg_sizes,
+                              uint32_t n_seg, uint64_t n_q, uint32_t k, const uint32_t* exclude, uint32_t max_id,
+                              uint32_t* out_ids, uint32_t* out_counts, void* stream) {
+  if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
+  flash_index* h = const_cast<flash_index*>(hc);
+  TRY(check_query_shape(h, k));
+  if (n_seg < 1 || n_seg > 4096) return fail(FLASH_EINVAL, "n_seg=%u outside [1, 4096]", n_seg);
+  if (n_q >= 0x80000000ull) return fail(FLASH_EINVAL, "n_q must be < 2^31");
+  if (n_q == 0) return FLASH_OK;
+  REQUIRE_DEV(seg_sizes);
+  REQUIRE_DEV(out_ids);
+  REQUIRE_DEV(out_counts);
+  if (exclude) REQUIRE_DEV(exclude);
+  if (cand && !device_accessible(cand)) return fail(FLASH_EINVAL, "cand is not a device pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enter(h, s));
+  const uint64_t nsq = (uint64_t)n_seg * n_q;
+  TRY(ensure(h->seg_off, sizeof(uint64_t) * (nsq + 1)));
+  TRY(ensure(h->xscan_tmp, scan_u32_to_u64_tmp_bytes(nsq)));
+  TRY(ensure(h->qscratch, query_scratch_bytes(n_q)));
+  Phase ph(h, 2, s);
+  launch_scan_sizes(seg_sizes, nsq, h->seg_off.as<uint64_t>(), h->xscan_tmp.p, h->xscan_tmp.cap, s);
+  QueryArgs a;
+  memset(&a, 0, sizeof a);
+  a.addrs = nullptr;
+  a.nq = n_q;
+  a.goff = h->seg_off.as<uint64_t>();
+  static const uint32_t kNoCand = 0;
+  a.ids = cand ? cand : &kNoCand;  // every segment is empty when cand is NULL (never dereferenced)
+  a.L = n_seg;
+  a.range = (uint32_t)n_q;
+  a.k = k;
+  a.cmax = h->L;
+  a.direct = 1;
+  a.exclude = exclude;
+  a.exclude_self = 0;
+  a.out_ids = out_ids;
+  a.out_counts = out_counts;
+  a.err = h->err;
+  a.table_log2 = h->table_log2;
+  a.packed = (max_id < 0xFFFFFEu && h->L <= 255) ? 1 : 0;
+  a.max_id = max_id;
+  h->launches += launch_query(a, h->qscratch.p, s);
+  CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }
 

@@ -68,13 +68,17 @@ __device__ __forceinline__ uint32_t prio_of(uint64_t tb, uint32_t id) {
 // ---------------------------------------------------------------------------
 
 // H1-H3: DOPH bin minima, densification, addresses.  codes / addrs may be null.
+// world > 1: addrs is written owner-blocked for a floor-block partition of the L tables
+// over `world` ranks (table window of rank g: [floor(gL/world), floor((g+1)L/world))):
+// rank g's block [n_rows][L_g] starts at element n_rows * t0(g).  world == 1: [n_rows][L].
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-                cudaStream_t s);
+                uint32_t world, cudaStream_t s);
 
 // Build scratch / state.  All bucket-indexed arrays have nb = L*range entries (+1).
 struct BuildArgs {
-  const uint32_t* addrs;  // [n][L]
+  const uint32_t* addrs;  // row r, table t at addrs[r*astride + t - acol0]
+  uint32_t astride, acol0;  // [n][L]: L, 0; a column window [n][t1-t0]: t1-t0, t0
   uint64_t n;
   uint32_t id_base;
   uint32_t L, R, range;
@@ -102,11 +106,16 @@ size_t build_scan_tmp_bytes(uint64_t nb);
 int launch_build(const BuildArgs& a, cudaStream_t s);
 
 struct QueryArgs {
-  const uint32_t* addrs;  // [nq][L]
+  // Segment t (t < L) of query q is ids[goff[i] .. goff[i+1]) with i = t*range + addrs[q*L+t]
+  // (a table bucket), or i = t*range + q when `direct` (pre-gathered candidate segments,
+  // range = nq: the candidate-exchange owner side).  Counts are <= cmax (the index's L).
+  const uint32_t* addrs;  // [nq][L] (unused when direct)
   uint64_t nq;
   const uint64_t* goff;   // [L*range+1]
   const uint32_t* ids;
   uint32_t L, range, k;
+  uint32_t cmax;          // largest possible count (= the index's L)
+  int direct;
   const uint32_t* exclude;  // [nq] or null
   int exclude_self;         // exclude id = self_base + q
   uint32_t self_base;
@@ -124,6 +133,20 @@ size_t query_scratch_bytes(uint64_t nq);
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
                       cudaStream_t s);
 size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k);
+
+// Candidate exchange, sender side (exchange.cu).  addrs: [n][t1-t0] (a table window's
+// columns).  sizes[q] = sum of the window buckets' sizes; off = exclusive scan (n+1).
+int launch_window_sizes(const uint32_t* addrs, uint64_t n, uint32_t t0, uint32_t t1, uint32_t range,
+                        const uint64_t* goff, uint32_t* sizes, uint64_t* off, void* scan_tmp,
+                        size_t scan_tmp_bytes, unsigned long long* err, cudaStream_t s);
+size_t scan_u32_to_u64_tmp_bytes(uint64_t n);
+// out[off[q] ..] = concatenation of query q's window buckets (table order).
+int launch_window_gather(const uint32_t* addrs, uint64_t n, uint32_t t0, uint32_t t1, uint32_t range,
+                         const uint64_t* goff, const uint32_t* ids, const uint64_t* off, uint32_t* out,
+                         cudaStream_t s);
+// exclusive scan of n uint32 sizes into n+1 uint64 offsets
+int launch_scan_sizes(const uint32_t* sizes, uint64_t n, uint64_t* off, void* scan_tmp, size_t scan_tmp_bytes,
+                      cudaStream_t s);
 uint32_t query_table_log2(uint32_t L, uint32_t R);
 
 }  // namespace flash

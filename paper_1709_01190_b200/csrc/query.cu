@@ -49,8 +49,9 @@ __host__ __device__ constexpr uint32_t class_max(int c) {
 constexpr int kClasses = kSortClasses + 2;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
-                             uint32_t L, uint32_t range, uint32_t* __restrict__ lists,
-                             uint32_t* __restrict__ counts, unsigned long long* err) {
+                             uint32_t L, uint32_t range, int direct, uint64_t mmax, uint32_t k,
+                             uint32_t* __restrict__ out_ids, uint32_t* __restrict__ out_counts,
+                             uint32_t* __restrict__ lists, uint32_t* __restrict__ counts, unsigned long long* err) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t q0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; q0 < nq;
        q0 += (uint64_t)gridDim.x * blockDim.x) {
@@ -58,7 +59,7 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
     uint64_t M = 0;
     if (q < nq) {
       for (uint32_t t = 0; t < L; ++t) {
-        const uint32_t a = addrs[q * L + t];
+        const uint32_t a = direct ? (uint32_t)q : addrs[q * L + t];
         if (a < range) {
           const uint64_t i = (uint64_t)t * range + a;
           M += goff[i + 1] - goff[i];
@@ -69,6 +70,14 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
     }
     int cls = 0;
     while (cls < kClasses - 1 && M > class_max(cls)) ++cls;
+    if (q < nq && M > mmax) {  // more candidates than L*R: only possible for bad direct segments
+      atomicAdd(err, 1ull);
+      for (uint32_t j = 0; j < k; ++j) {
+        out_ids[q * k + j] = kEmpty;
+        out_counts[q * k + j] = 0;
+      }
+      cls = kClasses;  // in no list
+    }
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) {
       const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
@@ -145,7 +154,7 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
   constexpr uint32_t S = 1u << LOG2S;
   constexpr uint32_t MASK = S - 1;
   extern __shared__ __align__(16) uint8_t sm[];
-  const uint32_t L = a.L, k = a.k;
+  const uint32_t L = a.L, CM = a.cmax, k = a.k;  // L segments per query; counts <= CM
   const uint32_t kp2 = pow2_ceil_q(k);
   uint64_t* outbuf = reinterpret_cast<uint64_t*>(sm);      // [kp2]
   uint64_t* base = outbuf + kp2;                             // [L]
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         uint32_t sz = 0;
         uint64_t st = 0;
         if (t < L) {
-          const uint32_t ad = a.addrs[q * L + t];
+          const uint32_t ad = a.direct ? (uint32_t)q : a.addrs[q * L + t];
           if (ad < a.range) {
             const uint64_t i = (uint64_t)t * a.range + ad;
             st = a.goff[i];
@@ -286,7 +295,7 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
       if (j < D) c = cnt[list[j]];
       const uint32_t ones = __ballot_sync(kFullMask, c == 1);
       if (lane == 0 && ones) atomicAdd(&hist[1], __popc(ones));
-      if (c > 1) atomicAdd(&hist[c < L ? c : L], 1u);
+      if (c > 1) atomicAdd(&hist[c < CM ? c : CM], 1u);
     }
     __syncthreads();
 
@@ -294,8 +303,8 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
     if (warp == 0) {
       uint32_t cstar = 0, need = 0, ties = 0;
       if (D > k) {
-        const uint32_t cs = (L + 31) / 32;  // counts per lane, lane 0 = highest counts
-        const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
+        const uint32_t cs = (CM + 31) / 32;  // counts per lane, lane 0 = highest counts
+        const int32_t hi = (int32_t)CM - (int32_t)(lane * cs);
         const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
         uint32_t sum = 0;
         for (int32_t c = hi; c >= lo; --c) sum += hist[c];
@@ -477,7 +486,7 @@ size_t class_smem(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
 template <int LOG2S, int NT>
 int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t hist_len,
                  cudaStream_t s) {
-  const size_t smem = class_smem(LOG2S, a.L, a.k, hist_len);
+  const size_t smem = class_smem(LOG2S, a.L > a.cmax ? a.L : a.cmax, a.k, hist_len);
   static size_t attr = 48 * 1024;
   if (smem > attr) {
     if (cudaFuncSetAttribute(k_query<LOG2S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -519,12 +528,13 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   const uint64_t warps = (a.nq + 31) / 32;
   uint64_t blocks = (warps + 7) / 8;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
-  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, lists, counts, a.err);
-  const uint32_t hist_len = (a.L + 1) > 1024 ? a.L + 1 : 1024;
+  const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
+  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, a.direct, max_m, a.k,
+                                                 a.out_ids, a.out_counts, lists, counts, a.err);
+  const uint32_t hist_len = (a.cmax + 1) > 1024 ? a.cmax + 1 : 1024;
   // The class kernels are persistent over their device-side query lists and run back to
   // back on the caller's stream (measured: overlapping them on side streams is slower,
   // since kernels with different shared-memory footprints then share the SMs).
-  const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
   int n = 1;
   for (int c = 0; c < kClasses; ++c) {
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large

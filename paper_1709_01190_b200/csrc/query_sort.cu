@@ -88,12 +88,12 @@ __device__ __forceinline__ void warp_sort_range(uint32_t* arr, uint32_t lo, uint
   }
 }
 
-__host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins, uint32_t L) {
+__host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins, uint32_t L, uint32_t CM) {
   size_t b = (size_t)mcap * 4            // ids, sorted in place by bin
              + (size_t)(kBins > mcap ? kBins : mcap) * 2  // u16 bin counters, later distinct counts
-             + (size_t)L * 8              // base of each non-empty bucket
+             + (size_t)L * 8              // base of each non-empty segment (bucket)
              + ((size_t)mcap / 32 + 2) * 4  // bucket-start bitmap
-             + (size_t)(L + 1) * 4;       // count histogram
+             + (size_t)(CM + 1) * 4;      // count histogram
   return (b + 15) & ~(size_t)15;
 }
 
@@ -103,9 +103,10 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   constexpr uint32_t NBW = MCAP / 32 + 2;
   constexpr uint32_t kBins = 1u << BINS_LOG2;
   extern __shared__ __align__(16) uint8_t sms[];
-  const uint32_t L = a.L, k = a.k;
+  const uint32_t L = a.L, k = a.k;  // L segments (table buckets) per query
+  const uint32_t CM = a.cmax;        // counts are <= CM (the index's L)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t* my = sms + sort_slice_bytes(MCAP, kBins, L) * wib;
+  uint8_t* my = sms + sort_slice_bytes(MCAP, kBins, L, CM) * wib;
   uint32_t* arr = reinterpret_cast<uint32_t*>(my);                  // [MCAP]
   uint32_t* binw = arr + MCAP;                                      // [kBins/2] packed u16
   constexpr uint32_t CW = (kBins > MCAP ? kBins : MCAP) / 2;        // words of the u16 area
@@ -113,13 +114,13 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   // so candidate p of that bucket is nbase[j][p] (one wide multiply-add per gather)
   const uint32_t** nbase = reinterpret_cast<const uint32_t**>(binw + CW);  // [L]
   uint32_t* bmap = reinterpret_cast<uint32_t*>(nbase + L);                 // [NBW]
-  uint32_t* hcnt = bmap + NBW;                                      // [L+1]
+  uint32_t* hcnt = bmap + NBW;                                      // [CM+1]
   const uint16_t* bin16 = reinterpret_cast<const uint16_t*>(binw);
   const uint32_t* __restrict__ gids = a.ids;
 
   for (uint32_t j = lane; j < kBins / 2; j += 32) binw[j] = 0;
   for (uint32_t j = lane; j < NBW; j += 32) bmap[j] = 0;
-  for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+  for (uint32_t j = lane; j <= CM; j += 32) hcnt[j] = 0;
   __syncwarp();
 
   const uint32_t nq = *qcount;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       uint32_t sz = 0;
       uint64_t st = 0;
       if (t < L) {
-        const uint32_t ad = a.addrs[q * L + t];
+        const uint32_t ad = a.direct ? (uint32_t)q : a.addrs[q * L + t];
         if (ad < a.range) {
           const uint64_t i = (uint64_t)t * a.range + ad;
           st = a.goff[i];
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
           const uint32_t d = nd + __popc(em & lanemask_lt_s());
           arr[d] = x;
           cnt16[d] = (uint16_t)c;
-          atomicAdd(&hcnt[c < L ? c : L], 1u);
+          atomicAdd(&hcnt[c < CM ? c : CM], 1u);
         }
         nd += __popc(em);
         if (sm) carry = i0 + 31 - __clz(sm);
@@ -338,8 +339,8 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     //      histogram becomes the output cursor of each count above c* (higher counts first) ----
     uint32_t cstar = 0, need = 0xFFFFFFFFu, nhi = nd;
     {
-      const uint32_t cs = (L + 31) / 32;
-      const int32_t hi = (int32_t)L - (int32_t)(lane * cs);
+      const uint32_t cs = (CM + 31) / 32;
+      const int32_t hi = (int32_t)CM - (int32_t)(lane * cs);
       const int32_t lo = hi - (int32_t)cs + 1 > 1 ? hi - (int32_t)cs + 1 : 1;
       uint32_t sum = 0;
       for (int32_t c = hi; c >= lo; --c) sum += hcnt[c];
@@ -396,14 +397,14 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       while (um) {  // one group per distinct count in this chunk (usually 0-2)
         const uint32_t c0 = __shfl_sync(kFullS, c, __ffs(um) - 1);
         const uint32_t m = __ballot_sync(kFullS, up && c == c0);
-        const uint32_t base = hcnt[c0 < L ? c0 : L];
+        const uint32_t base = hcnt[c0 < CM ? c0 : CM];
         if (up && c == c0) {
           const uint32_t pos = base + __popc(m & lanemask_lt_s());
           oid[pos] = x;
           ocnt[pos] = c;
         }
         __syncwarp();
-        if (lane == 0) hcnt[c0 < L ? c0 : L] = base + __popc(m);
+        if (lane == 0) hcnt[c0 < CM ? c0 : CM] = base + __popc(m);
         __syncwarp();
         um &= ~m;
       }
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     }
     __syncwarp();
     if (nt > need) nt = need;
-    for (uint32_t j = lane; j <= L; j += 32) hcnt[j] = 0;
+    for (uint32_t j = lane; j <= CM; j += 32) hcnt[j] = 0;
     for (uint32_t j = lane; j < kBins / 2; j += 32) binw[j] = 0;
     for (uint32_t j = nhi + nt + lane; j < k; j += 32) {
       oid[j] = kEmpty;
@@ -434,7 +435,7 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
   // digit = the top BL bits of the id range [0, max_id]
   const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
   const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
-  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L) * kWarps;
+  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * kWarps;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
     if (cudaFuncSetAttribute(k_query_sort<MCAP, BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -123,3 +123,55 @@ def knn_graph_sharded_build(index, row_ptr_local, col_idx_local, k: int, bounds:
     excl = torch.arange(bounds[rank], bounds[rank] + n_local, dtype=torch.int64,
                         device=addrs_local.device).to(torch.int32)
     return index.query_addrs(addrs_local, k, excl)                             # Q1-Q3 (own rows)
+
+
+def _splits(x: torch.Tensor) -> list[int]:
+    return [int(v) for v in x.tolist()]
+
+
+def knn_graph_candidate_exchange(index, row_ptr_local, col_idx_local, k: int, bounds: list[int], rank: int,
+                                 group=None):
+    """Multi-GPU k-NN graph with the L tables PARTITIONED across GPUs and candidate lists
+    exchanged to each query's owner (north_star (d)):
+
+    1. H1-H3: rank g hashes its row shard; the addresses come out owner-blocked
+       (flash_hash_blocked), i.e. already in the send layout of
+    2. X1: all-to-all of address blocks: rank h receives, for every row, the addresses of
+       its own table window [t0(h), t1(h)) — [N][W_h], rows in global order;
+    3. B1-B2: rank h builds its window tables over all N rows (flash_insert_addrs_cols);
+    4. Q1 (window): rank h gathers every query's window buckets (flash_window_sizes /
+       flash_window_gather), in owner order, so each destination's share is contiguous;
+    5. X2: all-to-all of the per-query segment sizes, then all-to-all-v of the candidate
+       ids, to the query's owner (the rank that hashed the row);
+    6. Q2-Q3: the owner counts over its G segments per query and selects the top-k
+       (flash_count_topk) with exclude = global row id.
+    The candidate multiset of each query is exactly the union of its L buckets, so the
+    result is byte-identical to the 1-GPU graph at every world size."""
+    world = len(bounds) - 1
+    counts = [bounds[g + 1] - bounds[g] for g in range(world)]
+    n_local, n_total = counts[rank], bounds[-1]
+    L = index.L
+    wins = [table_window(L, world, g) for g in range(world)]
+    t0, t1 = wins[rank]
+    W = t1 - t0
+    dev = row_ptr_local.device
+    send = index.hash_addrs_blocked(row_ptr_local, col_idx_local, world)             # H1-H3
+    recv = torch.empty(n_total * W, dtype=torch.int32, device=dev)
+    dist.all_to_all_single(recv, send, [c * W for c in counts],                     # X1
+                           [n_local * (w1 - w0) for (w0, w1) in wins], group=group)
+    addrs_win = recv.view(n_total, W)
+    if W > 0 and n_total > 0:
+        index.insert_addrs_cols(addrs_win, 0, t0, t1)                                # B1-B2
+    sizes, off = index.window_sizes(addrs_win, t0, t1)                             # Q1 sizes
+    cuts = off[torch.tensor(bounds, dtype=torch.int64, device=off.device)]
+    send_tot = (cuts[1:] - cuts[:-1]).contiguous()
+    cand_send = index.window_gather(addrs_win, t0, t1, off, int(cuts[-1].item()))  # Q1 gather
+    seg_sizes = torch.empty(world * n_local, dtype=torch.int32, device=dev)
+    dist.all_to_all_single(seg_sizes, sizes.contiguous(), [n_local] * world, counts, group=group)   # X2a
+    recv_tot = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv_tot, send_tot, group=group)
+    rs, ss = _splits(recv_tot), _splits(send_tot)
+    cand_recv = torch.empty(sum(rs), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(cand_recv, cand_send, rs, ss, group=group)               # X2b
+    excl = torch.arange(bounds[rank], bounds[rank] + n_local, dtype=torch.int64, device=dev).to(torch.int32)
+    return index.count_topk(cand_recv, seg_sizes.view(world, n_local), k, max(n_total - 1, 0), excl)  # Q2-Q3

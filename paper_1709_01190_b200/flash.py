@@ -33,6 +33,8 @@ EXPORTS = (
     "flash_get_table", "flash_clear", "flash_check", "flash_insert_addrs_window",
     "flash_table_arrays", "flash_import_tables", "flash_set_profiling", "flash_phase_ms",
     "flash_launch_count", "flash_reset_counters", "flash_last_error",
+    "flash_hash_blocked", "flash_insert_addrs_cols", "flash_window_sizes", "flash_window_gather",
+    "flash_count_topk",
 )
 
 
@@ -77,6 +79,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.flash_launch_count.argtypes = [vp]
     L.flash_launch_count.restype = u64
     L.flash_reset_counters.argtypes = [vp]
+    L.flash_hash_blocked.argtypes = [vp, vp, vp, u64, u32, vp, vp]
+    L.flash_insert_addrs_cols.argtypes = [vp, vp, u64, u32, u32, u32, vp]
+    L.flash_window_sizes.argtypes = [vp, vp, u64, u32, u32, vp, vp, vp]
+    L.flash_window_gather.argtypes = [vp, vp, u64, u32, u32, vp, vp, vp]
+    L.flash_count_topk.argtypes = [vp, vp, vp, u32, u64, u32, vp, u32, vp, vp, vp]
     L.flash_last_error.argtypes = []
     L.flash_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -206,6 +213,31 @@ def flash_table_arrays(h):
 def flash_import_tables(h, goff, ids, n_ids, arrivals, max_id, stream=None):
     _check(load_library().flash_import_tables(h, _ptr(goff), _ptr(ids), n_ids, _ptr(arrivals), max_id,
                                               _stream(stream, goff)))
+
+
+def flash_hash_blocked(h, row_ptr, col_idx, n_rows, world, addrs, stream=None):
+    _check(load_library().flash_hash_blocked(h, _ptr(row_ptr), _ptr(col_idx), n_rows, world, _ptr(addrs),
+                                             _stream(stream, row_ptr)))
+
+
+def flash_insert_addrs_cols(h, addrs, n_rows, id_base, t_begin, t_end, stream=None):
+    _check(load_library().flash_insert_addrs_cols(h, _ptr(addrs), n_rows, id_base, t_begin, t_end,
+                                                  _stream(stream, addrs)))
+
+
+def flash_window_sizes(h, addrs, n_q, t_begin, t_end, sizes, offsets, stream=None):
+    _check(load_library().flash_window_sizes(h, _ptr(addrs), n_q, t_begin, t_end, _ptr(sizes), _ptr(offsets),
+                                             _stream(stream, offsets)))
+
+
+def flash_window_gather(h, addrs, n_q, t_begin, t_end, offsets, out_ids, stream=None):
+    _check(load_library().flash_window_gather(h, _ptr(addrs), n_q, t_begin, t_end, _ptr(offsets), _ptr(out_ids),
+                                              _stream(stream, offsets)))
+
+
+def flash_count_topk(h, cand, seg_sizes, n_seg, n_q, k, exclude, max_id, out_ids, out_counts, stream=None):
+    _check(load_library().flash_count_topk(h, _ptr(cand), _ptr(seg_sizes), n_seg, n_q, k, _ptr(exclude), max_id,
+                                           _ptr(out_ids), _ptr(out_counts), _stream(stream, seg_sizes)))
 
 
 def flash_clear(h, stream=None):
@@ -348,3 +380,37 @@ class FlashIndex:
 
     def errors(self) -> int:
         return flash_check(self.h)
+
+    # ---- candidate exchange (dist.knn_graph_candidate_exchange) ----
+    def hash_addrs_blocked(self, row_ptr, col_idx, world: int):
+        """Addresses of the rows, owner-blocked for `world` table windows (flat int32 [n*L])."""
+        n = row_ptr.numel() - 1
+        a = torch.empty(n * self.L, dtype=torch.int32, device=self.device)
+        flash_hash_blocked(self.h, row_ptr, col_idx, n, world, a)
+        return a
+
+    def insert_addrs_cols(self, addrs, id_base, t_begin, t_end):
+        flash_insert_addrs_cols(self.h, addrs, addrs.shape[0], id_base, t_begin, t_end)
+
+    def window_sizes(self, addrs, t_begin, t_end):
+        """(sizes int32 [n], offsets int64 [n+1]) of the window's candidates per query."""
+        n = addrs.shape[0]
+        sizes = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)[:n]
+        off = torch.empty(n + 1, dtype=torch.int64, device=self.device)
+        flash_window_sizes(self.h, addrs, n, t_begin, t_end, sizes, off)
+        return sizes, off
+
+    def window_gather(self, addrs, t_begin, t_end, offsets, total: int):
+        out = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+        flash_window_gather(self.h, addrs, addrs.shape[0], t_begin, t_end, offsets, out)
+        return out[:total]
+
+    def count_topk(self, cand, seg_sizes, k, max_id: int, exclude=None):
+        """seg_sizes int32 [n_seg, n_q]; cand int32 in (segment, query) order; max_id bounds
+        the candidate ids (it sets the sort's digit range: pass the real bound)."""
+        n_seg, n_q = seg_sizes.shape
+        ids = torch.empty((n_q, k), dtype=torch.int32, device=self.device)
+        cnt = torch.empty((n_q, k), dtype=torch.int32, device=self.device)
+        flash_count_topk(self.h, cand if cand.numel() else None, seg_sizes.contiguous(), n_seg, n_q, k,
+                         exclude, int(max_id), ids, cnt)
+        return ids, cnt

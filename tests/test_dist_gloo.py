@@ -68,6 +68,62 @@ class OracleIndex:
         arr = arrivals.numpy().view(np.uint32).reshape(self.L, self.range).copy()
         self.T = oracle.Tables(self.L, self.R, self.range, arr, off, kept, stride)
 
+    # ---- candidate-exchange stand-ins (same semantics as the C ABI, computed by the oracle) ----
+    def hash_addrs_blocked(self, row_ptr, col_idx, world):
+        a = self.hash_addrs(row_ptr, col_idx).numpy().view(np.uint32)
+        blocks = [a[:, fdist.table_window(self.L, world, g)[0]: fdist.table_window(self.L, world, g)[1]].reshape(-1)
+                  for g in range(world)]
+        return torch.from_numpy(np.concatenate(blocks).view(np.int32))
+
+    def insert_addrs_cols(self, addrs, id_base, t0, t1):
+        a = np.full((addrs.shape[0], self.L), 0xFFFFFFFF, np.uint32)
+        a[:, t0:t1] = addrs.numpy().view(np.uint32)
+        self.insert_addrs(torch.from_numpy(a.view(np.int32)), id_base)
+
+    def _window_lists(self, addrs, t0, t1):
+        a = addrs.numpy().view(np.uint32)
+        out = []
+        for q in range(a.shape[0]):
+            parts = []
+            for j, t in enumerate(range(t0, t1)):
+                if self.T is not None and a[q, j] != 0xFFFFFFFF:
+                    off, kept, _ = self.T.table(t)
+                    parts.append(kept[off[a[q, j]]: off[a[q, j] + 1]])
+            out.append(np.concatenate(parts) if parts else np.zeros(0, np.uint32))
+        return out
+
+    def window_sizes(self, addrs, t0, t1):
+        lists = self._window_lists(addrs, t0, t1)
+        sizes = np.array([x.size for x in lists], np.int64)
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        return torch.from_numpy(sizes.astype(np.int32)), torch.from_numpy(off.astype(np.int64))
+
+    def window_gather(self, addrs, t0, t1, offsets, total):
+        lists = self._window_lists(addrs, t0, t1)
+        out = np.concatenate(lists) if lists else np.zeros(0, np.uint32)
+        assert out.size == total
+        return torch.from_numpy(out.astype(np.uint32).view(np.int32))
+
+    def count_topk(self, cand, seg_sizes, k, max_id, exclude):
+        """Q2-Q3 over segments: the oracle's query on a stand-in index whose table s,
+        bucket q is segment (s, q)."""
+        sz = seg_sizes.numpy().astype(np.int64)
+        n_seg, n_q = sz.shape
+        c = cand.numpy().view(np.uint32)
+        off = np.zeros((n_seg, n_q + 1), np.uint32)
+        stride = max(1, int(sz.sum(axis=1).max()) if n_q else 1)
+        kept = np.zeros(n_seg * stride, np.uint32)
+        base = 0
+        for s_ in range(n_seg):
+            off[s_, 1:] = np.cumsum(sz[s_])
+            n = int(off[s_, -1])
+            kept[s_ * stride: s_ * stride + n] = c[base: base + n]
+            base += n
+        T = oracle.Tables(n_seg, self.R, n_q, np.zeros((n_seg, n_q), np.uint32), off, kept, stride)
+        qa = np.tile(np.arange(n_q, dtype=np.uint32)[:, None], (1, n_seg))
+        ids, cnt = oracle.query(T, qa, k, exclude=exclude.numpy().astype(np.int64).astype(np.uint32))
+        return torch.from_numpy(ids.view(np.int32)), torch.from_numpy(cnt.view(np.int32))
+
     def query_addrs(self, addrs, k, exclude):
         ids, cnt = oracle.query(self.T, addrs.numpy().view(np.uint32), k,
                                 exclude=exclude.numpy().astype(np.int64).astype(np.uint32))
@@ -88,7 +144,8 @@ def _worker(rank, world, port, out_dir, mode="replicated"):
         bounds = fdist.shard_bounds(lens, world)
         rp, col = synth.generate(shape, rows=(bounds[rank], bounds[rank + 1]))
         idx = OracleIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"])
-        fn = fdist.knn_graph_replicated if mode == "replicated" else fdist.knn_graph_sharded_build
+        fn = {"replicated": fdist.knn_graph_replicated, "sharded": fdist.knn_graph_sharded_build,
+              "exchange": fdist.knn_graph_candidate_exchange}[mode]
         ids, cnt = fn(idx, torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)), CFG["k"], bounds, rank)
         np.save(os.path.join(out_dir, f"ids_{rank}.npy"), ids.numpy())
         np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), cnt.numpy())
@@ -103,7 +160,7 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,mode", [(2, "replicated"), (3, "replicated"), (2, "sharded"), (3, "sharded"),
-                                        (5, "sharded")])
+                                        (5, "sharded"), (2, "exchange"), (3, "exchange"), (5, "exchange")])
 def test_distributed_graph_equals_single_process(tmp_path, world, mode):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, join=True)
     shape = _shape()

@@ -353,8 +353,86 @@ def test_table_windows_assemble_to_the_full_index():
             g_ids, g_cnt = imp.query_addrs(addrs, k, excl)
             assert np.array_equal(flash.as_u32(g_ids), o_ids)
             assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
-            T = oracle.build(L, R, rng, seed, flash.as_u32(addrs), np.arange(n, dtype=np.uint32))
+            o_addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+            T = oracle.build(L, R, rng, seed, o_addrs, np.arange(n, dtype=np.uint32))
             for t in (0, 17, 49):
                 off, ids_t, arr_t = imp.table(t)
                 o_off, o_ids_t, o_arr = T.table(t)
                 assert np.array_equal(off, o_off) and np.array_equal(ids_t, o_ids_t) and np.array_equal(arr_t, o_arr)
+
+
+@pytest.mark.parametrize("G,L", [(2, 50), (3, 50), (8, 50), (5, 4)])
+def test_candidate_exchange_loopback_equals_oracle_graph(G, L):
+    """The table-partitioned multi-GPU path (north_star (d), dist.knn_graph_candidate_exchange)
+    with G virtual ranks on one GPU: every C-ABI step runs for real (owner-blocked hash,
+    window build from the address all-to-all's layout, window gather, count/top-k over
+    the G received segments); the all-to-alls are done by slicing.  The graph must equal
+    the oracle's single-process graph exactly (G = 5 > L = 4 leaves a rank tableless)."""
+    from paper_1709_01190_b200 import dist as fdist
+
+    rp, col = shape_slice("webspam", 1500)
+    n = rp.size - 1
+    K, R, rng, seed, k = 4, 128, 1 << 12, 0x5EED0002, 64
+    o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
+    bounds = fdist.shard_bounds(np.diff(rp), G)
+    wins = [fdist.table_window(L, G, g) for g in range(G)]
+    cnts = [bounds[g + 1] - bounds[g] for g in range(G)]
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    idx = [flash.FlashIndex(K, L, R, rng, seed) for _ in range(G)]
+    try:
+        # H1-H3 per rank (owner-blocked), X1 by slicing
+        sends = [idx[g].hash_addrs_blocked(d_rp[bounds[g]: bounds[g + 1] + 1], d_col, G) for g in range(G)]
+        recv = []
+        for h in range(G):
+            w = wins[h][1] - wins[h][0]
+            recv.append(torch.cat([sends[s][cnts[s] * wins[h][0]: cnts[s] * wins[h][0] + cnts[s] * w]
+                                   for s in range(G)]).view(n, w))
+        sizes, offs, cands = [], [], []
+        for h in range(G):
+            t0, t1 = wins[h]
+            if t1 > t0:
+                idx[h].insert_addrs_cols(recv[h], 0, t0, t1)
+            sz, off = idx[h].window_sizes(recv[h], t0, t1)
+            sizes.append(sz)
+            offs.append(off)
+            cands.append(idx[h].window_gather(recv[h], t0, t1, off, int(off[-1].item())))
+        for g in range(G):  # X2 by slicing, then Q2-Q3 on the owner
+            q0, q1 = bounds[g], bounds[g + 1]
+            seg = torch.stack([sizes[s][q0:q1] for s in range(G)])
+            cand = torch.cat([cands[s][int(offs[s][q0].item()): int(offs[s][q1].item())] for s in range(G)])
+            excl = torch.arange(q0, q1, dtype=torch.int32, device="cuda")
+            g_ids, g_cnt = idx[g].count_topk(cand, seg, k, n - 1, excl)
+            assert np.array_equal(flash.as_u32(g_ids), o_ids[q0:q1]), f"rank {g} ids"
+            assert np.array_equal(flash.as_u32(g_cnt), o_cnt[q0:q1]), f"rank {g} counts"
+        assert all(i.errors() == 0 for i in idx)
+    finally:
+        for i in idx:
+            i.close()
+
+
+def test_count_topk_on_raw_segments_matches_oracle_counting():
+    """flash_count_topk on arbitrary candidate segments (each id at most once per
+    segment, as in a table) equals the oracle's COUNTFREQUENCY + KSELECT on the same
+    multisets, including empty queries, k above the distinct count and excluded ids."""
+    rng_ = np.random.default_rng(7)
+    n_seg, n_q, L, k = 6, 300, 6, 20
+    segs = [[np.sort(rng_.choice(5000, size=int(rng_.integers(0, 120)), replace=False)).astype(np.uint32)
+             if q % 17 else np.zeros(0, np.uint32) for q in range(n_q)] for _ in range(n_seg)]
+    sizes = np.array([[segs[s][q].size for q in range(n_q)] for s in range(n_seg)], np.int32)
+    cand = np.concatenate([segs[s][q] for s in range(n_seg) for q in range(n_q)])
+    excl = rng_.integers(0, 5000, size=n_q).astype(np.uint32)
+    # oracle: one stand-in table per segment, bucket q = segment (s, q)
+    off = np.zeros((n_seg, n_q + 1), np.uint32)
+    stride = int(sizes.sum(axis=1).max())
+    kept = np.zeros(n_seg * stride, np.uint32)
+    for s in range(n_seg):
+        off[s, 1:] = np.cumsum(sizes[s])
+        kept[s * stride: s * stride + off[s, -1]] = np.concatenate(segs[s])
+    T = oracle.Tables(n_seg, 128, n_q, np.zeros((n_seg, n_q), np.uint32), off, kept, stride)
+    o_ids, o_cnt = oracle.query(T, np.tile(np.arange(n_q, dtype=np.uint32)[:, None], (1, n_seg)), k, exclude=excl)
+    with flash.FlashIndex(4, L, 128, 1 << 10, 1) as idx:
+        g_ids, g_cnt = idx.count_topk(torch.from_numpy(cand.view(np.int32)).cuda(),
+                                      torch.from_numpy(sizes).cuda(), k, 4999,
+                                      torch.from_numpy(excl.view(np.int32)).cuda())
+        assert np.array_equal(flash.as_u32(g_ids), o_ids)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
