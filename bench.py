@@ -470,6 +470,117 @@ def run_ours(args):
     return result
 
 
+# Secondary workloads (BASELINE.json configs[2], configs[3]): index every row, then answer
+# 10K sampled rows as queries with self-exclusion.  Index parameters from the
+# paper's own runs: url K=4, L=128, R=32, 2^15; kdd12 K=4,
+# L=32, R=64, 2^20.
+SHAPE_CFG = {
+    "url": dict(K=4, L=128, R=32, range_=1 << 15, seed=0x5EED0003, k=128, q=10_000, qseed=13),
+    "kdd12": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0004, k=128, q=10_000, qseed=14),
+}
+
+
+def sample_query_csr(h_rp, h_col, rows):
+    """CSR of the given rows (host numpy)."""
+    rp = np.asarray(h_rp)
+    lens = rp[rows + 1] - rp[rows]
+    q_rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = np.asarray(h_col)
+    q_col = np.concatenate([col[rp[r]: rp[r + 1]] for r in rows]) if len(rows) else np.zeros(1, col.dtype)
+    return q_rp, q_col
+
+
+def run_shape(args):
+    """N=1 line for the url / kdd12 shapes: one step = index all N rows (H1-H3, B1-B2) +
+    10K queries (H1-H3 of the query rows, Q1-Q3).  value = queries/s of the query phase;
+    the index time and hash nnz/s are reported beside it."""
+    import torch
+
+    from paper_1709_01190_b200 import flash
+
+    rank, world, local = dist_env()
+    assert world == 1, "--workload url/kdd12 runs on one GPU"
+    cfg = SHAPE_CFG[args.workload]
+    shape = synth.SHAPES[args.workload]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    h_rp, h_col, nnz = gen_local(shape, [0, shape.N], 0)
+    log(f"generated {shape.N} rows nnz={nnz} in {time.time() - t0:.1f}s")
+    rows = np.sort(np.random.default_rng(cfg["qseed"]).choice(shape.N, size=cfg["q"], replace=False))
+    q_rp, q_col = sample_query_csr(h_rp.numpy(), h_col.numpy(), rows)
+    d_rp, d_col = h_rp.to(dev), h_col.to(dev)
+    dq_rp = torch.from_numpy(q_rp).to(dev)
+    dq_col = torch.from_numpy(np.ascontiguousarray(q_col).view(np.int32)).to(dev)
+    excl = torch.from_numpy(rows.astype(np.uint32).view(np.int32)).to(dev)
+    k = cfg["k"]
+    out_ids = torch.empty((cfg["q"], k), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty((cfg["q"], k), dtype=torch.int32, device=dev)
+    idx = flash.FlashIndex(cfg["K"], cfg["L"], cfg["R"], cfg["range_"], cfg["seed"])
+    stream = torch.cuda.current_stream()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+
+    def step(ev=None):
+        idx.clear()
+        if ev:
+            ev[0].record(stream)
+        flash.flash_insert(idx.h, d_rp, d_col, shape.N, 0)
+        if ev:
+            ev[1].record(stream)
+        flash.flash_query_topk(idx.h, dq_rp, dq_col, cfg["q"], k, excl, out_ids, out_cnt)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flash.flash_reset_counters(idx.h)
+    flash.flash_set_profiling(idx.h, True)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            step(evs[i])
+        torch.cuda.synchronize()
+    index_ms = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+    query_ms = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    phase_ms, phase_calls = flash.flash_phase_ms(idx.h)
+    launches = flash.flash_launch_count(idx.h)
+    flash.flash_set_profiling(idx.h, False)
+    # the hash phase covers the N indexed rows and the Q query rows; split by nnz
+    hash_ms_all = phase_ms[0] / args.steps
+    q_nnz = int(q_rp[-1])
+    hash_ms_index = hash_ms_all * nnz / (nnz + q_nnz)
+    hbm_peak, peak_kind = peaks()
+    L_ = cfg["L"]
+    hash_bytes = 4 * nnz + 8 * (shape.N + 1) + 4 * L_ * shape.N
+    idx.close()
+    return {
+        "metric": METRIC,
+        "value": cfg["q"] / (query_ms * 1e-3),
+        "unit": "queries/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": index_ms + query_ms,
+        "index_time_s": index_ms * 1e-3,
+        "query_time_s": query_ms * 1e-3,
+        "hash_nnz_per_s": nnz / (hash_ms_index * 1e-3),
+        "phase_ms_per_step": {"hash": hash_ms_all, "build": phase_ms[1] / args.steps,
+                              "query": phase_ms[2] / args.steps},
+        "hash_roofline": {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms_index * 1e-3) / 1e9,
+                          "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
+                          "frac": hash_bytes / (hash_ms_index * 1e-3) / 1e9 / hbm_peak,
+                          "algorithmic_bytes": hash_bytes,
+                          "note": "densification makes this shape ALU-bound (DESIGN.md §6)"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": f"synthetic (synth/, {args.workload} shape, seed {shape.seed})",
+        "config": {"workload": f"{args.workload}-shaped: index all rows + {cfg['q']} sampled queries, top-{k}",
+                   "N": shape.N, "D": shape.D, "nnz": nnz, "nnz_per_row": round(nnz / shape.N, 1),
+                   "K": cfg["K"], "L": L_, "R": cfg["R"], "range": cfg["range_"], "k": k,
+                   "seed": cfg["seed"], "query_seed": cfg["qseed"], "parallelism": "1 GPU",
+                   "l2_policy": f"inputs larger than L2 (col_idx {4 * nnz / 1e9:.1f} GB vs 126 MB L2); no flush"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+
 def cpu_baseline(sample_queries: int, steps: int = 1):
     """The oracle as it stands on the host cores: full hash + build, a query sample."""
     import oracle
@@ -532,7 +643,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
     ap.add_argument("--quality-queries", type=int, default=1000)
+    ap.add_argument("--workload", choices=["webspam", "url", "kdd12"], default="webspam",
+                    help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines")
     args = ap.parse_args()
+    if args.workload != "webspam" and args.impl == "ours":
+        print(json.dumps(run_shape(args)), flush=True)
+        return
     if args.impl == "reference":
         res = run_reference(args)
         if res is not None:

@@ -46,6 +46,8 @@ def lib():
         L.oracle_perm.argtypes, L.oracle_perm.restype = [u64, u32], u32
         L.oracle_probe.argtypes, L.oracle_probe.restype = [u64, u32, u32, u32], u32
         L.oracle_prio.argtypes, L.oracle_prio.restype = [u64, u32, u32, u32], u32
+        L.oracle_prio_batch.argtypes = [u64, vp, vp, vp, u64, vp]
+        L.oracle_prio_batch.restype = None
         L.oracle_doph.argtypes = [u32, u32, u64, vp, vp, u64, vp]
         L.oracle_addresses.argtypes = [u32, u32, u32, u64, vp, u64, vp]
         L.oracle_build.argtypes = [u32, u32, u32, u64, vp, vp, u64, vp, vp, vp]
@@ -97,6 +99,17 @@ def probe(seed: int, i: int, a: int, B: int) -> int:
 
 def prio(seed: int, t: int, b: int, id_: int) -> int:
     return lib().oracle_prio(seed, t, b, id_)
+
+
+def prio_batch(seed: int, t, b, ids) -> np.ndarray:
+    """prio(t[i], b[i], ids[i]) for arrays of equal length (HASHSPEC B; R#9)."""
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    b = np.ascontiguousarray(b, dtype=np.uint32)
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    out = np.empty(max(t.size, 1), dtype=np.uint32)
+    if t.size:
+        lib().oracle_prio_batch(seed & 0xFFFFFFFFFFFFFFFF, _p(t), _p(b), _p(ids), t.size, _p(out))
+    return out[:t.size]
 
 
 # ---- the path -------------------------------------------------------------

@@ -105,6 +105,12 @@ uint32_t oracle_prio(uint64_t seed, uint32_t t, uint32_t b, uint32_t id) {
     return (uint32_t)(oracle_mix64(tb ^ (uint64_t)id) >> 32);
 }
 
+/* oracle_prio for n (t, b, id) triples (a loop over oracle_prio; for sampled checks). */
+void oracle_prio_batch(uint64_t seed, const uint32_t *t, const uint32_t *b, const uint32_t *id, uint64_t n,
+                       uint32_t *out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = oracle_prio(seed, t[i], b[i], id[i]);
+}
+
 /* ------------------------------------------------------------------------- */
 /* DOPH (§2.3; §3.2(1)).                               */
 /* ------------------------------------------------------------------------- */
