@@ -32,9 +32,51 @@ __device__ __forceinline__ uint4 ld_stream4(const uint4* p) {
   return v;
 }
 
+// Two 16-byte streaming loads issued back to back (one asm block, so the compiler cannot
+// sink the second load below the first one's uses: two tiles in flight per lane).
+__device__ __forceinline__ void ld_stream4x2(const uint4* p0, const uint4* p1, uint4& a, uint4& b) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%8];\n\t"
+      "ld.global.nc.L1::no_allocate.v4.u32 {%4, %5, %6, %7}, [%9];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p0), "l"(p1));
+}
+
+__host__ __device__ __forceinline__ uint32_t warp_words(uint32_t B) {
+  return 2 * B + (B + 1) / 2;  // v[B], code[B], u16 elist[B]
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt_d() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 __device__ __forceinline__ void bin_min(uint32_t* v, uint32_t B, const HashKeys& k, uint32_t c) {
   const uint32_t h = perm(k, c);
   atomicMin(&v[__umulhi(h, B)], h);
+}
+
+// H3 for one row (lanes over tables): fmix32 fold of each table's K-tuple, multiply-high to
+// [0, range).  world > 1 writes owner-blocked (flash_hash_blocked).
+__device__ __forceinline__ void write_addrs(const uint32_t* code, bool nonempty, uint32_t K, uint32_t L,
+                                            uint32_t range, const HashKeys& keys, uint32_t* __restrict__ addrs,
+                                            uint64_t n_rows, uint64_t r, uint32_t world, uint32_t lane) {
+  for (uint32_t t = lane; t < L; t += 32) {
+    uint32_t a = kEmpty;
+    if (nonempty) {
+      uint32_t x = fmix32(keys.s_addr ^ t);
+      for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
+      a = __umulhi(x, range);
+    }
+    if (world == 1) {
+      addrs[r * L + t] = a;
+    } else {  // owner-blocked: table t goes to the block of the rank whose window holds it
+      const uint32_t g = ((t + 1) * world - 1) / L;
+      const uint32_t g0 = (g * L) / world, g1 = ((g + 1) * L) / world;
+      addrs[n_rows * g0 + r * (g1 - g0) + (t - g0)] = a;
+    }
+  }
 }
 
 template <bool kCodes, bool kAddrs>
@@ -43,16 +85,19 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
                                                    uint64_t n_rows, uint32_t K, uint32_t L,
                                                    uint32_t range, HashKeys keys,
                                                    uint32_t* __restrict__ codes,
-                                                   uint32_t* __restrict__ addrs, uint32_t world) {
+                                                   uint32_t* __restrict__ addrs, uint32_t world,
+                                                   int64_t skip_le) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t wpb = blockDim.x >> 5;
-  uint32_t* v = smem + (size_t)warp * 2 * B;  // bin minima (pre-densification)
-  uint32_t* code = v + B;                      // densified codes of the current row
+  uint32_t* v = smem + (size_t)warp * warp_words(B);  // bin minima (pre-densification)
+  uint32_t* code = v + B;                              // densified codes of the current row
+  uint16_t* elist = reinterpret_cast<uint16_t*>(code + B);  // empty bins of the current row
 
   for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += (uint64_t)gridDim.x * wpb) {
+    if (row_ptr[r + 1] - row_ptr[r] <= skip_le) continue;  // a sparse row: k_doph_sparse's
     for (uint32_t i = lane; i < B; i += 32) v[i] = kEmpty;
     __syncwarp();
 
@@ -64,17 +109,30 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
     if (e + (int64_t)lane < head) bin_min(v, B, keys, ld_stream(col_idx + e + lane));
     e = head;
     const int64_t vec_end2 = e + ((end - e) & ~(int64_t)255);  // pairs of 512-B warp tiles
-    for (; e < vec_end2; e += 256) {  // two 16-B loads in flight per lane
-      const uint4 q0 = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e) + lane);
-      const uint4 q1 = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e + 128) + lane);
-      bin_min(v, B, keys, q0.x);
-      bin_min(v, B, keys, q0.y);
-      bin_min(v, B, keys, q0.z);
-      bin_min(v, B, keys, q0.w);
-      bin_min(v, B, keys, q1.x);
-      bin_min(v, B, keys, q1.y);
-      bin_min(v, B, keys, q1.z);
-      bin_min(v, B, keys, q1.w);
+    if (e < vec_end2) {  // software-pipelined: the next pair of tiles loads while this one hashes
+      uint4 q0, q1;
+      ld_stream4x2(reinterpret_cast<const uint4*>(col_idx + e) + lane,
+                   reinterpret_cast<const uint4*>(col_idx + e + 128) + lane, q0, q1);
+      while (true) {
+        const int64_t en = e + 256;
+        const bool more = en < vec_end2;
+        uint4 n0 = q0, n1 = q1;
+        if (more)
+          ld_stream4x2(reinterpret_cast<const uint4*>(col_idx + en) + lane,
+                       reinterpret_cast<const uint4*>(col_idx + en + 128) + lane, n0, n1);
+        bin_min(v, B, keys, q0.x);
+        bin_min(v, B, keys, q0.y);
+        bin_min(v, B, keys, q0.z);
+        bin_min(v, B, keys, q0.w);
+        bin_min(v, B, keys, q1.x);
+        bin_min(v, B, keys, q1.y);
+        bin_min(v, B, keys, q1.z);
+        bin_min(v, B, keys, q1.w);
+        e = en;
+        if (!more) break;
+        q0 = n0;
+        q1 = n1;
+      }
     }
     if (end - e >= 128) {  // one more whole tile
       const uint4 q = ld_stream4(reinterpret_cast<const uint4*>(col_idx + e) + lane);
@@ -88,50 +146,165 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
     __syncwarp();
 
     // ---- H2: densify (donors from v only) ----
-    bool nonempty = false;
-    for (uint32_t i = lane; i < B; i += 32) nonempty |= (v[i] != kEmpty);
-    nonempty = __any_sync(0xFFFFFFFFu, nonempty);
-    for (uint32_t i = lane; i < B; i += 32) {
-      uint32_t x = v[i];
-      if (x == kEmpty && nonempty) {
-        uint32_t j = 0;
-        for (uint32_t a = 1; a <= kProbes; ++a) {
-          j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B);
+    // Pass 1: non-empty bins keep their minimum; the empty bins are listed (ascending).
+    uint32_t ne = 0;
+    for (uint32_t i0 = 0; i0 < B; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t x = i < B ? v[i] : 0u;
+      const bool empty = i < B && x == kEmpty;
+      if (i < B && !empty) code[i] = x;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, empty);
+      if (empty) elist[ne + __popc(m & lanemask_lt_d())] = (uint16_t)i;
+      ne += __popc(m);
+    }
+    const bool nonempty = ne < B;
+    __syncwarp();
+    if (!nonempty) {  // empty row: every code stays EMPTY
+      for (uint32_t i = lane; i < B; i += 32) code[i] = kEmpty;
+    } else if (ne) {
+      // Pass 2: the probe chains of the empty bins, dynamically balanced over the lanes:
+      // a lane that finds its donor takes the next listed bin, so every step of the
+      // warp-uniform loop advances ~32 chains (a probe count per bin is geometric; a
+      // static bin-per-lane split would wait for the longest chain of each round).
+      uint32_t e = lane, a = 1, next = 32;
+      uint32_t i = e < ne ? elist[e] : 0u;
+      while (__any_sync(0xFFFFFFFFu, e < ne)) {
+        const bool active = e < ne;
+        bool hit = false;
+        uint32_t x = kEmpty;
+        if (active) {
+          const uint32_t j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B);
           x = v[j];
-          if (x != kEmpty) break;
-        }
-        if (x == kEmpty) {  // circular scan from the last probed bin
-          for (uint32_t m = 1; m <= B; ++m) {
-            uint32_t jj = j + m;
-            if (jj >= B) jj -= B;
-            x = v[jj];
-            if (x != kEmpty) break;
+          hit = x != kEmpty;
+          if (!hit && a == kProbes) {  // chain exhausted: circular scan from its last bin
+            for (uint32_t m = 1; m <= B; ++m) {
+              uint32_t jj = j + m;
+              if (jj >= B) jj -= B;
+              x = v[jj];
+              if (x != kEmpty) break;
+            }
+            hit = true;  // the row is non-empty, so the scan found a donor
           }
         }
+        const uint32_t done = __ballot_sync(0xFFFFFFFFu, hit);
+        if (hit) {
+          code[i] = x;
+          e = next + __popc(done & lanemask_lt_d());
+          a = 1;
+          if (e < ne) i = elist[e];
+        } else if (active) {
+          ++a;
+        }
+        next += __popc(done);
       }
-      code[i] = x;
-      if (kCodes) codes[r * B + i] = x;
     }
     __syncwarp();
+    if (kCodes)
+      for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = code[i];
 
     // ---- H3: L table addresses ----
-    if (kAddrs) {
-      for (uint32_t t = lane; t < L; t += 32) {
-        uint32_t a = kEmpty;
-        if (nonempty) {
-          uint32_t x = fmix32(keys.s_addr ^ t);
-          for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
-          a = __umulhi(x, range);
-        }
-        if (world == 1) {
-          addrs[r * L + t] = a;
-        } else {  // owner-blocked: table t goes to the block of the rank whose window holds it
-          const uint32_t g = ((t + 1) * world - 1) / L;
-          const uint32_t g0 = (g * L) / world, g1 = ((g + 1) * L) / world;
-          addrs[n_rows * g0 + r * (g1 - g0) + (t - g0)] = a;
-        }
-      }
+    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Very sparse rows (nnz <= kSparseNnz, B <= kSparseMaxB: the kdd12 shape, 11 nnz into
+// 128 bins).  Probing costs ~B/|NE| probes per empty bin, each a dependent hash + load,
+// with per-lane divergence; here the chains are tabulated once per CTA instead:
+//   first[j*B + i] = the first position a <= T at which bin i's chain probes bin j
+//                    (255: never), data-independent (HASHSPEC H2).
+// An empty bin's donor is then the non-empty bin j minimising first[j*B + i] — the same
+// bin the chain reaches first — found with |NE| (<= nnz) uniform table lookups per lane,
+// no divergence.  A bin whose T probes all miss falls back to the circular scan from its
+// last probe, i.e. the first non-empty bin after it (a search in the sorted NE list).
+// One warp per row; persistent CTAs (the table is built once per CTA).
+constexpr uint32_t kSparseNnz = 32;
+constexpr uint32_t kSparseMaxB = 256;
+
+__host__ __device__ __forceinline__ uint32_t sparse_warp_words(uint32_t B) {
+  return 2 * B + (B + 3) / 4 + (B + 3) / 4;  // v[B], code[B], u8 NE list, u8 empty list
+}
+
+template <bool kCodes, bool kAddrs>
+__global__ void __launch_bounds__(kThreads) k_doph_sparse(const int64_t* __restrict__ row_ptr,
+                                                          const uint32_t* __restrict__ col_idx,
+                                                          uint64_t n_rows, uint32_t K, uint32_t L,
+                                                          uint32_t range, HashKeys keys,
+                                                          uint32_t* __restrict__ codes,
+                                                          uint32_t* __restrict__ addrs, uint32_t world) {
+  extern __shared__ uint32_t smem[];
+  const uint32_t B = K * L;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  uint8_t* first = reinterpret_cast<uint8_t*>(smem);  // [B][B]
+  uint32_t* v = smem + (B * B + 3) / 4 + (size_t)warp * sparse_warp_words(B);
+  uint32_t* code = v + B;
+  uint8_t* nel = reinterpret_cast<uint8_t*>(code + B);  // non-empty bins, ascending
+  uint8_t* eel = nel + ((B + 3) & ~3u);                 // empty bins
+
+  for (uint32_t x = threadIdx.x; x < (B * B + 3) / 4; x += blockDim.x) smem[x] = 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x)
+    for (uint32_t a = kProbes; a >= 1; --a)  // descending: the smallest position wins
+      first[__umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B) * B + i] = (uint8_t)a;
+  __syncthreads();
+
+  const uint64_t nw = (uint64_t)gridDim.x * wpb;
+  for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += nw) {
+    const int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    if (e1 - e0 > (int64_t)kSparseNnz) continue;  // k_doph's
+    for (uint32_t i = lane; i < B; i += 32) v[i] = kEmpty;
+    __syncwarp();
+    if (e0 + (int64_t)lane < e1) bin_min(v, B, keys, col_idx[e0 + lane]);  // H1
+    __syncwarp();
+    // NE / empty lists (ascending bin order); non-empty bins keep their minimum
+    uint32_t nne = 0, ne = 0;
+    for (uint32_t i0 = 0; i0 < B; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t x = i < B ? v[i] : kEmpty;
+      const bool full = x != kEmpty;
+      if (full) code[i] = x;
+      const uint32_t mf = __ballot_sync(0xFFFFFFFFu, full);
+      const uint32_t me = __ballot_sync(0xFFFFFFFFu, i < B && !full);
+      if (full) nel[nne + __popc(mf & lanemask_lt_d())] = (uint8_t)i;
+      if (i < B && !full) eel[ne + __popc(me & lanemask_lt_d())] = (uint8_t)i;
+      nne += __popc(mf);
+      ne += __popc(me);
     }
+    __syncwarp();
+    const bool nonempty = nne > 0;
+    for (uint32_t e = lane; e < ne; e += 32) {  // H2 (R#4) by table lookups
+      const uint32_t i = eel[e];
+      uint32_t x = kEmpty;
+      if (nonempty) {
+        uint32_t best = 255, dj = 0;
+        for (uint32_t k = 0; k < nne; ++k) {
+          const uint32_t j = nel[k];
+          const uint32_t f = first[j * B + i];
+          if (f < best) {
+            best = f;
+            dj = j;
+          }
+        }
+        if (best == 255) {  // every probe missed: first non-empty bin after the T-th probe
+          const uint32_t j0 = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | kProbes)), B);
+          dj = nel[0];
+          for (uint32_t k = 0; k < nne; ++k) {
+            const uint32_t j = nel[k];
+            if (j > j0) {
+              dj = j;
+              break;
+            }
+          }
+        }
+        x = v[dj];
+      }
+      code[i] = x;
+    }
+    __syncwarp();
+    if (kCodes)
+      for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = code[i];
+    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
     __syncwarp();
   }
 }
@@ -141,7 +314,27 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
              uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
              uint32_t world, cudaStream_t s) {
   const uint32_t B = K * L;
-  const size_t per_warp = (size_t)2 * B * sizeof(uint32_t);
+  int launched = 0;
+  int64_t skip_le = -1;
+  if (B <= kSparseMaxB) {  // rows with <= kSparseNnz nonzeros: the table-driven kernel
+    const size_t smem = ((size_t)(B * B + 3) / 4 + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
+    static bool attr_s = false;
+    if (!attr_s) {
+      cudaFuncSetAttribute(k_doph_sparse<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      attr_s = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t blocks = 148ull * per_sm;
+    const uint64_t need = (n_rows + kThreads / 32 - 1) / (kThreads / 32);
+    if (blocks > need) blocks = need;
+    k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
+                                                                 codes, addrs, world);
+    ++launched;
+    skip_le = kSparseNnz;
+  }
+  const size_t per_warp = (size_t)warp_words(B) * sizeof(uint32_t);
   int wpb = (int)((96 * 1024) / per_warp);
   wpb = wpb < 1 ? 1 : (wpb > kThreads / 32 ? kThreads / 32 : wpb);
   const size_t smem = per_warp * wpb;
@@ -151,12 +344,14 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     attr = smem;
   }
   uint64_t blocks = (n_rows + wpb - 1) / wpb;  // one warp per row: the block scheduler balances
-  const uint64_t cap = 0x7FFFFFFFull;             // the skewed row lengths
+  // the skewed row lengths; with the sparse kernel in use, a grid-stride cap keeps the launch
+  // from scheduling millions of CTAs that would only skip sparse rows
+  const uint64_t cap = skip_le >= 0 ? 65536ull : 0x7FFFFFFFull;
   if (blocks > cap) blocks = cap;
-  if (blocks == 0) return 0;
+  if (blocks == 0) return launched;
   k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                         codes, addrs, world);
-  return 1;
+                                                         codes, addrs, world, skip_le);
+  return launched + 1;
 }
 
 }  // namespace
