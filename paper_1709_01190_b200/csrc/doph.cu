@@ -96,14 +96,11 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
   uint32_t* code = v + B;                              // densified codes of the current row
   uint16_t* elist = reinterpret_cast<uint16_t*>(code + B);  // empty bins of the current row
 
-  for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += (uint64_t)gridDim.x * wpb) {
-    if (row_ptr[r + 1] - row_ptr[r] <= skip_le) continue;  // a sparse row: k_doph_sparse's
+  auto do_row = [&](const uint64_t r, int64_t e, const int64_t end) {
     for (uint32_t i = lane; i < B; i += 32) v[i] = kEmpty;
     __syncwarp();
 
     // ---- H1: stream the row.  16-byte loads once the cursor is 16-B aligned. ----
-    int64_t e = row_ptr[r];
-    const int64_t end = row_ptr[r + 1];
     const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(col_idx + e) & 15u);
     const int64_t head = min(end, e + (int64_t)(((16u - mis) & 15u) >> 2));
     if (e + (int64_t)lane < head) bin_min(v, B, keys, ld_stream(col_idx + e + lane));
@@ -205,6 +202,13 @@ __global__ void __launch_bounds__(kThreads) k_doph(const int64_t* __restrict__ r
     // ---- H3: L table addresses ----
     if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
     __syncwarp();
+  };
+
+  // one warp per row, the block scheduler balances skewed row lengths; rows with <= skip_le
+  // nonzeros belong to k_doph_sparse (their extents are read here anyway)
+  for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += (uint64_t)gridDim.x * wpb) {
+    const int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    if (e1 - e0 > skip_le) do_row(r, e0, e1);
   }
 }
 
@@ -250,9 +254,16 @@ __global__ void __launch_bounds__(kThreads) k_doph_sparse(const int64_t* __restr
   __syncthreads();
 
   const uint64_t nw = (uint64_t)gridDim.x * wpb;
-  for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += nw) {
-    const int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
-    if (e1 - e0 > (int64_t)kSparseNnz) continue;  // k_doph's
+  // chunks of 32 rows per warp: one coalesced read of their extents, then the sparse ones
+  for (uint64_t r0 = ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 += nw * 32) {
+   const uint64_t rl = r0 + lane;
+   const int64_t my_e0 = rl < n_rows ? row_ptr[rl] : 0, my_e1 = rl < n_rows ? row_ptr[rl + 1] : 0;
+   uint32_t todo = __ballot_sync(0xFFFFFFFFu, rl < n_rows && my_e1 - my_e0 <= (int64_t)kSparseNnz);
+   while (todo) {  // the others are k_doph's
+    const uint32_t src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint64_t r = r0 + src;
+    const int64_t e0 = __shfl_sync(0xFFFFFFFFu, my_e0, src), e1 = __shfl_sync(0xFFFFFFFFu, my_e1, src);
     for (uint32_t i = lane; i < B; i += 32) v[i] = kEmpty;
     __syncwarp();
     if (e0 + (int64_t)lane < e1) bin_min(v, B, keys, col_idx[e0 + lane]);  // H1
@@ -306,6 +317,7 @@ __global__ void __launch_bounds__(kThreads) k_doph_sparse(const int64_t* __restr
       for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = code[i];
     if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
     __syncwarp();
+   }
   }
 }
 
@@ -321,13 +333,14 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     static bool attr_s = false;
     if (!attr_s) {
       cudaFuncSetAttribute(k_doph_sparse<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaFuncSetAttribute(k_doph_sparse<C, A>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       attr_s = true;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t blocks = 148ull * per_sm;
-    const uint64_t need = (n_rows + kThreads / 32 - 1) / (kThreads / 32);
+    const uint64_t need = (n_rows + kThreads - 1) / kThreads;  // 32 rows per warp-chunk
     if (blocks > need) blocks = need;
     k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
                                                                  codes, addrs, world);
@@ -338,9 +351,12 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int wpb = (int)((96 * 1024) / per_warp);
   wpb = wpb < 1 ? 1 : (wpb > kThreads / 32 ? kThreads / 32 : wpb);
   const size_t smem = per_warp * wpb;
-  static size_t attr = 48 * 1024;
+  static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the column stream bypasses L1 (no_allocate): give the whole carveout to shared memory,
+    // so the per-warp bin arrays never cap the resident warps below the thread limit
+    cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = smem;
   }
   uint64_t blocks = (n_rows + wpb - 1) / wpb;  // one warp per row: the block scheduler balances
