@@ -118,6 +118,83 @@ __global__ void k_count(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t
   }
 }
 
+// Table-major build (large indexes).  When the per-bucket arrays (cursor 4 B + pool
+// offset 8 B per bucket) outgrow L2, the row-major passes above touch every table's arrays
+// from every warp and each atomic misses L2.  Instead the window's addresses are first
+// transposed to [W][n] (k_transpose_cols), and the histogram / scatter kernels run with a
+// table-major grid (block b covers table b / chunks, rows of chunk b % chunks): blocks are
+// dispatched in order, so the resident blocks share one or two tables whose arrays stay
+// L2-resident while every row passes through.
+constexpr uint32_t kTmRows = 4096;  // rows per block in the table-major passes
+
+__global__ void __launch_bounds__(256) k_transpose_cols(const uint32_t* __restrict__ addrs, uint64_t n,
+                                                        uint32_t astride, uint32_t c0, uint32_t W,
+                                                        uint32_t* __restrict__ out) {
+  __shared__ uint32_t tile[32][257];
+  const uint64_t r0 = (uint64_t)blockIdx.x * 256;
+  const uint32_t nr = (uint32_t)(n - r0 < 256 ? n - r0 : 256);
+  for (uint32_t cb = 0; cb < W; cb += 32) {
+    const uint32_t wc = W - cb < 32 ? W - cb : 32;
+    for (uint32_t k = threadIdx.x; k < nr * wc; k += 256) {  // row-major reads
+      const uint32_t rr = k / wc, cc = k - rr * wc;
+      tile[cc][rr] = addrs[(r0 + rr) * astride + c0 + cb + cc];
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < 256 * wc; k += 256) {  // column-major writes
+      const uint32_t cc = k >> 8, rr = k & 255;
+      if (rr < nr) out[(uint64_t)(cb + cc) * n + r0 + rr] = tile[cc][rr];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_count_tm(const uint32_t* __restrict__ addrsT, uint64_t n, uint32_t t0,
+                                                  uint32_t range, uint32_t chunks, uint32_t* __restrict__ cnt,
+                                                  unsigned long long* err) {
+  const uint32_t j = blockIdx.x / chunks, ch = blockIdx.x - j * chunks;
+  const uint64_t r0 = (uint64_t)ch * kTmRows;
+  const uint64_t r1 = n - r0 < kTmRows ? n : r0 + kTmRows;
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  uint32_t* c = cnt + (uint64_t)(t0 + j) * range;
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4 * 256) {
+    uint32_t a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = r + u * 256 < r1 ? col[r + u * 256] : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (a[u] == kEmpty) continue;
+      if (a[u] >= range) atomicAdd(err, 1ull);
+      else atomicAdd(&c[a[u]], 1u);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fill_tm(const uint32_t* __restrict__ addrsT, uint64_t n, uint32_t t0,
+                                                 uint32_t range, uint32_t chunks, uint32_t id_base,
+                                                 uint32_t* __restrict__ cursor, const uint64_t* __restrict__ pool_off,
+                                                 uint32_t* __restrict__ pool) {
+  const uint32_t j = blockIdx.x / chunks, ch = blockIdx.x - j * chunks;
+  const uint64_t r0 = (uint64_t)ch * kTmRows;
+  const uint64_t r1 = n - r0 < kTmRows ? n : r0 + kTmRows;
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  const uint64_t tb = (uint64_t)(t0 + j) * range;
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4 * 256) {
+    uint32_t a[4], pos[4];
+    uint64_t po[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = r + u * 256 < r1 ? col[r + u * 256] : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a[u] < range) {
+        pos[u] = atomicAdd(&cursor[tb + a[u]], 1u);
+        po[u] = pool_off[tb + a[u]];
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a[u] < range) pool[po[u] + pos[u]] = id_base + (uint32_t)(r + u * 256);
+  }
+}
+
 __global__ void k_pool_sizes(uint32_t nb, uint32_t R, const uint64_t* __restrict__ goff_old,
                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ arrivals,
                              uint64_t* __restrict__ pool_cnt, uint64_t* __restrict__ keep_cnt) {
@@ -435,7 +512,16 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
   cudaMemsetAsync(a.big_count, 0, 2 * sizeof(uint32_t), s);  // big + mid list counters
-  if (a.n) {
+  const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
+  const bool tm = a.addrsT != nullptr && a.n && W;  // table-major passes (see k_count_tm)
+  const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
+  if (tm) {
+    k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
+                                                                   a.addrsT);
+    k_count_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.cursor,
+                                                       a.err);
+    launches += 2;
+  } else if (a.n) {
     k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.cursor, a.err);
     launches++;
   }
@@ -451,7 +537,11 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);
     launches++;
   }
-  if (a.n) {
+  if (tm) {
+    k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,
+                                                      a.cursor, a.pool_off, a.pool);
+    launches++;
+  } else if (a.n) {
     k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.id_base,
                                            a.cursor, a.pool_off, a.pool);
     launches++;

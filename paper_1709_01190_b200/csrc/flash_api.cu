@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -102,6 +103,7 @@ struct flash_index {
   // scratch
   DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
   DevBuf seg_off, xscan_tmp;  // flash_count_topk segment offsets; exchange scans
+  DevBuf addrsT;              // build: window addresses transposed to [W][n] (table-major passes)
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -202,6 +204,11 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * kept_cap));
   TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 2)));
   TRY(ensure(h->scan_tmp, build_scan_tmp_bytes(nb)));
+  // Table-major passes once the per-bucket arrays (cursor + pool offset, 12 B per bucket)
+  // no longer fit comfortably in L2; FLASH_BUILD_TM=0/1 forces the choice (tests).
+  const char* tm_env = getenv("FLASH_BUILD_TM");
+  const bool tm = tm_env ? tm_env[0] == '1' : nb * 12 > (32ull << 20);
+  if (tm && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
 
   Phase ph(h, 1, s);
   BuildArgs a;
@@ -209,6 +216,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.addrs = addrs;
   a.astride = cols ? t1 - t0 : h->L;  // cols: addrs holds only the window's columns
   a.acol0 = cols ? t0 : 0;
+  a.addrsT = (tm && t1 > t0) ? h->addrsT.as<uint32_t>() : nullptr;
   a.n = n;
   a.id_base = id_base;
   a.L = h->L;
@@ -346,7 +354,7 @@ void flash_destroy(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT,
                     &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);

@@ -79,6 +79,7 @@ int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows
 struct BuildArgs {
   const uint32_t* addrs;  // row r, table t at addrs[r*astride + t - acol0]
   uint32_t astride, acol0;  // [n][L]: L, 0; a column window [n][t1-t0]: t1-t0, t0
+  uint32_t* addrsT;         // scratch [t1-t0][n] for the table-major passes, or null (row-major)
   uint64_t n;
   uint32_t id_base;
   uint32_t L, R, range;

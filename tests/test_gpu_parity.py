@@ -118,8 +118,12 @@ BUILD_CASES = [
 ]
 
 
+@pytest.mark.parametrize("tm", ["0", "1"], ids=["rowmajor", "tablemajor"])
 @pytest.mark.parametrize("name,make,K,L,R,rng", BUILD_CASES, ids=[c[0] for c in BUILD_CASES])
-def test_tables_bit_exact(name, make, K, L, R, rng):
+def test_tables_bit_exact(monkeypatch, name, make, K, L, R, rng, tm):
+    """Both build schedules: row-major passes, and the table-major passes (transposed
+    addresses, table-ordered grid) used for indexes whose bucket arrays outgrow L2."""
+    monkeypatch.setenv("FLASH_BUILD_TM", tm)
     rp, col = make()
     n = rp.size - 1
     seed = 0xB0 + R
@@ -152,7 +156,9 @@ def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch, mode):
             _check_tables(idx, T)
 
 
-def test_incremental_inserts_equal_one_build():
+@pytest.mark.parametrize("tm", ["0", "1"], ids=["rowmajor", "tablemajor"])
+def test_incremental_inserts_equal_one_build(monkeypatch, tm):
+    monkeypatch.setenv("FLASH_BUILD_TM", tm)
     rp, col = shape_slice("url", 5000)
     n = rp.size - 1
     K, L, R, rng, seed = 3, 20, 16, 1 << 9, 99
@@ -361,8 +367,8 @@ def test_table_windows_assemble_to_the_full_index():
                 assert np.array_equal(off, o_off) and np.array_equal(ids_t, o_ids_t) and np.array_equal(arr_t, o_arr)
 
 
-@pytest.mark.parametrize("G,L", [(2, 50), (3, 50), (8, 50), (5, 4)])
-def test_candidate_exchange_loopback_equals_oracle_graph(G, L):
+@pytest.mark.parametrize("G,L,tm", [(2, 50, "0"), (3, 50, "1"), (8, 50, "0"), (5, 4, "1")])
+def test_candidate_exchange_loopback_equals_oracle_graph(monkeypatch, G, L, tm):
     """The table-partitioned multi-GPU path (north_star (d), dist.knn_graph_candidate_exchange)
     with G virtual ranks on one GPU: every C-ABI step runs for real (owner-blocked hash,
     window build from the address all-to-all's layout, window gather, count/top-k over
@@ -370,6 +376,7 @@ def test_candidate_exchange_loopback_equals_oracle_graph(G, L):
     the oracle's single-process graph exactly (G = 5 > L = 4 leaves a rank tableless)."""
     from paper_1709_01190_b200 import dist as fdist
 
+    monkeypatch.setenv("FLASH_BUILD_TM", tm)
     rp, col = shape_slice("webspam", 1500)
     n = rp.size - 1
     K, R, rng, seed, k = 4, 128, 1 << 12, 0x5EED0002, 64
