@@ -26,6 +26,7 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kSelThreads = 256;
 constexpr uint32_t kWarpCap = 1024;   // per-warp sort buffer (u64 keys)
 constexpr uint32_t kBigCap = 4096;    // CTA path: kept ids sorted in smem (R <= kBigCap)
+constexpr uint32_t kMidMax = 256;     // register path (k_select_mid): m, R <= kMidMax
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -250,6 +251,7 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
                const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
                const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
                uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
+               uint32_t* __restrict__ reg_list, uint32_t* __restrict__ reg_count,
                uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -259,6 +261,7 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
     if (m == 0) continue;
     if (m > 32) {  // > 2048 members: the CTA path streams them with 256 threads
       if (force_big || m > 2048) push_big(i, big_list, big_count);
+      else if (m <= kMidMax && R <= kMidMax) push_big(i, reg_list, reg_count);
       else push_big(i, mid_list, mid_count);
       continue;
     }
@@ -274,6 +277,141 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
     }
     id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
     if (lane < keep) out[lane] = id;
+  }
+}
+
+// Ascending bitonic sort of E*32 u32 keys held E per lane (element index r*32 + lane).
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint32_t (&v)[E]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32u * E; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const uint32_t rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if ((r & rj) == 0) {
+            const bool up = ((r * 32 + lane) & k) == 0;
+            const uint32_t x = v[r], y = v[r | rj];
+            v[r] = up ? min(x, y) : max(x, y);
+            v[r | rj] = up ? max(x, y) : min(x, y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const uint32_t w = __shfl_xor_sync(kFull, v[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0, lower = (lane & j) == 0;
+          v[r] = (lower == up) ? min(v[r], w) : max(v[r], w);
+        }
+      }
+    }
+  }
+}
+
+// Sort the first n (<= E*32) ids of buf ascending and store them to out (one warp).
+template <int E>
+__device__ __forceinline__ void sort_store(const uint32_t* buf, uint32_t n, uint32_t* out) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t v[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r] = r * 32 + lane < n ? buf[r * 32 + lane] : kEmpty;
+  warp_sort_regs<E>(v);
+#pragma unroll
+  for (int r = 0; r < E; ++r)
+    if (r * 32 + lane < n) out[r * 32 + lane] = v[r];
+}
+
+template <int E>
+__device__ __forceinline__ void sort_store_upto(const uint32_t* buf, uint32_t n, uint32_t* out) {
+  if (E > 1 && n <= 32u * (E / 2)) {
+    sort_store_upto<(E > 1 ? E / 2 : 1)>(buf, n, out);
+    return;
+  }
+  sort_store<E>(buf, n, out);
+}
+
+// B2, buckets with 33..256 members (and R <= 256): one warp per bucket, members in
+// registers (8 per lane).  When m > R the bottom-R priority threshold is found by a
+// bitwise radix select over the 32-bit priorities (a warp reduction per bit, stopping as
+// soon as the keep-th smallest is pinned down, ~log2(m) bits); the kept ids are then
+// sorted ascending in registers.  Exact priority ties at the threshold (probability
+// ~m^2/2^33) go to the exact CTA path.
+__global__ void __launch_bounds__(256)
+k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restrict__ mid_list,
+             const uint32_t* __restrict__ mid_count, const uint64_t* __restrict__ pool_off,
+             const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
+             uint32_t* __restrict__ ids_out, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  __shared__ uint32_t kept_s[8][kMidMax];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* kbuf = kept_s[w];
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nmid = *mid_count;
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + w; it < nmid; it += nw) {
+    const uint32_t i = mid_list[it];
+    const uint64_t p0 = pool_off[i];
+    const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
+    uint32_t* out = ids_out + goff[i];
+    uint32_t id[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) id[u] = lane + 32u * u < m ? pool[p0 + lane + 32u * u] : kEmpty;
+    uint32_t keep = m;
+    if (m > R) {
+      const uint32_t t = i / range, b = i - t * range;
+      const uint64_t tb = prio_bucket_key(keys, t, b);
+      uint32_t pr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pr[u] = lane + 32u * u < m ? prio_of(tb, id[u]) : 0xFFFFFFFFu;
+      // radix select: the R-th smallest priority lies in [prefix, prefix + 2^(bit+1))
+      uint32_t prefix = 0, need = R, tot = m, ubound = 0;
+      bool done = false;
+      for (int bit = 31; bit >= 0 && !done; --bit) {
+        const uint32_t hi_mask = bit == 31 ? 0u : ~((2u << bit) - 1u);
+        uint32_t c = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          c += (lane + 32u * u < m) && (pr[u] & hi_mask) == prefix && !((pr[u] >> bit) & 1u);
+        const uint32_t c0 = __reduce_add_sync(kFull, c);
+        if (need <= c0) {
+          tot = c0;
+          if (need == c0) {
+            ubound = prefix + (1u << bit);  // keep every priority < ubound
+            done = true;
+          }
+        } else {
+          need -= c0;
+          tot -= c0;
+          prefix |= 1u << bit;
+          if (need == tot) {
+            ubound = prefix + (1u << bit);  // may wrap to 0 at the very top: handled below
+            done = true;
+          }
+        }
+      }
+      if (!done) {  // priorities tie at the threshold: exact CTA path
+        push_big(i, big_list, big_count);
+        continue;
+      }
+      // compact the kept ids (priority < ubound; ubound == 0 means 2^32) into shared memory
+      uint32_t base = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool k_ = (lane + 32u * u < m) && (ubound == 0 || pr[u] < ubound);
+        const uint32_t bal = __ballot_sync(kFull, k_);
+        if (k_) kbuf[base + __popc(bal & lanemask_lt())] = id[u];
+        base += __popc(bal);
+      }
+      keep = R;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (lane + 32u * u < m) kbuf[lane + 32u * u] = id[u];
+    }
+    __syncwarp();
+    sort_store_upto<8>(kbuf, keep, out);  // kept ids ascending (R#10)
+    __syncwarp();
   }
 }
 
@@ -511,7 +649,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < 148ull * 32 ? (a.n + 7) / 8 : 148ull * 32);
   const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
-  cudaMemsetAsync(a.big_count, 0, 2 * sizeof(uint32_t), s);  // big + mid list counters
+  cudaMemsetAsync(a.big_count, 0, 3 * sizeof(uint32_t), s);  // big, mid, register-path list counters
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
   const bool tm = a.addrsT != nullptr && a.n && W;  // table-major passes (see k_count_tm)
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
@@ -558,9 +696,15 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
   uint32_t* mid_list = a.cursor;  // free once k_fill_new is done
   uint32_t* mid_count = a.big_count + 1;
+  uint32_t* reg_list = reinterpret_cast<uint32_t*>(a.pool_cnt);  // free once pool_off is scanned
+  uint32_t* reg_count = a.big_count + 2;
   const unsigned small_blocks = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 64 ? ((uint64_t)nb + 7) / 8 : 148ull * 64);
   k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
-                                             a.ids_new, mid_list, mid_count, a.big_list, a.big_count);
+                                             a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
+                                             a.big_count);
+  k_select_mid<<<148 * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, a.pool, a.goff_new,
+                                       a.ids_new, a.big_list, a.big_count);
+  launches += 1;
   k_select_warp<<<148 * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
                                                       a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;

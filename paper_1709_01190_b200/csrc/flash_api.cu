@@ -202,12 +202,15 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
   TRY(ensure(h->pool, sizeof(uint32_t) * pool_cap));
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * kept_cap));
-  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 2)));
+  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 3)));
   TRY(ensure(h->scan_tmp, build_scan_tmp_bytes(nb)));
   // Table-major passes once the per-bucket arrays (cursor + pool offset, 12 B per bucket)
-  // no longer fit comfortably in L2; FLASH_BUILD_TM=0/1 forces the choice (tests).
+  // no longer fit comfortably in L2 and each table has enough buckets that the resident
+  // CTAs' atomics (all on one or two tables) do not pile onto the same counters (measured:
+  // kdd12, 2^20 buckets/table, 3.6x faster; url, 2^15, 2.6x slower); FLASH_BUILD_TM=0/1
+  // forces the choice (tests).
   const char* tm_env = getenv("FLASH_BUILD_TM");
-  const bool tm = tm_env ? tm_env[0] == '1' : nb * 12 > (32ull << 20);
+  const bool tm = tm_env ? tm_env[0] == '1' : (nb * 12 > (32ull << 20) && h->range >= (1u << 18));
   if (tm && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
 
   Phase ph(h, 1, s);

@@ -115,6 +115,10 @@ BUILD_CASES = [
     ("range2_R100_m2500_cta", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=5000)), 1, 2, 100, 2),
     ("webspam_slice", lambda: shape_slice("webspam", 1500), 4, 50, 128, 1 << 10),
     ("url_slice", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 12),
+    # 33..256 members per bucket: the register-resident select (k_select_mid)
+    ("mid_R16", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=20000, seed=9)), 2, 4, 16, 256),
+    ("mid_R64", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=20000, seed=9)), 2, 4, 64, 256),
+    ("mid_R200_all_kept", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=20000, seed=9)), 2, 4, 200, 256),
 ]
 
 
