@@ -316,10 +316,11 @@ def test_full_webspam_graph_sampled_parity():
     assert np.array_equal(flash.as_u32(g_cnt)[sample], o_cnt)
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
-    """compute-sanitizer finds no memory errors / shared-memory races on small graphs
-    (tools/sanitize_run.py: tiny, webspam, url shapes plus the edge-case rows)."""
+    """compute-sanitizer finds no memory errors / shared-memory races / barrier misuse on
+    small runs of every kernel family (tools/sanitize_run.py: tiny, webspam, url, kdd12
+    shapes plus the edge-case rows, both build schedules, the exchange steps)."""
     import shutil
     import subprocess
     import sys
