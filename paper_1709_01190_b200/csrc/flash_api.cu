@@ -104,6 +104,7 @@ struct flash_index {
   DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
   DevBuf seg_off, xscan_tmp;  // flash_count_topk segment offsets; exchange scans
   DevBuf addrsT;              // build: window addresses transposed to [W][n] (table-major passes)
+  DevBuf qhuge;               // query: global count tables of the L*R > 8192 class (kept clean)
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -253,6 +254,16 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   return FLASH_OK;
 }
 
+// The L*R > 8192 query class keeps its count tables in global memory: allocated and
+// cleared on first use (the kernels leave them clean).
+flash_status ensure_huge_table(flash_index* h, cudaStream_t s) {
+  if ((uint64_t)h->L * h->R <= 8192 || h->qhuge.p) return FLASH_OK;
+  TRY(ensure(h->qhuge, query_huge_table_bytes()));
+  query_huge_table_init(h->qhuge.p, s);
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
 flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64_t nq, uint32_t k,
                             const uint32_t* exclude, int exclude_self, uint32_t self_base,
                             uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s) {
@@ -264,6 +275,7 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
     return FLASH_OK;
   }
   TRY(ensure(h->qscratch, query_scratch_bytes(nq)));
+  TRY(ensure_huge_table(h, s));
   Phase ph(h, 2, s);
   QueryArgs a;
   a.addrs = addrs;
@@ -284,15 +296,15 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   a.table_log2 = h->table_log2;
   a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
   a.max_id = (uint32_t)h->max_id;
-  h->launches += launch_query(a, h->qscratch.p, s);
+  h->launches += launch_query(a, h->qscratch.p, h->qhuge.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }
 
 flash_status check_query_shape(const flash_index* h, uint32_t k) {
   if (k == 0 || k > FLASH_MAX_TOPK) return fail(FLASH_EINVAL, "k=%u outside [1, %u]", k, FLASH_MAX_TOPK);
-  if ((uint64_t)h->L * h->R > 8192)
-    return fail(FLASH_EINVAL, "L*R=%llu too large for the shared-memory count table (current limit L*R <= 8192)",
+  if ((uint64_t)h->L * h->R > 32768)
+    return fail(FLASH_EINVAL, "L*R=%llu too large for the count tables (limit L*R <= 32768)",
                 (unsigned long long)h->L * h->R);
   if (h->L > 4096) return fail(FLASH_EINVAL, "L=%u too large for the query kernel (limit 4096)", h->L);
   if (query_smem_bytes(h->table_log2, h->L, k) > 227 * 1024)
@@ -357,7 +369,7 @@ void flash_destroy(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge,
                     &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
@@ -688,6 +700,7 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
   TRY(ensure(h->seg_off, sizeof(uint64_t) * (nsq + 1)));
   TRY(ensure(h->xscan_tmp, scan_u32_to_u64_tmp_bytes(nsq)));
   TRY(ensure(h->qscratch, query_scratch_bytes(n_q)));
+  TRY(ensure_huge_table(h, s));
   Phase ph(h, 2, s);
   launch_scan_sizes(seg_sizes, nsq, h->seg_off.as<uint64_t>(), h->xscan_tmp.p, h->xscan_tmp.cap, s);
   QueryArgs a;
@@ -710,7 +723,7 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
   a.table_log2 = h->table_log2;
   a.packed = (max_id < 0xFFFFFEu && h->L <= 255) ? 1 : 0;
   a.max_id = max_id;
-  h->launches += launch_query(a, h->qscratch.p, s);
+  h->launches += launch_query(a, h->qscratch.p, h->qhuge.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }

@@ -128,7 +128,11 @@ struct QueryArgs {
   uint32_t max_id;          // largest id inserted (the sort kernel's digit range)
 };
 // scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
-int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s);
+// huge_tab: query_huge_table_bytes() of global memory initialised once with
+// query_huge_table_init (kept clean by the kernels), needed only when L*R > 8192
+int launch_query(const QueryArgs& a, void* scratch, void* huge_tab, cudaStream_t s);
+size_t query_huge_table_bytes();
+void query_huge_table_init(void* gtab, cudaStream_t s);
 size_t query_scratch_bytes(uint64_t nq);
 // radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,

@@ -44,9 +44,13 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
 constexpr int kSortClasses = 6;
 __host__ __device__ constexpr uint32_t class_max(int c) {
   return c == 0 ? 768u : c == 1 ? 1024u : c == 2 ? 1280u : c == 3 ? 1536u : c == 4 ? 2048u
-         : c == 5 ? 3072u : c == 6 ? 4096u : 8192u;
+         : c == 5 ? 3072u : c == 6 ? 4096u : c == 7 ? 8192u : 32768u;
 }
-constexpr int kClasses = kSortClasses + 2;
+// the last class (M <= 32768, indexes with L*R > 8192) keeps its count table of 2^16 slots
+// in a per-CTA region of global memory (L2-resident), since it exceeds shared memory
+constexpr int kClasses = kSortClasses + 3;
+constexpr uint32_t kHugeLog2 = 16;
+constexpr uint32_t kHugeCtas = 148;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              uint32_t L, uint32_t range, int direct, uint64_t mmax, uint32_t k,
@@ -148,9 +152,13 @@ struct QueryShared {
   uint32_t M, nlist, nout, cstar, need, ties, theta, maxid, done, prefix;
 };
 
-template <int LOG2S, int NT>
+// GLOBAL: keys / counts / list live in this CTA's slice of `gtab` (kept clean between
+// queries and launches: every query resets the slots it touched), read with ld.global.cg
+// so no stale L1 copy is seen after another thread's atomic.
+template <int LOG2S, int NT, bool GLOBAL>
 __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __restrict__ qlist,
-                                             const uint32_t* __restrict__ qcount, uint32_t hist_len) {
+                                             const uint32_t* __restrict__ qcount, uint32_t hist_len,
+                                             uint8_t* __restrict__ gtab) {
   constexpr uint32_t S = 1u << LOG2S;
   constexpr uint32_t MASK = S - 1;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -158,17 +166,32 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
   const uint32_t kp2 = pow2_ceil_q(k);
   uint64_t* outbuf = reinterpret_cast<uint64_t*>(sm);      // [kp2]
   uint64_t* base = outbuf + kp2;                             // [L]
-  uint32_t* keys = reinterpret_cast<uint32_t*>(base + L);    // [S]
-  uint32_t* pref = keys + S;                                 // [L+1]
+  uint32_t* pref = reinterpret_cast<uint32_t*>(base + L);    // [L+1]
   uint32_t* hist = pref + L + 1;                             // [hist_len]
-  uint32_t* cnt32 = hist + hist_len;                         // [S/2] (u16 counts)
+  uint32_t* keys;                                            // [S]
+  uint32_t* cnt32;                                           // [S/2] (u16 counts)
+  if (GLOBAL) {
+    if (blockIdx.x >= *qcount) return;
+    keys = reinterpret_cast<uint32_t*>(gtab) + (size_t)blockIdx.x * S;
+    cnt32 = reinterpret_cast<uint32_t*>(gtab) + (size_t)kHugeCtas * S + (size_t)blockIdx.x * (S / 2);
+  } else {
+    keys = hist + hist_len;
+    cnt32 = keys + S;
+  }
   uint16_t* cnt = reinterpret_cast<uint16_t*>(cnt32);
-  uint16_t* list = cnt + S;                                  // [S]
+  uint16_t* list = GLOBAL ? reinterpret_cast<uint16_t*>(reinterpret_cast<uint32_t*>(gtab) + (size_t)kHugeCtas * S * 3 / 2) +
+                                (size_t)blockIdx.x * S
+                          : reinterpret_cast<uint16_t*>(cnt32 + S / 2);  // [S]
+  auto ldk = [&](uint32_t slot) -> uint32_t { return GLOBAL ? __ldcg(&keys[slot]) : keys[slot]; };
+  auto ldc = [&](uint32_t slot) -> uint32_t { return GLOBAL ? (uint32_t)__ldcg(&cnt[slot]) : (uint32_t)cnt[slot]; };
+  auto ldl = [&](uint32_t j) -> uint32_t { return GLOBAL ? (uint32_t)__ldcg(&list[j]) : (uint32_t)list[j]; };
   __shared__ QueryShared sh;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (uint32_t j = tid; j < S; j += NT) keys[j] = kEmpty;
-  for (uint32_t j = tid; j < S / 2; j += NT) cnt32[j] = 0;
+  if (!GLOBAL) {
+    for (uint32_t j = tid; j < S; j += NT) keys[j] = kEmpty;
+    for (uint32_t j = tid; j < S / 2; j += NT) cnt32[j] = 0;
+  }
   for (uint32_t j = tid; j < hist_len; j += NT) hist[j] = 0;
   if (tid == 0) {
     sh.nlist = 0;
@@ -254,7 +277,7 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
             mymax = id > mymax ? id : mymax;
             uint32_t slot = (id * 0x9E3779B1u) >> (32 - LOG2S);
             while (true) {
-              uint32_t cur = keys[slot];
+              uint32_t cur = ldk(slot);
               if (cur == kEmpty) {
                 cur = atomicCAS(&keys[slot], kEmpty, id);
                 if (cur == kEmpty) {
@@ -292,7 +315,7 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
     for (uint32_t j0 = warp * 32; j0 < D; j0 += NT) {
       const uint32_t j = j0 + lane;
       uint32_t c = 0;
-      if (j < D) c = cnt[list[j]];
+      if (j < D) c = ldc(ldl(j));
       const uint32_t ones = __ballot_sync(kFullMask, c == 1);
       if (lane == 0 && ones) atomicAdd(&hist[1], __popc(ones));
       if (c > 1) atomicAdd(&hist[c < CM ? c : CM], 1u);
@@ -360,9 +383,9 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         __syncthreads();
         const uint32_t prefix = sh.prefix;
         for (uint32_t j = tid; j < D; j += NT) {
-          const uint32_t slot = list[j];
-          const uint32_t id = keys[slot];
-          if (cnt[slot] == cstar && (id & pmask) == prefix) atomicAdd(&hist[(id >> shift) & dmask], 1u);
+          const uint32_t slot = ldl(j);
+          const uint32_t id = ldk(slot);
+          if (ldc(slot) == cstar && (id & pmask) == prefix) atomicAdd(&hist[(id >> shift) & dmask], 1u);
         }
         __syncthreads();
         if (warp == 0) {
@@ -412,9 +435,9 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
       bool keep = false;
       uint64_t key = 0;
       if (j < D) {
-        const uint32_t slot = list[j];
-        const uint32_t c = cnt[slot];
-        const uint32_t id = keys[slot];
+        const uint32_t slot = ldl(j);
+        const uint32_t c = ldc(slot);
+        const uint32_t id = ldk(slot);
         keep = c > cstar || (c == cstar && id <= theta);
         key = ((uint64_t)(0xFFFFu - c) << 32) | id;
         keys[slot] = kEmpty;
@@ -476,30 +499,35 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
 }
 
 
-size_t class_smem(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len) {
+size_t class_smem(uint32_t log2s, uint32_t L, uint32_t k, uint32_t hist_len, bool global_table = false) {
   uint32_t kp2 = 1;
   while (kp2 < k) kp2 <<= 1;
-  const size_t S = (size_t)1 << log2s;
+  const size_t S = global_table ? 0 : (size_t)1 << log2s;
   return (size_t)kp2 * 8 + (size_t)L * 8 + S * 4 + (size_t)(L + 1) * 4 + (size_t)hist_len * 4 + S * 2 + S * 2;
 }
 
-template <int LOG2S, int NT>
+template <int LOG2S, int NT, bool GLOBAL>
 int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t hist_len,
-                 cudaStream_t s) {
-  const size_t smem = class_smem(LOG2S, a.L > a.cmax ? a.L : a.cmax, a.k, hist_len);
+                 uint8_t* gtab, cudaStream_t s) {
+  const size_t smem = class_smem(LOG2S, a.L > a.cmax ? a.L : a.cmax, a.k, hist_len, GLOBAL);
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query<LOG2S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(k_query<LOG2S, NT, GLOBAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return 0;
     attr = smem;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<LOG2S, NT>, NT, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = 148ull * per_sm;
+  uint64_t grid;
+  if (GLOBAL) {
+    grid = kHugeCtas;  // one table slice each (query_huge_table_bytes)
+  } else {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<LOG2S, NT, GLOBAL>, NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    grid = 148ull * per_sm;
+  }
   if (grid > a.nq) grid = a.nq;
-  k_query<LOG2S, NT><<<(unsigned)grid, NT, smem, s>>>(a, list, count, hist_len);
+  k_query<LOG2S, NT, GLOBAL><<<(unsigned)grid, NT, smem, s>>>(a, list, count, hist_len, gtab);
   return 1;
 }
 
@@ -514,13 +542,26 @@ uint32_t query_table_log2(uint32_t L, uint32_t R) {
 
 size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k) {
   const uint32_t hist_len = (L + 1) > 1024 ? L + 1 : 1024;
-  const uint32_t lg = table_log2 < 11 ? 11 : table_log2;
+  uint32_t lg = table_log2 < 11 ? 11 : table_log2;
+  if (lg > 14) lg = 14;  // the largest class keeps its table in global memory
   return class_smem(lg, L, k, hist_len);
+}
+
+size_t query_huge_table_bytes() {
+  const size_t S = (size_t)1 << kHugeLog2;
+  return kHugeCtas * (S * 4 + S * 2 + S * 2);  // keys, u16 counts, u16 list per CTA
+}
+
+void query_huge_table_init(void* gtab, cudaStream_t s) {
+  const size_t S = (size_t)1 << kHugeLog2;
+  cudaMemsetAsync(gtab, 0xFF, kHugeCtas * S * 4, s);                               // keys = EMPTY
+  cudaMemsetAsync(static_cast<uint8_t*>(gtab) + kHugeCtas * S * 4, 0, kHugeCtas * S * 2, s);  // counts
 }
 
 size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * kClasses + kClasses); }
 
-int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
+int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream_t s) {
+  uint8_t* huge_tab = static_cast<uint8_t*>(huge_tab_v);
   if (a.nq == 0) return 0;
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* counts = lists + a.nq * kClasses;
@@ -540,8 +581,9 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
     const uint32_t* lc = lists + (uint64_t)c * a.nq;
     if (c < kSortClasses) n += launch_query_sort(a, class_max(c), lc, counts + c, s);
-    else if (c == kSortClasses) n += launch_class<13, 256>(a, lc, counts + c, hist_len, s);
-    else n += launch_class<14, 256>(a, lc, counts + c, hist_len, s);
+    else if (c == kSortClasses) n += launch_class<13, 256, false>(a, lc, counts + c, hist_len, nullptr, s);
+    else if (c == kSortClasses + 1) n += launch_class<14, 256, false>(a, lc, counts + c, hist_len, nullptr, s);
+    else n += launch_class<kHugeLog2, 256, true>(a, lc, counts + c, hist_len, huge_tab, s);
   }
   return n;
 }

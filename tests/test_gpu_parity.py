@@ -191,6 +191,10 @@ QUERY_CASES = [
     ("webspam_dense_buckets_k128", lambda: shape_slice("webspam", 2500), 4, 50, 128, 1 << 7, 128),
     ("url_k128", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 15, 128),
     ("edge_k5", edge_csr, 4, 16, 4, 1000, 5),
+    # L*R = 10240 > 8192 with full buckets: M = 10240 candidates per query, the class whose
+    # count table lives in global memory
+    ("full_buckets_LR10240_k100", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=8000, seed=3)), 1, 40, 256, 16, 100),
+    ("LR32768_k64", lambda: shape_slice("webspam", 1500), 4, 128, 256, 1 << 12, 64),
 ]
 
 
@@ -289,7 +293,7 @@ def test_errors_and_states():
         bad = torch.full((4, 16), 1 << 20, dtype=torch.int32, device="cuda")  # >= range
         idx.insert_addrs(bad, 5000)
         assert idx.errors() == 64
-    with flash.FlashIndex(4, 64, 256, 1 << 15, 1) as idx:  # L*R = 16384: beyond the count table
+    with flash.FlashIndex(4, 128, 512, 1 << 15, 1) as idx:  # L*R = 65536: beyond the count tables
         with pytest.raises(flash.FlashError) as e:
             idx.query(d_rp, d_col, 5)
         assert e.value.status == flash.FLASH_EINVAL
