@@ -112,7 +112,10 @@ flash_status flash_import_tables(flash_index *h, const uint64_t *goff, const uin
 /* Querying phase (Alg. 3) for n_q CSR query rows: aggregate the L addressed
  * buckets, count each candidate's multiplicity (full count, R#11), drop exclude[q] (if
  * exclude != NULL, R#14), order by (count desc, id asc) (R#12), keep k, pad with
- * (FLASH_EMPTY, 0) (R#13).  out_ids / out_counts: [n_q][k] uint32.  1 <= k <= FLASH_MAX_TOPK. */
+ * (FLASH_EMPTY, 0) (R#13).  out_ids / out_counts: [n_q][k] uint32.  1 <= k <= FLASH_MAX_TOPK.
+ * Every query call (also flash_query_addrs, flash_knn_graph*, flash_count_topk) requires
+ * L*R <= FLASH_MAX_CANDIDATES (the count tables' capacity), else FLASH_EINVAL. */
+#define FLASH_MAX_CANDIDATES 32768u
 flash_status flash_query_topk(const flash_index *h, const int64_t *row_ptr, const uint32_t *col_idx,
                               uint64_t n_q, uint32_t k, const uint32_t *exclude, uint32_t *out_ids,
                               uint32_t *out_counts, void *stream);

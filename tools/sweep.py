@@ -1,0 +1,98 @@
+"""Parameter sweep on the webspam-shaped data (BASELINE.json configs[4]; SURVEY §8 table,
+cf. the paper's Fig. 5/6 sweeps): K in {2..6}, L in {16, 32, 64, 128}, R in
+{32, 64, 128, 256}, range 2^15, k = 128.  For every point: the full k-NN graph on one GPU
+(device-timed, median of --reps after a warm-up) with its hash / build / query split, and
+R@k / S@k of 1,000 sampled rows against exact binary cosine (computed once).
+
+    python tools/sweep.py [--out profiles/r01_sweep.json] [--reps 3] [--K 2,3,4,5,6] ...
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import synth  # noqa: E402
+from paper_1709_01190_b200 import flash  # noqa: E402
+
+
+def ints(s):
+    return [int(x) for x in s.split(",") if x]
+
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.json"))
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--K", type=ints, default=[2, 3, 4, 5, 6])
+ap.add_argument("--L", type=ints, default=[16, 32, 64, 128])
+ap.add_argument("--R", type=ints, default=[32, 64, 128, 256])
+ap.add_argument("--queries", type=int, default=1000)
+args = ap.parse_args()
+
+torch.cuda.set_device(0)
+shape = synth.SHAPES["webspam"]
+t0 = time.time()
+h_rp, h_col, nnz = bench.gen_local(shape, [0, shape.N], 0)
+d_rp, d_col = h_rp.cuda(), h_col.cuda()
+N, k = shape.N, 128
+print(f"generated {N} rows, {nnz} nnz in {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+t0 = time.time()
+crow, col, cnt, key = bench.dedup_csr(h_rp, d_col)
+del key
+qs = np.random.default_rng(13).choice(N, size=args.queries, replace=False)
+cos, best = bench.exact_cosine(crow, col, cnt, qs)
+del crow, col, cnt
+qsel = torch.from_numpy(qs).cuda()
+print(f"exact cosine for {qs.size} queries in {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+
+out_ids = torch.empty((N, k), dtype=torch.int32, device="cuda")
+out_cnt = torch.empty_like(out_ids)
+stream = torch.cuda.current_stream()
+rows = []
+for K in args.K:
+    for L in args.L:
+        for R in args.R:
+            rec = {"K": K, "L": L, "R": R, "range": 1 << 15, "k": k}
+            try:
+                idx = flash.FlashIndex(K, L, R, 1 << 15, bench.SEED)
+                times = []
+                flash.flash_set_profiling(idx.h, True)
+                for rep in range(args.reps + 1):
+                    idx.clear()
+                    if rep == 1:
+                        flash.flash_reset_counters(idx.h)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    flash.flash_knn_graph(idx.h, d_rp, d_col, N, k, out_ids, out_cnt)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    if rep > 0:
+                        times.append(e0.elapsed_time(e1))
+                ms, calls = flash.flash_phase_ms(idx.h)
+                idx.close()
+                g = statistics.median(times)
+                r_at, s_at = bench.recall_at_k(cos, best, out_ids[qsel], k)
+                rec.update({"graph_ms": g, "queries_per_s": N / (g * 1e-3),
+                            "hash_ms": ms[0] / args.reps, "build_ms": ms[1] / args.reps,
+                            "query_ms": ms[2] / args.reps, "R@k": r_at, "S@k": s_at})
+            except flash.FlashError as e:
+                rec["error"] = str(e)
+            rows.append(rec)
+            print(json.dumps(rec), flush=True)
+
+meta = {"workload": "webspam-shaped k-NN graph sweep (synth/ seed 2, N=350000, ~1.3G nnz)",
+        "queries_for_recall": int(qs.size), "gpu": torch.cuda.get_device_name(0), "n_gpus": 1,
+        "timing": f"device events, median of {args.reps} graphs after one warm-up",
+        "definition": "R@k: exact cosine 1-NN (any tie) in the reported top-k (P:393); "
+                      "S@k: mean exact cosine of the reported top-k (P:395)"}
+with open(args.out, "w") as f:
+    json.dump({"meta": meta, "points": rows}, f, indent=1)
+print(f"wrote {args.out}", file=sys.stderr)
