@@ -315,6 +315,32 @@ def sample_query_csr(h_rp, h_col, rows):
     return q_rp, q_col
 
 
+def shape_stats(idx, q_addrs, lens, L_, R_, rng_):
+    """SURVEY §8(d) statistics beside a secondary-shape timing, computed on the device from
+    the built index: nnz mean / p99, candidates per query (sum of its L bucket sizes) and
+    the bucket-arrival histogram (log2 bins).  Evaluation only."""
+    import torch
+
+    goff, _, arr = idx.table_arrays(ids=False)
+    sizes = goff[1:] - goff[:-1]
+    a = q_addrs.to(torch.int64) & 0xFFFFFFFF
+    valid = a < rng_
+    tb = torch.arange(L_, device=a.device, dtype=torch.int64)[None, :] * rng_
+    per_q = torch.where(valid, sizes[(tb + a.clamp(max=rng_ - 1))], torch.zeros_like(a)).sum(1).cpu().numpy()
+    arr = arr.to(torch.int64)
+    lg = torch.zeros_like(arr)
+    nz = arr > 0
+    lg[nz] = torch.floor(torch.log2(arr[nz].double())).to(torch.int64) + 1
+    hist = torch.bincount(lg, minlength=34)[:34].cpu().numpy()
+    top = int(np.nonzero(hist)[0].max()) if hist.any() else 0
+    labels = ["0"] + [f"{1 << (i - 1)}-{(1 << i) - 1}" for i in range(1, top + 1)]
+    return {"nnz_mean": float(lens.mean()), "nnz_p99": float(np.percentile(lens, 99)),
+            "candidates_per_query": {"mean": float(per_q.mean()), "p99": float(np.percentile(per_q, 99)),
+                                     "max": int(per_q.max())},
+            "bucket_arrivals": {"buckets": int(hist.sum()), "histogram_log2": dict(zip(labels, hist[: top + 1].tolist())),
+                                "frac_over_R": float((arr > R_).double().mean().item())}}
+
+
 def run_shape(args):
     """N=1 line for the url / kdd12 shapes: one step = index all N rows (H1-H3, B1-B2) +
     10K queries (H1-H3 of the query rows, Q1-Q3).  value = queries/s of the query phase;
@@ -370,6 +396,8 @@ def run_shape(args):
     phase_ms, phase_calls = flash.flash_phase_ms(idx.h)
     launches = flash.flash_launch_count(idx.h)
     flash.flash_set_profiling(idx.h, False)
+    stats = shape_stats(idx, idx.hash_addrs(dq_rp, dq_col), np.diff(h_rp.numpy()), cfg["L"], cfg["R"],
+                        cfg["range_"])
     # the hash phase covers the N indexed rows and the Q query rows; split by nnz
     hash_ms_all = phase_ms[0] / args.steps
     q_nnz = int(q_rp[-1])
@@ -403,6 +431,7 @@ def run_shape(args):
                    "l2_policy": f"inputs larger than L2 (col_idx {4 * nnz / 1e9:.1f} GB vs 126 MB L2); no flush"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "data_stats": stats,
     }
 
 

@@ -368,11 +368,12 @@ class FlashIndex:
     def insert_addrs_window(self, addrs, id_base, t_begin, t_end):
         flash_insert_addrs_window(self.h, addrs, addrs.shape[0], id_base, t_begin, t_end)
 
-    def table_arrays(self):
-        """Copies of (goff int64 [L*range+1], ids int32 [n], arrivals int32 [L*range])."""
+    def table_arrays(self, ids: bool = True):
+        """Copies of (goff int64 [L*range+1], ids int32 [n] (None unless ids), arrivals int32
+        [L*range])."""
         g, i, a, n = flash_table_arrays(self.h)
         nb = self.L * self.range
-        return (_copy_device(g, nb + 1, self.device, "<i8"), _copy_device(i, n, self.device),
+        return (_copy_device(g, nb + 1, self.device, "<i8"), _copy_device(i, n, self.device) if ids else None,
                 _copy_device(a, nb, self.device))
 
     def import_tables(self, goff, ids, arrivals, max_id):
