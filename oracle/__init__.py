@@ -46,6 +46,11 @@ def lib():
         L.oracle_perm.argtypes, L.oracle_perm.restype = [u64, u32], u32
         L.oracle_probe.argtypes, L.oracle_probe.restype = [u64, u32, u32, u32], u32
         L.oracle_prio.argtypes, L.oracle_prio.restype = [u64, u32, u32, u32], u32
+        L.oracle_reservoir.argtypes, L.oracle_reservoir.restype = [u64, u32, u32, u32, u32, u64], u32
+        L.oracle_build_pool.argtypes = [u32, u32, u32, u64, u64, vp, vp, u64, vp, vp, vp]
+        L.oracle_query_pool.argtypes = [u32, u32, u64, u64, vp, vp, vp, u64, u32, vp, vp, vp]
+        L.oracle_build_pool.restype = i32
+        L.oracle_query_pool.restype = i32
         L.oracle_prio_batch.argtypes = [u64, vp, vp, vp, u64, vp]
         L.oracle_prio_batch.restype = None
         L.oracle_doph.argtypes = [u32, u32, u64, vp, vp, u64, vp]
@@ -173,6 +178,68 @@ def query(tables: Tables, q_addrs: np.ndarray, k: int, exclude=None):
                               _p(q if nq else np.full((1, L), EMPTY, np.uint32)), nq, k,
                               _p(ex), _p(ids), _p(cnt)), "oracle_query")
     return ids[:nq], cnt[:nq]
+
+
+# ---- reservoir sharing (§3.2(4), §3.5; R#23) ---------------------
+
+def pool_size(F: float, L: int, range_: int) -> int:
+    """P = ceil(F * L * range) shared reservoirs ("Allocated Range = F * Actual Range")."""
+    import math
+    return max(1, min(L * range_, int(math.ceil(F * L * range_))))
+
+
+def reservoir(seed: int, t: int, b: int, L: int, range_: int, P: int) -> int:
+    return lib().oracle_reservoir(seed, t, b, L, range_, P)
+
+
+class PoolTables:
+    """Oracle index over a shared pool: arrivals [P], off [P+1], kept ids (flat)."""
+
+    def __init__(self, L, R, range_, P, arrivals, off, kept):
+        self.L, self.R, self.range, self.P = L, R, range_, P
+        self.arrivals, self.off, self.kept = arrivals, off, kept
+
+    def reservoir(self, r: int):
+        return self.kept[self.off[r]: self.off[r + 1]]
+
+
+def build_pool(L: int, R: int, range_: int, P: int, seed: int, addrs: np.ndarray, ids: np.ndarray) -> PoolTables:
+    """Adding phase over P shared reservoirs (oracle_build_pool)."""
+    addrs = np.ascontiguousarray(addrs, dtype=np.uint32).reshape(-1, L)
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    n = addrs.shape[0]
+    arrivals = np.empty(P, dtype=np.uint32)
+    off = np.empty(P + 1, dtype=np.uint32)
+    kept = np.empty(max(n * L, 1), dtype=np.uint32)
+    a = addrs if n else np.full((1, L), EMPTY, np.uint32)
+    i = ids if n else np.zeros(1, np.uint32)
+    _check(lib().oracle_build_pool(L, R, range_, P, seed, _p(a), _p(i), n, _p(arrivals), _p(off), _p(kept)),
+           "oracle_build_pool")
+    return PoolTables(L, R, range_, P, arrivals, off, kept[: int(off[-1])].copy())
+
+
+def query_pool(T: PoolTables, seed: int, q_addrs: np.ndarray, k: int, exclude=None):
+    """Querying phase over the shared pool (oracle_query_pool): top-k (ids, counts)."""
+    L = T.L
+    q = np.ascontiguousarray(q_addrs, dtype=np.uint32).reshape(-1, L)
+    nq = q.shape[0]
+    ids = np.empty((max(nq, 1), k), dtype=np.uint32)
+    cnt = np.empty((max(nq, 1), k), dtype=np.uint32)
+    ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.uint32)
+    kept = T.kept if T.kept.size else np.zeros(1, np.uint32)
+    _check(lib().oracle_query_pool(L, T.range, T.P, seed, _p(T.off), _p(kept),
+                                   _p(q if nq else np.full((1, L), EMPTY, np.uint32)), nq, k, _p(ex),
+                                   _p(ids), _p(cnt)), "oracle_query_pool")
+    return ids[:nq], cnt[:nq]
+
+
+def knn_graph_pool(K, L, R, range_, P, seed, row_ptr, col_idx, k):
+    """k-NN graph over a shared pool: insert ids 0..n-1, query every row excluding itself."""
+    rp, ci = _csr(row_ptr, col_idx)
+    n = rp.size - 1
+    a = addresses(K, L, range_, seed, doph(K, L, seed, rp, ci))
+    T = build_pool(L, R, range_, P, seed, a, np.arange(n, dtype=np.uint32))
+    return query_pool(T, seed, a, k, exclude=np.arange(n, dtype=np.uint32))
 
 
 def knn_graph(K, L, R, range_, seed, row_ptr, col_idx, k):

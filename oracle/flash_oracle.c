@@ -68,6 +68,7 @@ static uint32_t mulhi_range(uint32_t h, uint32_t n) {
 typedef struct {
     uint32_t a1, m1, a2, s_dens; /* DOPH's "4 random numbers" */
     uint32_t s_addr;             /* address-map key (R#5) */
+    uint32_t s_pool;             /* shared-reservoir map key (R#23) */
     uint64_t s_prio;             /* bottom-R priority key (R#9) */
 } oracle_seeds;
 
@@ -80,6 +81,7 @@ void oracle_derive_seeds(uint64_t seed, oracle_seeds *s) {
     s->a2 = (uint32_t)w[1];
     s->s_dens = (uint32_t)(w[1] >> 32);
     s->s_addr = (uint32_t)w[2];
+    s->s_pool = (uint32_t)(w[2] >> 32);
     s->s_prio = w[3];
 }
 
@@ -328,6 +330,143 @@ int oracle_query(uint32_t L, uint32_t range, const uint32_t *off, const uint32_t
         }
         free(A);
         free(kv);
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Reservoir sharing across tables (§3.2(4); §3.5, Fig. 3/4). */
+/* ------------------------------------------------------------------------- */
+
+/* The reservoir that table t's bucket b points to in a shared pool of P reservoirs
+ * ("one shared chunk of reservoirs ... the pointer points to a randomly selected shared
+ * reservoir"; "Allocated Range = F * Actual Range", so P = ceil(F*L*range)).
+ * P = L*range (F = 1) is the unshared index: reservoir t*range + b.  Otherwise a keyed
+ * hash of (t, b) reduced to [0, P) — a data-independent binding with the paper's law (a
+ * uniformly random reservoir), so the index does not depend on insertion order (R#23). */
+uint32_t oracle_reservoir(uint64_t seed, uint32_t t, uint32_t b, uint32_t L, uint32_t range, uint64_t P) {
+    if (P == (uint64_t)L * range) return t * range + b;
+    oracle_seeds s;
+    oracle_derive_seeds(seed, &s);
+    return mulhi_range(oracle_fmix32(oracle_fmix32(s.s_pool ^ t) ^ b), (uint32_t)P);
+}
+
+/* The distinct reservoirs of one row (addresses a[0..L)), in table order: a reservoir
+ * that several of the row's tables point to is listed once (R#23).  Returns the count. */
+static uint32_t row_reservoirs(uint64_t seed, const uint32_t *a, uint32_t L, uint32_t range, uint64_t P,
+                               uint32_t *res, int *bad) {
+    uint32_t n = 0;
+    for (uint32_t t = 0; t < L; ++t) {
+        if (a[t] == ORACLE_EMPTY) continue;
+        if (a[t] >= range) { *bad = 1; continue; }
+        uint32_t r = oracle_reservoir(seed, t, a[t], L, range, P);
+        int dup = 0;
+        for (uint32_t j = 0; j < n; ++j) dup |= res[j] == r;
+        if (!dup) res[n++] = r;
+    }
+    return n;
+}
+
+/* Adding phase over a shared pool of P reservoirs.  For every reservoir r:
+ *   S(r) = { id : r is one of the row's distinct reservoirs }   arrivals[r] = |S(r)|
+ *   kept(r) = the min(|S|, R) members with the smallest (prio(r div range, r mod range, id), id),
+ *             ascending id;  off[r] = sum over r' < r of |kept(r')|  (off has P+1 entries).
+ * kept_ids needs n_rows*L entries.  P = L*range gives exactly oracle_build's tables laid out
+ * table after table. */
+int oracle_build_pool(uint32_t L, uint32_t R, uint32_t range, uint64_t P, uint64_t seed,
+                      const uint32_t *addrs, const uint32_t *ids, uint64_t n_rows, uint32_t *arrivals,
+                      uint32_t *off, uint32_t *kept_ids) {
+    if (L == 0 || R == 0 || range == 0 || P == 0 || P > (uint64_t)L * range) return 1;
+    oracle_seeds s;
+    oracle_derive_seeds(seed, &s);
+    int bad = 0;
+    arrival *A = (arrival *)malloc(sizeof(arrival) * (n_rows * L + 1));
+    uint32_t *res = (uint32_t *)malloc(sizeof(uint32_t) * (L + 1));
+    uint64_t m = 0;
+    for (uint64_t r = 0; r < n_rows; ++r) {
+        uint32_t nr = row_reservoirs(seed, addrs + r * L, L, range, P, res, &bad);
+        for (uint32_t j = 0; j < nr; ++j) {
+            uint32_t v = res[j];
+            uint64_t tb = oracle_mix64(s.s_prio ^ (((uint64_t)(v / range) << 32) | (uint64_t)(v % range)));
+            A[m].b = v;
+            A[m].prio = (uint32_t)(oracle_mix64(tb ^ (uint64_t)ids[r]) >> 32);
+            A[m].id = ids[r];
+            m++;
+        }
+    }
+    qsort(A, m, sizeof(arrival), cmp_arrival); /* group by reservoir, then (prio, id) */
+    uint64_t i = 0, w = 0;
+    for (uint64_t v = 0; v < P; ++v) {
+        off[v] = (uint32_t)w;
+        uint64_t j = i;
+        while (j < m && A[j].b == v) j++;
+        arrivals[v] = (uint32_t)(j - i);
+        uint64_t keep = (j - i) < R ? (j - i) : R;
+        for (uint64_t q = 0; q < keep; ++q) kept_ids[w + q] = A[i + q].id;
+        qsort(kept_ids + w, keep, sizeof(uint32_t), cmp_u32); /* ascending id (R#10) */
+        w += keep;
+        i = j;
+    }
+    off[P] = (uint32_t)w;
+    free(A);
+    free(res);
+    return bad;
+}
+
+/* Querying phase over a shared pool: A = concatenation of kept(r) over the query's
+ * DISTINCT reservoirs in table order (a shared reservoir is aggregated once, R#23), then
+ * KSELECT exactly as oracle_query (full multiplicity, drop exclude, (count desc, id asc),
+ * pad (EMPTY, 0)). */
+int oracle_query_pool(uint32_t L, uint32_t range, uint64_t P, uint64_t seed, const uint32_t *off,
+                      const uint32_t *kept_ids, const uint32_t *q_addrs, uint64_t n_q, uint32_t k,
+                      const uint32_t *exclude, uint32_t *out_ids, uint32_t *out_counts) {
+    if (L == 0 || range == 0 || k == 0 || P == 0) return 1;
+    int bad = 0;
+#pragma omp parallel
+    {
+        uint64_t cap = 1024;
+        uint32_t *A = (uint32_t *)malloc(sizeof(uint32_t) * cap);
+        kvpair *kv = (kvpair *)malloc(sizeof(kvpair) * cap);
+        uint32_t *res = (uint32_t *)malloc(sizeof(uint32_t) * (L + 1));
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t q = 0; q < (int64_t)n_q; ++q) {
+            int lbad = 0;
+            uint32_t nr = row_reservoirs(seed, q_addrs + (uint64_t)q * L, L, range, P, res, &lbad);
+            if (lbad) bad = 1;
+            uint64_t m = 0;
+            for (uint32_t j = 0; j < nr; ++j) {
+                uint64_t len = off[res[j] + 1] - off[res[j]];
+                if (m + len > cap) {
+                    while (m + len > cap) cap *= 2;
+                    A = (uint32_t *)realloc(A, sizeof(uint32_t) * cap);
+                    kv = (kvpair *)realloc(kv, sizeof(kvpair) * cap);
+                }
+                memcpy(A + m, kept_ids + off[res[j]], sizeof(uint32_t) * len);
+                m += len;
+            }
+            qsort(A, m, sizeof(uint32_t), cmp_u32);
+            uint64_t nkv = 0;
+            for (uint64_t i = 0; i < m; ++i) {
+                if (i > 0 && A[i] == A[i - 1]) { kv[nkv - 1].count++; continue; }
+                kv[nkv].id = A[i];
+                kv[nkv].count = 1;
+                nkv++;
+            }
+            if (exclude) {
+                uint64_t w = 0;
+                for (uint64_t i = 0; i < nkv; ++i)
+                    if (kv[i].id != exclude[q]) kv[w++] = kv[i];
+                nkv = w;
+            }
+            qsort(kv, nkv, sizeof(kvpair), cmp_by_value);
+            for (uint32_t j = 0; j < k; ++j) {
+                out_ids[(uint64_t)q * k + j] = j < nkv ? kv[j].id : ORACLE_EMPTY;
+                out_counts[(uint64_t)q * k + j] = j < nkv ? kv[j].count : 0u;
+            }
+        }
+        free(A);
+        free(kv);
+        free(res);
     }
     return bad;
 }

@@ -509,3 +509,99 @@ def test_reservoirs_of_different_tables_sample_independently(orc):
         a, b = T.table(0)[1], T.table(1)[1]
         overlaps.append(np.intersect1d(a, b).size)
     assert abs(np.mean(overlaps) - R * R / m) < 1.0
+
+
+# --------------------------------------------------------------------------
+# Reservoir sharing across tables (§3.2(4); §3.5, Fig. 3/4; R#23)
+# --------------------------------------------------------------------------
+
+def test_pool_with_full_allocation_is_the_unshared_index(orc):
+    """F = 1 (P = L*range): every reservoir is one table's bucket, exactly the unshared
+    build and query (P:362 "Allocated Range = F * Actual Range")."""
+    rng = np.random.default_rng(40)
+    L, R, range_, seed = 5, 6, 32, 9
+    addrs, ids = _random_build_input(rng, 500, L, range_)
+    addrs[::5, 2] = EMPTY
+    T = orc.build(L, R, range_, seed, addrs, ids)
+    P = orc.build_pool(L, R, range_, L * range_, seed, addrs, ids)
+    assert P.arrivals.tolist() == T.arrivals.reshape(-1).tolist()
+    flat = np.concatenate([T.table(t)[1] for t in range(L)])
+    assert np.array_equal(P.kept, flat)
+    q = addrs[:60]
+    want = orc.query(T, q, 7, exclude=ids[:60])
+    got = orc.query_pool(P, seed, q, 7, exclude=ids[:60])
+    assert np.array_equal(want[0], got[0]) and np.array_equal(want[1], got[1])
+
+
+def test_pool_reservoirs_equal_bruteforce(orc):
+    """Brute force with Python sets: a reservoir holds the distinct rows pointing to it
+    through any of their tables (a row enters a shared reservoir once), keeps the
+    min(arrivals, R) with smallest (prio, id), ascending."""
+    rng = np.random.default_rng(41)
+    L, R, range_, seed = 4, 3, 16, 77
+    addrs, ids = _random_build_input(rng, 200, L, range_)
+    addrs[::9, 0] = EMPTY
+    P = orc.pool_size(0.25, L, range_)
+    T = orc.build_pool(L, R, range_, P, seed, addrs, ids)
+    members = [set() for _ in range(P)]
+    for row, i in zip(addrs, ids):
+        for t in range(L):
+            if row[t] != EMPTY:
+                members[orc.reservoir(seed, t, int(row[t]), L, range_, P)].add(int(i))
+    for r in range(P):
+        S = members[r]
+        assert T.arrivals[r] == len(S)
+        want = sorted(sorted(S, key=lambda i: (orc.prio(seed, r // range_, r % range_, i), i))[:R])
+        assert T.reservoir(r).tolist() == want
+    assert T.off[-1] == sum(min(len(S), R) for S in members)  # memory <= P reservoirs of R
+
+
+def test_pool_binding_is_uniform(orc):
+    """Each table bucket points to a uniformly random shared reservoir: chi-square
+    over the pool for every (t, b) cell, p > 0.001."""
+    from scipy.stats import chisquare
+
+    L, range_, seed = 8, 4096, 5
+    P = orc.pool_size(0.125, L, range_)
+    hits = np.zeros(P, np.int64)
+    for t in range(L):
+        for b in range(range_):
+            hits[orc.reservoir(seed, t, b, L, range_, P)] += 1
+    assert chisquare(hits).pvalue > 1e-3
+
+
+def test_pool_queries_return_only_inserted_ids_and_counts_le_L(orc):
+    """SPEC S:234 sharing correctness: every reported id was inserted into one of the
+    query's reservoirs, and its count (each distinct reservoir aggregated once) is at most
+    the number of those reservoirs <= L."""
+    rng = np.random.default_rng(42)
+    L, R, range_, seed, k = 6, 8, 16, 3, 12
+    addrs, ids = _random_build_input(rng, 400, L, range_)
+    P = orc.pool_size(0.1, L, range_)
+    T = orc.build_pool(L, R, range_, P, seed, addrs, ids)
+    got_ids, got_cnt = orc.query_pool(T, seed, addrs[:80], k)
+    for q in range(80):
+        res = {orc.reservoir(seed, t, int(addrs[q, t]), L, range_, P) for t in range(L)}
+        for i, c in zip(got_ids[q], got_cnt[q]):
+            if i == EMPTY:
+                continue
+            holders = [r for r in res if int(i) in set(T.reservoir(r).tolist())]
+            assert c == len(holders) and 1 <= c <= len(res) <= L
+
+
+def test_pool_quality_degrades_only_for_small_F(orc):
+    """Fig. 4: search quality is essentially unchanged down to F = 0.2 and
+    degrades for very small F.  R@10 of the exact cosine 1-NN on planted tiny data."""
+    rp, col = synth.generate(synth.SHAPES["tiny"].with_(N=3000, seed=21))
+    n = rp.size - 1
+    K, L, R, range_, seed, k = 4, 32, 16, 1 << 12, 77, 10
+    nn, _ = orc.bruteforce_topk(rp, col, np.arange(n), 1, metric="cosine")
+
+    def recall(F):
+        ids, cnt = orc.knn_graph_pool(K, L, R, range_, orc.pool_size(F, L, range_), seed, rp, col, k)
+        assert cnt.max() <= L
+        return np.mean([nn[q, 0] in set(ids[q].tolist()) for q in range(n)])
+
+    full = recall(1.0)
+    assert recall(0.2) >= full - 0.01
+    assert recall(0.002) < full - 0.3
