@@ -295,6 +295,208 @@ def data_quality_stats(h_rp, d_col, out_ids, n_q=1000, n_pairs=100_000, seed=13)
     return res
 
 
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_01190_b200 import dist as fdist
+    from paper_1709_01190_b200 import flash
+
+    rank, world, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # FLASH_BENCH_ONE_GPU=1 (debug only): every rank on cuda:0 over gloo, to exercise the
+    # multi-rank path on a 1-GPU box; its timings mean nothing.
+    one_gpu = os.environ.get("FLASH_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    if world > 1:
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = synth.SHAPES["webspam"]
+    t0 = time.time()
+    all_lens = np.empty(shape.N, dtype=np.int64)
+    import ctypes
+
+    synth._load().synth_row_lengths(ctypes.byref(synth._cparams(shape)), 0, shape.N, all_lens.ctypes.data)
+    bounds = fdist.shard_bounds(all_lens, world)
+    h_rp, h_col, nnz_local = gen_local(shape, bounds, rank)
+    nnz_total = int(all_lens.sum())
+    log(f"[rank {rank}] generated rows {bounds[rank]}..{bounds[rank + 1]} nnz={nnz_local} in {time.time() - t0:.1f}s")
+    n_local = bounds[rank + 1] - bounds[rank]
+    dev = torch.device("cuda", local)
+    # device-resident CSR (row_ptr rebased to this shard's col_idx)
+    d_rp = (h_rp.to(dev, non_blocking=True) - h_rp[0].item()).contiguous()
+    d_col = h_col.to(dev, non_blocking=True)
+    out_ids = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
+    idx = flash.FlashIndex(K, L, R, RANGE, SEED)
+    stream = torch.cuda.current_stream()
+    # N > 1: tables partitioned over the GPUs with the candidate all-to-all (north_star (d),
+    # default) or the sharded build + table all-gather
+    graph_fn = (fdist.knn_graph_candidate_exchange if args.mode == "exchange"
+                else fdist.knn_graph_sharded_build)
+
+    def step():
+        idx.clear()
+        if world == 1:
+            flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, TOPK, out_ids, out_cnt)
+            return out_ids, out_cnt
+        return graph_fn(idx, d_rp, d_col, TOPK, bounds, rank)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flash.flash_reset_counters(idx.h)
+    flash.flash_set_profiling(idx.h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    phase_ms, phase_calls = flash.flash_phase_ms(idx.h)
+    launches = flash.flash_launch_count(idx.h)
+    flash.flash_set_profiling(idx.h, False)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    ms_step = ms_max / args.steps
+
+    # end-to-end through the host-buffer C-ABI entry point (N=1) / host copies around the
+    # distributed graph (N>1)
+    e2e_ms = []
+    h_ids = torch.empty((n_local, TOPK), dtype=torch.int32).pin_memory()
+    h_cnt = torch.empty((n_local, TOPK), dtype=torch.int32).pin_memory()
+    h_rp_local = (h_rp - h_rp[0]).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    for i in range(e2e_steps + 1):
+        idx.clear()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        if world == 1:
+            flash.flash_knn_graph_host(idx.h, h_rp_local, h_col, n_local, TOPK, h_ids, h_cnt)
+        else:
+            d_rp2 = h_rp_local.to(dev, non_blocking=True)
+            d_col2 = h_col.to(dev, non_blocking=True)
+            ids_, cnt_ = graph_fn(idx, d_rp2, d_col2, TOPK, bounds, rank)
+            h_ids.copy_(ids_, non_blocking=True)
+            h_cnt.copy_(cnt_, non_blocking=True)
+            torch.cuda.synchronize()
+        dt = (time.perf_counter() - t) * 1e3
+        if i > 0:  # first is warm-up
+            e2e_ms.append(dt)
+    e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(e2e_local.item())
+
+    # work counts for the roofline (graph of the last step; rank-local)
+    idx.clear()
+    step()
+    torch.cuda.synchronize()
+    addrs_np = flash.as_u32(idx.hash_addrs(d_rp, d_col))
+    per_q, arrivals = query_work(lambda t: idx.table(t), addrs_np)  # this rank's queries
+    n_cand = int(per_q.sum())
+
+    result = None
+    if rank == 0:
+        hbm_peak, peak_kind = peaks()
+        per_step = {name: phase_ms[i] / max(phase_calls[i], 1) * (phase_calls[i] / args.steps)
+                    for i, name in enumerate(["hash", "build", "query", "copy"])}
+        # algorithmic bytes per launch
+        hash_bytes = 4 * nnz_local + 8 * (n_local + 1) + 4 * L * n_local
+        hash_ms = per_step["hash"]
+        query_ms = per_step["query"]
+        build_ms = per_step["build"]
+        dominant = max(("hash", hash_ms), ("build", build_ms), ("query", query_ms), key=lambda x: x[1])[0]
+        traffic = {}  # ncu --set full DRAM bytes of one graph, summed per kernel name
+        try:
+            with open(TRAFFIC_PATH) as f:
+                for d in json.load(f):
+                    nm = d["kernel"].split("::")[-1].split("<")[0]
+                    if d.get("dram_traffic_bytes") is not None:
+                        traffic[nm] = traffic.get(nm, 0.0) + d["dram_traffic_bytes"]
+        except Exception:
+            pass
+        q_traffic = None
+        if "k_query_sort" in traffic:
+            q_traffic = sum(traffic.get(nm, 0.0) for nm in ("k_query_plan", "k_query_sort", "k_query"))
+        if dominant == "query" and n_cand is not None:
+            # the count kernel is bound by per-candidate shared-memory work, not by HBM
+            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query for M > 3072)",
+                    "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
+                    "peak": SMEM_RMW_PEAK, "unit": "candidate-updates/s", "peak_kind": "measured (smem RMW microbench)",
+                    "traffic": q_traffic, "candidates": n_cand,
+                    "hbm_view": {"algorithmic_bytes": 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local,
+                                 "achieved_GBps": (4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local)
+                                 / (query_ms * 1e-3) / 1e9}}
+        elif dominant == "build":
+            bbytes = 8 * L * n_local * 2 + 12 * L * n_local
+            roof = {"kernel": "build (k_count..k_select_big)", "bound": "hbm",
+                    "achieved": bbytes / (build_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": bbytes}
+        else:
+            roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
+                    "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
+        hash_roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
+                     "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        value = shape.N / (ms_step * 1e-3)
+        h2d = 8 * (n_local + 1) + 4 * nnz_local
+        d2h = 8 * n_local * TOPK
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "graph_time_s": ms_step * 1e-3,
+            "hash_nnz_per_s": nnz_local / (hash_ms * 1e-3) * world if hash_ms else None,
+            "queries_per_s": shape.N / (ms_step * 1e-3),
+            "phase_ms_per_step": per_step,
+            "hash_roofline": hash_roof,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (synth/, webspam shape, seed 2)",
+            "config": workload_config(shape, nnz_total, args),
+            "roofline": roof,
+            "e2e": {"value": shape.N / (e2e_ms_max * 1e-3), "unit": "queries/s",
+                    "ms_per_step": e2e_ms_max, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "flash_knn_graph_host (pinned host buffers)" if world == 1 else
+                           f"host copies + dist {args.mode} graph"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        result["candidates_per_query"] = {"mean": n_cand / n_local, "p99": float(np.percentile(per_q, 99)),
+                                          "max": int(per_q.max())}
+        result["bucket_arrivals"] = arrivals
+        if world == 1 and not args.no_quality:
+            t0 = time.time()
+            result["data_stats"] = data_quality_stats(h_rp, d_col, out_ids, n_q=args.quality_queries)
+            log(f"data/quality stats in {time.time() - t0:.1f}s")
+    idx.close()
+    return result
+
+
 # Secondary workloads (BASELINE.json configs[2], configs[3]): index every row, then answer
 # 10K sampled rows as queries with self-exclusion.  Index parameters from the
 # paper's own runs: url K=4, L=128, R=32, 2^15; kdd12 K=4,

@@ -63,6 +63,18 @@ typedef enum {
 flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed,
                           flash_index **out);
 
+/* flash_create with reservoir sharing across tables (§3.2(4); §3.5 P:352-362;
+ * R#23): the L*range table buckets point into one pool of `pool` reservoirs
+ * (pool = ceil(F*L*range) for the paper's fraction F).  Bucket (t, b) is bound to
+ * reservoir mulhi(fmix32(fmix32(s_pool ^ t) ^ b), pool) (data-independent, so the index is
+ * order-free); a row enters each of its distinct reservoirs once and a query aggregates each
+ * distinct reservoir once (counts <= L).  pool = 0 or L*range: the unshared index (exactly
+ * flash_create).  1 <= pool <= L*range, else FLASH_EINVAL.  With sharing, flash_get_table
+ * and the table-window calls (multi-GPU) return FLASH_ESTATE / FLASH_EINVAL;
+ * flash_table_arrays reports the pool ([pool+1] offsets, [pool] arrivals). */
+flash_status flash_create_pool(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t pool, uint64_t seed,
+                               flash_index **out);
+
 /* Free the tables and the handle (synchronizes the device first).  NULL is a no-op. */
 void flash_destroy(flash_index *h);
 

@@ -105,16 +105,17 @@ __device__ void block_bitonic(T* a, uint32_t n) {
 
 // B1: per-bucket arrival histogram of the new rows (warp per row, lanes over tables).
 __global__ void k_count(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t acol0,
-                        uint32_t range, uint32_t t0, uint32_t t1, uint32_t* __restrict__ cnt,
+                        uint32_t range, uint32_t t0, uint32_t t1, uint32_t shared, uint32_t* __restrict__ cnt,
                         unsigned long long* err) {
+  const uint32_t lim = shared ? shared : range;  // shared: addrs are reservoir indices
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
     for (uint32_t t = t0 + lane; t < t1; t += 32) {
       const uint32_t a = addrs[r * L + t - acol0];
       if (a == kEmpty) continue;
-      if (a >= range) { atomicAdd(err, 1ull); continue; }
-      atomicAdd(&cnt[t * range + a], 1u);
+      if (a >= lim) { atomicAdd(err, 1ull); continue; }
+      atomicAdd(&cnt[shared ? a : t * range + a], 1u);
     }
   }
 }
@@ -223,7 +224,7 @@ __global__ void k_fill_old(uint32_t nb, const uint64_t* __restrict__ goff_old,
 }
 
 __global__ void k_fill_new(const uint32_t* __restrict__ addrs, uint64_t n, uint32_t L, uint32_t acol0,
-                           uint32_t range, uint32_t t0, uint32_t t1, uint32_t id_base,
+                           uint32_t range, uint32_t t0, uint32_t t1, uint32_t shared, uint32_t id_base,
                            uint32_t* __restrict__ cursor,
                            const uint64_t* __restrict__ pool_off, uint32_t* __restrict__ pool) {
   const uint32_t lane = threadIdx.x & 31;
@@ -231,11 +232,40 @@ __global__ void k_fill_new(const uint32_t* __restrict__ addrs, uint64_t n, uint3
   for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
     for (uint32_t t = t0 + lane; t < t1; t += 32) {
       const uint32_t a = addrs[r * L + t - acol0];
-      if (a >= range) continue;  // EMPTY or invalid (counted by k_count)
-      const uint32_t i = t * range + a;
+      if (a >= (shared ? shared : range)) continue;  // EMPTY or invalid (counted by k_count)
+      const uint32_t i = shared ? a : t * range + a;
       const uint32_t pos = atomicAdd(&cursor[i], 1u);
       pool[pool_off[i] + pos] = id_base + (uint32_t)r;
     }
+  }
+}
+
+// Reservoir sharing pre-pass (R#23): warp per row, the row's L reservoir indices staged
+// in shared memory so each entry can drop itself when an earlier table of the row points
+// to the same reservoir.
+__global__ void __launch_bounds__(256) k_shared_reservoirs(const uint32_t* __restrict__ addrs, uint64_t n,
+                                                           uint32_t L, uint32_t range, uint32_t P, HashKeys keys,
+                                                           uint32_t* __restrict__ out, unsigned long long* err) {
+  extern __shared__ uint32_t rbuf_all[];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* rbuf = rbuf_all + (size_t)w * L;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + w; r < n; r += nw) {
+    for (uint32_t t = lane; t < L; t += 32) {
+      const uint32_t a = addrs[r * L + t];
+      uint32_t v = kEmpty;
+      if (a < range) v = shared_reservoir(keys, t, a, P);
+      else if (a != kEmpty) atomicAdd(err, 1ull);
+      rbuf[t] = v;
+    }
+    __syncwarp();
+    for (uint32_t t = lane; t < L; t += 32) {
+      const uint32_t v = rbuf[t];
+      bool dup = false;
+      for (uint32_t j = 0; j < t && !dup; ++j) dup = rbuf[j] == v;
+      out[r * L + t] = (v == kEmpty || dup) ? kEmpty : v;
+    }
+    __syncwarp();
   }
 }
 
@@ -643,15 +673,30 @@ size_t build_scan_tmp_bytes(uint64_t nb) {
   return bytes;
 }
 
+int launch_shared_reservoirs(const uint32_t* addrs, uint64_t n, uint32_t L, uint32_t range, uint32_t P,
+                             const HashKeys& keys, uint32_t* out, unsigned long long* err, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = (size_t)8 * L * sizeof(uint32_t);
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_shared_reservoirs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const uint64_t want = (n + 7) / 8;
+  const unsigned blocks = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
+  k_shared_reservoirs<<<blocks, 256, smem, s>>>(addrs, n, L, range, P, keys, out, err);
+  return 1;
+}
+
 int launch_build(const BuildArgs& a, cudaStream_t s) {
-  const uint32_t nb = a.L * a.range;
+  const uint32_t nb = a.shared ? a.shared : a.L * a.range;
   int launches = 0;
   const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < 148ull * 32 ? (a.n + 7) / 8 : 148ull * 32);
   const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
   cudaMemsetAsync(a.big_count, 0, 3 * sizeof(uint32_t), s);  // big, mid, register-path list counters
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
-  const bool tm = a.addrsT != nullptr && a.n && W;  // table-major passes (see k_count_tm)
+  const bool tm = a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (see k_count_tm)
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
   if (tm) {
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
@@ -660,7 +705,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                                        a.err);
     launches += 2;
   } else if (a.n) {
-    k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.cursor, a.err);
+    k_count<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.shared, a.cursor,
+                                        a.err);
     launches++;
   }
   k_pool_sizes<<<nb_blocks, 256, 0, s>>>(nb, a.R, a.goff_old, a.cursor, a.arrivals, a.pool_cnt, a.keep_cnt);
@@ -680,8 +726,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                                       a.cursor, a.pool_off, a.pool);
     launches++;
   } else if (a.n) {
-    k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.id_base,
-                                           a.cursor, a.pool_off, a.pool);
+    k_fill_new<<<rows_blocks, 256, 0, s>>>(a.addrs, a.n, a.astride, a.acol0, a.range, a.t0, a.t1, a.shared,
+                                           a.id_base, a.cursor, a.pool_off, a.pool);
     launches++;
   }
   static bool attr = false;

@@ -88,6 +88,7 @@ void release(DevBuf& b) {
 
 struct flash_index {
   uint32_t K, L, R, range;
+  uint32_t shared = 0;  // reservoir sharing (R#23): pool size P < L*range, or 0 (unshared)
   uint64_t seed;
   HashKeys keys;
   int device;
@@ -105,6 +106,7 @@ struct flash_index {
   DevBuf seg_off, xscan_tmp;  // flash_count_topk segment offsets; exchange scans
   DevBuf addrsT;              // build: window addresses transposed to [W][n] (table-major passes)
   DevBuf qhuge;               // query: global count tables of the L*R > 8192 class (kept clean)
+  DevBuf raddr, qraddr;       // shared mode: rows' / queries' distinct reservoir indices
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -179,6 +181,9 @@ __global__ void k_table_off(const uint64_t* goff, uint32_t t, uint32_t range, ui
     off[b] = (uint32_t)(goff[(uint64_t)t * range + b] - base);
 }
 
+// buckets (reservoirs) the index holds: L*range, or the shared pool's P (R#23)
+uint64_t nbuckets(const flash_index* h) { return h->shared ? h->shared : (uint64_t)h->L * h->range; }
+
 flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n,
                      uint32_t* codes, uint32_t* addrs, cudaStream_t s, uint32_t world = 1) {
   Phase ph(h, 0, s);
@@ -189,9 +194,18 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
 }
 
 flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
-                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX, bool cols = false) {
+                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX, bool cols = false,
+                             bool converted = false) {
   if (t1 > h->L) t1 = h->L;
-  const uint64_t nb = (uint64_t)h->L * h->range;
+  const uint64_t nb = nbuckets(h);
+  if (h->shared && !converted) {  // table addresses -> each row's distinct shared reservoirs
+    TRY(ensure(h->raddr, sizeof(uint32_t) * n * h->L));
+    Phase ph(h, 1, s);
+    h->launches += launch_shared_reservoirs(addrs, n, h->L, h->range, h->shared, h->keys,
+                                            h->raddr.as<uint32_t>(), h->err, s);
+    CUDA_TRY(cudaGetLastError());
+    addrs = h->raddr.as<uint32_t>();
+  }
   const uint64_t pool_cap = h->kept_ub + n * h->L;
   const uint64_t kept_cap = pool_cap < nb * h->R ? pool_cap : nb * h->R;
   const int nxt = h->have_tables ? 1 - h->cur : h->cur;
@@ -211,7 +225,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   // kdd12, 2^20 buckets/table, 3.6x faster; url, 2^15, 2.6x slower); FLASH_BUILD_TM=0/1
   // forces the choice (tests).
   const char* tm_env = getenv("FLASH_BUILD_TM");
-  const bool tm = tm_env ? tm_env[0] == '1' : (nb * 12 > (32ull << 20) && h->range >= (1u << 18));
+  const bool tm = !h->shared &&
+                  (tm_env ? tm_env[0] == '1' : (nb * 12 > (32ull << 20) && h->range >= (1u << 18)));
   if (tm && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
 
   Phase ph(h, 1, s);
@@ -221,6 +236,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.astride = cols ? t1 - t0 : h->L;  // cols: addrs holds only the window's columns
   a.acol0 = cols ? t0 : 0;
   a.addrsT = (tm && t1 > t0) ? h->addrsT.as<uint32_t>() : nullptr;
+  a.shared = h->shared;
   a.n = n;
   a.id_base = id_base;
   a.L = h->L;
@@ -266,8 +282,16 @@ flash_status ensure_huge_table(flash_index* h, cudaStream_t s) {
 
 flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64_t nq, uint32_t k,
                             const uint32_t* exclude, int exclude_self, uint32_t self_base,
-                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s) {
+                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s, bool converted = false) {
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->shared && !converted && h->have_tables) {  // each distinct reservoir aggregated once
+    TRY(ensure(h->qraddr, sizeof(uint32_t) * nq * h->L));
+    Phase ph(h, 2, s);
+    h->launches += launch_shared_reservoirs(addrs, nq, h->L, h->range, h->shared, h->keys,
+                                            h->qraddr.as<uint32_t>(), h->err, s);
+    CUDA_TRY(cudaGetLastError());
+    addrs = h->qraddr.as<uint32_t>();
+  }
   if (!h->have_tables) {  // nothing inserted: every query returns k pads
     Phase ph(h, 2, s);
     CUDA_TRY(cudaMemsetAsync(out_ids, 0xFF, sizeof(uint32_t) * nq * k, s));
@@ -287,6 +311,7 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   a.k = k;
   a.cmax = h->L;
   a.direct = 0;
+  a.shared = h->shared;
   a.exclude = exclude;
   a.exclude_self = exclude_self;
   a.self_base = self_base;
@@ -320,6 +345,11 @@ const char* flash_last_error(void) { return g_last_error.c_str(); }
 
 flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed,
                           flash_index** out) {
+  return flash_create_pool(K, L, R, range, 0, seed, out);
+}
+
+flash_status flash_create_pool(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t pool, uint64_t seed,
+                               flash_index** out) {
   if (!out) return fail(FLASH_EINVAL, "out is NULL");
   *out = nullptr;
   if (K < 1 || L < 1 || (uint64_t)K * L > FLASH_MAX_BINS)
@@ -327,6 +357,10 @@ flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, ui
   if (R < 1 || R > FLASH_MAX_R) return fail(FLASH_EINVAL, "R=%u outside [1, %u]", R, FLASH_MAX_R);
   if (range < 1 || range > (1u << 31)) return fail(FLASH_EINVAL, "range=%u outside [1, 2^31]", range);
   if ((uint64_t)L * range > (1ull << 31)) return fail(FLASH_EINVAL, "L*range must be <= 2^31");
+  if (pool > (uint64_t)L * range)
+    return fail(FLASH_EINVAL, "pool=%llu exceeds L*range=%llu", (unsigned long long)pool,
+                (unsigned long long)L * range);
+  const uint32_t shared = (pool == 0 || pool == (uint64_t)L * range) ? 0u : (uint32_t)pool;
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   flash_index* h = new (std::nothrow) flash_index();
@@ -339,8 +373,10 @@ flash_status flash_create(uint32_t K, uint32_t L, uint32_t R, uint32_t range, ui
   h->keys = derive_keys(seed);
   h->device = dev;
   h->table_log2 = query_table_log2(L, R);
-  cudaError_t e = cudaMalloc(&h->arrivals, sizeof(uint32_t) * (size_t)L * range);
-  if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * (size_t)L * range);
+  h->shared = shared;
+  const size_t nb = shared ? shared : (size_t)L * range;
+  cudaError_t e = cudaMalloc(&h->arrivals, sizeof(uint32_t) * nb);
+  if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * nb);
   if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
@@ -369,7 +405,7 @@ void flash_destroy(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge, &h->raddr, &h->qraddr,
                     &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
@@ -405,6 +441,7 @@ flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t 
 flash_status flash_insert_addrs_window(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
                                        uint32_t t_begin, uint32_t t_end, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L) return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
   if (n_rows == 0) return FLASH_OK;
   REQUIRE_DEV(addrs);
@@ -424,7 +461,7 @@ flash_status flash_table_arrays(const flash_index* hc, const uint64_t** goff, co
   if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
   const uint64_t* g = h->goff[h->cur].as<uint64_t>();
   uint64_t total = 0;
-  CUDA_TRY(cudaMemcpy(&total, g + (uint64_t)h->L * h->range, sizeof total, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&total, g + nbuckets(h), sizeof total, cudaMemcpyDeviceToHost));
   if (goff) *goff = g;
   if (ids) *ids = h->ids[h->cur].as<uint32_t>();
   if (arrivals) *arrivals = h->arrivals;
@@ -440,7 +477,7 @@ flash_status flash_import_tables(flash_index* h, const uint64_t* goff, const uin
   if (arrivals) REQUIRE_DEV(arrivals);
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
-  const uint64_t nb = (uint64_t)h->L * h->range;
+  const uint64_t nb = nbuckets(h);
   const int nxt = h->have_tables ? 1 - h->cur : h->cur;
   TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * (n_ids ? n_ids : 1)));
@@ -525,6 +562,8 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
   uint32_t* addrs = h->addrs.as<uint32_t>();
   TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
   TRY(do_insert_addrs(h, addrs, n_rows, 0, s));
+  if (h->shared)  // the rows' distinct reservoirs are the queries' too
+    return do_query_addrs(h, h->raddr.as<uint32_t>(), n_rows, k, nullptr, 1, 0, out_ids, out_counts, s, true);
   return do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s);
 }
 
@@ -598,7 +637,10 @@ flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const 
     r0 = r1;
   }
   TRY(do_insert_addrs(h, d_addrs, n_rows, 0, s));
-  TRY(do_query_addrs(h, d_addrs, n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s));
+  if (h->shared)
+    TRY(do_query_addrs(h, h->raddr.as<uint32_t>(), n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s, true));
+  else
+    TRY(do_query_addrs(h, d_addrs, n_rows, k, nullptr, 1, 0, d_ids, d_cnt, s));
   {
     Phase ph(h, 3, s);
     CUDA_TRY(cudaMemcpyAsync(out_ids, d_ids, sizeof(uint32_t) * n_rows * k, cudaMemcpyDeviceToHost, s));
@@ -624,6 +666,7 @@ flash_status flash_hash_blocked(const flash_index* h, const int64_t* row_ptr, co
 flash_status flash_insert_addrs_cols(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
                                      uint32_t t_begin, uint32_t t_end, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin >= t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) must be non-empty and inside [0, %u)", t_begin, t_end, h->L);
   if (n_rows == 0) return FLASH_OK;
@@ -639,6 +682,7 @@ flash_status flash_window_sizes(const flash_index* hc, const uint32_t* addrs, ui
                                 uint32_t t_end, uint32_t* sizes, uint64_t* offsets, void* stream) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
   REQUIRE_DEV(offsets);
@@ -665,6 +709,7 @@ flash_status flash_window_gather(const flash_index* hc, const uint32_t* addrs, u
                                  uint32_t t_end, const uint64_t* offsets, uint32_t* out_ids, void* stream) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
   if (n_q == 0 || t_end == t_begin || !h->have_tables) return FLASH_OK;
@@ -732,7 +777,7 @@ flash_status flash_clear(flash_index* h, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
-  CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * (size_t)h->L * h->range, s));
+  CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * nbuckets(h), s));
   h->have_tables = false;
   h->kept_ub = 0;
   h->n_inserted = 0;
@@ -745,6 +790,7 @@ flash_status flash_get_table(const flash_index* hc, uint32_t t, const uint32_t**
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
   if (t >= h->L) return fail(FLASH_EINVAL, "table %u >= L=%u", t, h->L);
+  if (h->shared) return fail(FLASH_ESTATE, "tables share reservoirs: use flash_table_arrays");
   if (!h->have_tables) return fail(FLASH_ESTATE, "nothing inserted yet");
   CUDA_TRY(cudaSetDevice(h->device));
   if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));

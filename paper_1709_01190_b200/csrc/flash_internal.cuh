@@ -19,6 +19,7 @@ constexpr uint32_t kProbes = 64;          // densification chain cap T (R#4)
 struct HashKeys {
   uint32_t a1, m1, a2, s_dens;  // DOPH's "4 random numbers"
   uint32_t s_addr;              // K-tuple -> address key (R#5)
+  uint32_t s_pool;              // shared-reservoir binding key (R#23)
   uint64_t s_prio;              // bottom-R priority key (R#9)
 };
 
@@ -46,6 +47,7 @@ inline HashKeys derive_keys(uint64_t seed) {
   s.a2 = (uint32_t)w[1];
   s.s_dens = (uint32_t)(w[1] >> 32);
   s.s_addr = (uint32_t)w[2];
+  s.s_pool = (uint32_t)(w[2] >> 32);
   s.s_prio = w[3];
   return s;
 }
@@ -53,6 +55,12 @@ inline HashKeys derive_keys(uint64_t seed) {
 // pi(c): keyed bijection on uint32 standing in for the random permutation of Eq. 1.
 __device__ __forceinline__ uint32_t perm(const HashKeys& k, uint32_t c) {
   return fmix32(((c ^ k.a1) * k.m1) + k.a2);
+}
+
+// Reservoir sharing (R#23): table t's bucket b points to shared reservoir
+// mulhi(fmix32(fmix32(s_pool ^ t) ^ b), P) of a pool of P reservoirs.
+__device__ __forceinline__ uint32_t shared_reservoir(const HashKeys& k, uint32_t t, uint32_t b, uint32_t P) {
+  return __umulhi(fmix32(fmix32(k.s_pool ^ t) ^ b), P);
 }
 
 // prio(t, b, id) = hi32(mix64(tb ^ id)) with tb = mix64(s_prio ^ (t<<32 | b)).
@@ -75,11 +83,20 @@ int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
                 uint32_t world, cudaStream_t s);
 
+// Reservoir sharing (R#23): addrs [n][L] -> reservoir indices [n][L]: entry (r, t) is
+// shared_reservoir(t, addrs[r][t]) unless the address is EMPTY/invalid or an earlier table of
+// the same row points to the same reservoir (then EMPTY: a row enters / a query aggregates
+// each distinct reservoir once).
+int launch_shared_reservoirs(const uint32_t* addrs, uint64_t n, uint32_t L, uint32_t range, uint32_t P,
+                             const HashKeys& keys, uint32_t* out, unsigned long long* err, cudaStream_t s);
+
 // Build scratch / state.  All bucket-indexed arrays have nb = L*range entries (+1).
 struct BuildArgs {
   const uint32_t* addrs;  // row r, table t at addrs[r*astride + t - acol0]
   uint32_t astride, acol0;  // [n][L]: L, 0; a column window [n][t1-t0]: t1-t0, t0
   uint32_t* addrsT;         // scratch [t1-t0][n] for the table-major passes, or null (row-major)
+  uint32_t shared;          // 0: bucket (t, a) is t*range + a; else addrs hold shared-reservoir
+                            // indices < shared (k_shared_reservoirs output) used as the bucket
   uint64_t n;
   uint32_t id_base;
   uint32_t L, R, range;
@@ -117,6 +134,7 @@ struct QueryArgs {
   uint32_t L, range, k;
   uint32_t cmax;          // largest possible count (= the index's L)
   int direct;
+  uint32_t shared;        // 0, or: addrs hold shared-reservoir indices (bucket = the index itself)
   const uint32_t* exclude;  // [nq] or null
   int exclude_self;         // exclude id = self_base + q
   uint32_t self_base;

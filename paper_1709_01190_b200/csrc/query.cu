@@ -53,7 +53,7 @@ constexpr uint32_t kHugeLog2 = 16;
 constexpr uint32_t kHugeCtas = 148;
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
-                             uint32_t L, uint32_t range, int direct, uint64_t mmax, uint32_t k,
+                             uint32_t L, uint32_t range, int direct, uint32_t shared, uint64_t mmax, uint32_t k,
                              uint32_t* __restrict__ out_ids, uint32_t* __restrict__ out_counts,
                              uint32_t* __restrict__ lists, uint32_t* __restrict__ counts, unsigned long long* err) {
   const uint32_t lane = threadIdx.x & 31;
@@ -64,8 +64,8 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
     if (q < nq) {
       for (uint32_t t = 0; t < L; ++t) {
         const uint32_t a = direct ? (uint32_t)q : addrs[q * L + t];
-        if (a < range) {
-          const uint64_t i = (uint64_t)t * range + a;
+        if (a < (shared ? shared : range)) {
+          const uint64_t i = shared ? (uint64_t)a : (uint64_t)t * range + a;
           M += goff[i + 1] - goff[i];
         } else if (a != kEmpty) {
           atomicAdd(err, 1ull);
@@ -213,8 +213,8 @@ __global__ void __launch_bounds__(NT) k_query(QueryArgs a, const uint32_t* __res
         uint64_t st = 0;
         if (t < L) {
           const uint32_t ad = a.direct ? (uint32_t)q : a.addrs[q * L + t];
-          if (ad < a.range) {
-            const uint64_t i = (uint64_t)t * a.range + ad;
+          if (ad < (a.shared ? a.shared : a.range)) {
+            const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)t * a.range + ad;
             st = a.goff[i];
             sz = (uint32_t)(a.goff[i + 1] - st);
           }
@@ -570,7 +570,7 @@ int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream
   uint64_t blocks = (warps + 7) / 8;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
-  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, a.direct, max_m, a.k,
+  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, a.direct, a.shared, max_m, a.k,
                                                  a.out_ids, a.out_counts, lists, counts, a.err);
   const uint32_t hist_len = (a.cmax + 1) > 1024 ? a.cmax + 1 : 1024;
   // The class kernels are persistent over their device-side query lists and run back to

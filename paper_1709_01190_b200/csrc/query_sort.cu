@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
       uint64_t st = 0;
       if (t < L) {
         const uint32_t ad = a.direct ? (uint32_t)q : a.addrs[q * L + t];
-        if (ad < a.range) {
-          const uint64_t i = (uint64_t)t * a.range + ad;
+        if (ad < (a.shared ? a.shared : a.range)) {
+          const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)t * a.range + ad;
           st = a.goff[i];
           sz = (uint32_t)(a.goff[i + 1] - st);
         }

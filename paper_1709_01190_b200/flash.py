@@ -34,7 +34,7 @@ EXPORTS = (
     "flash_table_arrays", "flash_import_tables", "flash_set_profiling", "flash_phase_ms",
     "flash_launch_count", "flash_reset_counters", "flash_last_error",
     "flash_hash_blocked", "flash_insert_addrs_cols", "flash_window_sizes", "flash_window_gather",
-    "flash_count_topk",
+    "flash_count_topk", "flash_create_pool",
 )
 
 
@@ -57,6 +57,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L = ctypes.CDLL(path)
     vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
     L.flash_create.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(vp)]
+    L.flash_create_pool.argtypes = [u32, u32, u32, u32, u64, u64, ctypes.POINTER(vp)]
     L.flash_destroy.argtypes = [vp]
     L.flash_destroy.restype = None
     L.flash_hash.argtypes = [vp, vp, vp, u64, vp, vp, vp]
@@ -148,6 +149,19 @@ def flash_create(K: int, L: int, R: int, range_: int, seed: int) -> int:
     h = ctypes.c_void_p()
     _check(load_library().flash_create(K, L, R, range_, seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(h)))
     return h.value
+
+
+def flash_create_pool(K: int, L: int, R: int, range_: int, pool: int, seed: int) -> int:
+    torch.cuda.current_device()
+    h = ctypes.c_void_p()
+    _check(load_library().flash_create_pool(K, L, R, range_, pool, seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(h)))
+    return h.value
+
+
+def pool_size(F: float, L: int, range_: int) -> int:
+    """P = ceil(F * L * range) shared reservoirs ("Allocated Range = F * Actual Range")."""
+    import math
+    return max(1, min(L * range_, int(math.ceil(F * L * range_))))
 
 
 def flash_destroy(h: int) -> None:
@@ -295,10 +309,12 @@ def _copy_device(ptr: int, n: int, device, typestr: str = "<i4") -> torch.Tensor
 class FlashIndex:
     """Owns one flash_index handle (device = the current CUDA device)."""
 
-    def __init__(self, K: int, L: int, R: int, range_: int, seed: int):
+    def __init__(self, K: int, L: int, R: int, range_: int, seed: int, F: float = 1.0):
+        """F < 1: reservoir sharing over a pool of ceil(F*L*range) reservoirs (R#23)."""
         self.K, self.L, self.R, self.range, self.seed = K, L, R, range_, seed
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.h = flash_create(K, L, R, range_, seed)
+        self.pool = pool_size(F, L, range_) if F < 1.0 else L * range_
+        self.h = flash_create_pool(K, L, R, range_, self.pool, seed) if F < 1.0 else flash_create(K, L, R, range_, seed)
 
     def close(self):
         if getattr(self, "h", None):
@@ -372,7 +388,7 @@ class FlashIndex:
         """Copies of (goff int64 [L*range+1], ids int32 [n] (None unless ids), arrivals int32
         [L*range])."""
         g, i, a, n = flash_table_arrays(self.h)
-        nb = self.L * self.range
+        nb = self.pool
         return (_copy_device(g, nb + 1, self.device, "<i8"), _copy_device(i, n, self.device) if ids else None,
                 _copy_device(a, nb, self.device))
 

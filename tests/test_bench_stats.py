@@ -45,3 +45,10 @@ def test_quality_stats_match_brute_force():
         assert abs(res["quality"]["R@k"][str(kk)] - r_at[kk] / 60) < 1e-12
         assert abs(res["quality"]["S@k"][str(kk)] - s_at[kk] / 60) < 1e-9
     assert res["quality"]["R@k"]["1"] > 0.2  # the planted neighbours are found
+
+
+def test_bench_entry_points_exist():
+    """bench.py's driver contract: every arm main() dispatches to is defined."""
+    for fn in ("run_ours", "run_shape", "run_reference", "cpu_baseline", "main", "data_quality_stats",
+               "exact_cosine", "recall_at_k", "shape_stats"):
+        assert callable(getattr(bench, fn)), fn
