@@ -309,12 +309,14 @@ def _copy_device(ptr: int, n: int, device, typestr: str = "<i4") -> torch.Tensor
 class FlashIndex:
     """Owns one flash_index handle (device = the current CUDA device)."""
 
-    def __init__(self, K: int, L: int, R: int, range_: int, seed: int, F: float = 1.0):
-        """F < 1: reservoir sharing over a pool of ceil(F*L*range) reservoirs (R#23)."""
+    def __init__(self, K: int, L: int, R: int, range_: int, seed: int, F: float = 1.0, pool: int | None = None):
+        """F < 1 (or an explicit pool < L*range): reservoir sharing over a pool of
+        ceil(F*L*range) reservoirs (R#23)."""
         self.K, self.L, self.R, self.range, self.seed = K, L, R, range_, seed
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.pool = pool_size(F, L, range_) if F < 1.0 else L * range_
-        self.h = flash_create_pool(K, L, R, range_, self.pool, seed) if F < 1.0 else flash_create(K, L, R, range_, seed)
+        self.pool = int(pool) if pool is not None else (pool_size(F, L, range_) if F < 1.0 else L * range_)
+        self.h = (flash_create_pool(K, L, R, range_, self.pool, seed) if self.pool < L * range_
+                  else flash_create(K, L, R, range_, seed))
 
     def close(self):
         if getattr(self, "h", None):
@@ -397,6 +399,32 @@ class FlashIndex:
 
     def errors(self) -> int:
         return flash_check(self.h)
+
+    # ---- serialization ----
+    FORMAT = "flash-b200-index-v1"
+
+    def save(self, path: str, max_id: int):
+        """Write the index (config + bucket offsets + kept ids + arrivals) to an .npz file.
+        max_id: the largest id inserted (the query kernels' digit range)."""
+        goff, ids, arr = self.table_arrays()
+        np.savez(path, format=self.FORMAT, K=self.K, L=self.L, R=self.R, range=self.range, seed=self.seed,
+                 pool=self.pool, max_id=max_id, goff=goff.cpu().numpy(), ids=as_u32(ids), arrivals=as_u32(arr))
+
+    @classmethod
+    def load(cls, path: str) -> "FlashIndex":
+        """Rebuild an index from save(): load(save(x)) answers queries and takes further
+        inserts exactly like x (bottom-R is composable)."""
+        z = np.load(path)
+        if str(z["format"]) != cls.FORMAT:
+            raise ValueError(f"{path}: not a {cls.FORMAT} file")
+        K, L, R, rng, seed, pool = (int(z[k]) for k in ("K", "L", "R", "range", "seed", "pool"))
+        idx = cls(K, L, R, rng, seed, pool=pool)
+        dev = idx.device
+        goff = torch.from_numpy(z["goff"].astype(np.int64)).to(dev)
+        ids = torch.from_numpy(np.ascontiguousarray(z["ids"]).view(np.int32)).to(dev)
+        arr = torch.from_numpy(np.ascontiguousarray(z["arrivals"]).view(np.int32)).to(dev)
+        idx.import_tables(goff, ids, arr, int(z["max_id"]))
+        return idx
 
     # ---- candidate exchange (dist.knn_graph_candidate_exchange) ----
     def hash_addrs_blocked(self, row_ptr, col_idx, world: int):

@@ -109,3 +109,30 @@ def test_full_pool_is_the_unshared_index_and_errors():
         with pytest.raises(flash.FlashError) as e:
             s.insert_addrs_window(s.hash_addrs(d_rp, d_col), 0, 0, 10)
         assert e.value.status == flash.FLASH_EINVAL
+
+
+@pytest.mark.parametrize("F", [1.0, 0.2])
+def test_save_load_round_trip_then_further_inserts(tmp_path, F):
+    """SPEC S:247 / S:478: load(save(index)) is bit-exact — same tables, same query answers —
+    and inserting more rows into the loaded index equals one build over all rows."""
+    rp, col = _shape("webspam", 3000)
+    n = rp.size - 1
+    K, L, R, rng, seed, k = 4, 50, 16, 1 << 10, 11, 32
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    h = 1800
+    with flash.FlashIndex(K, L, R, rng, seed, F=F) as a:
+        flash.flash_insert(a.h, d_rp[: h + 1].contiguous(), d_col, h, 0)
+        a.save(str(tmp_path / "idx.npz"), max_id=h - 1)
+        want = a.query(d_rp, d_col, k)
+        g0, i0, r0 = a.table_arrays()
+    with flash.FlashIndex.load(str(tmp_path / "idx.npz")) as b:
+        g1, i1, r1 = b.table_arrays()
+        assert torch.equal(g0 - g0[0], g1 - g1[0]) and torch.equal(i0, i1) and torch.equal(r0, r1)
+        got = b.query(d_rp, d_col, k)
+        assert torch.equal(want[0], got[0]) and torch.equal(want[1], got[1])
+        flash.flash_insert(b.h, d_rp[h:].contiguous(), d_col, n - h, h)
+        with flash.FlashIndex(K, L, R, rng, seed, F=F) as c:
+            c.insert(d_rp, d_col, 0)
+            g2, i2, r2 = c.table_arrays()
+            g3, i3, r3 = b.table_arrays()
+            assert torch.equal(g2 - g2[0], g3 - g3[0]) and torch.equal(i2, i3) and torch.equal(r2, r3)
