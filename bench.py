@@ -504,6 +504,9 @@ def run_ours(args):
 SHAPE_CFG = {
     "url": dict(K=4, L=128, R=32, range_=1 << 15, seed=0x5EED0003, k=128, q=10_000, qseed=13),
     "kdd12": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0004, k=128, q=10_000, qseed=14),
+    # the friendster 20-NN graph from scratch (the paper
+    # gives no K/L/R for it: kdd12's K=4, L=32, R=64, 2^20 for a dataset of that scale)
+    "friendster": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0005, k=20, graph=True),
 }
 
 
@@ -543,6 +546,74 @@ def shape_stats(idx, q_addrs, lens, L_, R_, rng_):
                                 "frac_over_R": float((arr > R_).double().mean().item())}}
 
 
+def run_shape_graph(args, cfg, shape):
+    """N=1 line for a k-NN graph of a secondary shape (friendster): one step =
+    flash_knn_graph over every row (hash, build, query all rows).  value = rows/s."""
+    import torch
+
+    from paper_1709_01190_b200 import flash
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    h_rp, h_col, nnz = gen_local(shape, [0, shape.N], 0)
+    log(f"generated {shape.N} rows nnz={nnz} in {time.time() - t0:.1f}s")
+    d_rp, d_col = h_rp.to(dev), h_col.to(dev)
+    k = cfg["k"]
+    out_ids = torch.empty((shape.N, k), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty_like(out_ids)
+    idx = flash.FlashIndex(cfg["K"], cfg["L"], cfg["R"], cfg["range_"], cfg["seed"])
+    stream = torch.cuda.current_stream()
+
+    def step():
+        idx.clear()
+        flash.flash_knn_graph(idx.h, d_rp, d_col, shape.N, k, out_ids, out_cnt)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flash.flash_reset_counters(idx.h)
+    flash.flash_set_profiling(idx.h, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    phase_ms, _ = flash.flash_phase_ms(idx.h)
+    launches = flash.flash_launch_count(idx.h)
+    flash.flash_set_profiling(idx.h, False)
+    lens = np.diff(h_rp.numpy())
+    hbm_peak, peak_kind = peaks()
+    hash_ms = phase_ms[0] / args.steps
+    hash_bytes = 4 * nnz + 8 * (shape.N + 1) + 4 * cfg["L"] * shape.N
+    idx.close()
+    return {
+        "metric": METRIC, "value": shape.N / (ms * 1e-3), "unit": "queries/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "graph_time_s": ms * 1e-3,
+        "hash_nnz_per_s": nnz / (hash_ms * 1e-3),
+        "phase_ms_per_step": {"hash": hash_ms, "build": phase_ms[1] / args.steps, "query": phase_ms[2] / args.steps},
+        "hash_roofline": {"kernel": "k_doph_sparse + k_doph", "bound": "hbm",
+                          "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                          "peak_kind": peak_kind, "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
+                          "algorithmic_bytes": hash_bytes},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": f"synthetic (synth/, {args.workload} shape, seed {shape.seed})",
+        "config": {"workload": f"{args.workload}-shaped approximate {k}-NN graph from scratch",
+                   "N": shape.N, "D": shape.D, "nnz": nnz, "nnz_per_row": round(nnz / shape.N, 1),
+                   "K": cfg["K"], "L": cfg["L"], "R": cfg["R"], "range": cfg["range_"], "k": k,
+                   "seed": cfg["seed"], "parallelism": "1 GPU",
+                   "l2_policy": f"inputs larger than L2 (col_idx {4 * nnz / 1e9:.1f} GB vs 126 MB L2); no flush"},
+        "paper": "friendster 20-NN graph from scratch: 1578 s on 2x Xeon E5-2660 v4, 56 threads (P:505)",
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "data_stats": {"nnz_mean": float(lens.mean()), "nnz_p99": float(np.percentile(lens, 99)),
+                       "nnz_max": int(lens.max())},
+    }
+
+
 def run_shape(args):
     """N=1 line for the url / kdd12 shapes: one step = index all N rows (H1-H3, B1-B2) +
     10K queries (H1-H3 of the query rows, Q1-Q3).  value = queries/s of the query phase;
@@ -555,6 +626,8 @@ def run_shape(args):
     assert world == 1, "--workload url/kdd12 runs on one GPU"
     cfg = SHAPE_CFG[args.workload]
     shape = synth.SHAPES[args.workload]
+    if cfg.get("graph"):
+        return run_shape_graph(args, cfg, shape)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     t0 = time.time()
@@ -699,7 +772,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
     ap.add_argument("--quality-queries", type=int, default=1000)
-    ap.add_argument("--workload", choices=["webspam", "url", "kdd12"], default="webspam",
+    ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster"], default="webspam",
                     help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines")
     args = ap.parse_args()
     if args.workload != "webspam" and args.impl == "ours":

@@ -66,6 +66,9 @@ SHAPES = {
     "url": Shape("url", 2_386_130, 3_231_961, 116.0, 0.4, 0.85, 129, 2, 1.0, 0.015, 3),
     # kdd12: 149.6M x 54.7M dims, 11 nnz/row
     "kdd12": Shape("kdd12", 149_629_105, 54_686_452, 11.0, 0.3, 0.5, 18, 1, 1.0, 0.1, 4),
+    # friendster: 65.6M users x 65.6M dims (friend lists), 27.5 nnz/row, pairwise cos ~0;
+    # heavy-tailed degrees (sigma 1.0), families of users with similar friend sets (mu_f 0.3)
+    "friendster": Shape("friendster", 65_608_366, 65_608_366, 27.5, 1.0, 0.05, 1000, 1, 1.0, 0.3, 5),
 }
 
 
