@@ -11,12 +11,14 @@
 //               few).  The array is now sorted by id.
 //   Q3 count    run lengths of equal ids are the full multiplicities (R#11), found with
 //   + top-k     a ballot of run starts per 32 elements; a histogram of the counts (<= L)
-//               gives the threshold count c*; because the distinct ids come in ascending
-//               order, the ids tied at c* that survive are the first `need` of them (ties
-//               by ascending id, R#12); ids with count > c* go to per-count output cursors
-//               (higher counts first, ids ascending within a count), the ties after them.
-//               No final sort is needed.  Pads are (EMPTY, 0) (R#13).  The excluded id
-//               (self, R#14) is dropped at the gather.
+//               gives the threshold count c*; runs of >= 2 ids (a query's near-
+//               duplicates, few) are listed in ascending id order.  Ids with count > c*
+//               go from that list to per-count output cursors (higher counts first, ids
+//               ascending within a count); the ties at c* that survive are the first
+//               `need` in ascending id order (R#12) — from the list when c* >= 2, else
+//               the once-seen ids, scanned from the start of the sorted array only until
+//               `need` are found.  No final sort.  Pads are (EMPTY, 0) (R#13).  The
+//               excluded id (self, R#14) is dropped at the gather.
 // No hash table, no probing, no CAS: two shared-memory atomics per candidate.
 #include "flash_internal.cuh"
 
@@ -303,11 +305,12 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     __syncwarp();
     QMARK(4);
 
-    // ---- Q3a: run lengths.  Distinct ids are compacted in place to arr[0..nd) (a run's
-    //      write index never exceeds its end index) with their counts in cnt16 (the bin
-    //      counters are done); the count histogram is built on the way. ----
-    uint16_t* cnt16 = reinterpret_cast<uint16_t*>(binw);
-    uint32_t nd = 0;
+    // ---- Q3a: run lengths of equal ids are the multiplicities (R#11).  The count histogram
+    //      is built on the way (runs of one id, the bulk, aggregated per warp); runs of two
+    //      or more are listed as (end index << 16 | count), in ascending id order, in the
+    //      area of the finished bin counters.  The sorted array itself is left in place. ----
+    uint32_t* mlist = binw;
+    uint32_t nd = 0, nm = 0;
     {
       uint32_t carry = 0;  // start index of the run open at the chunk boundary
       for (uint32_t i0 = 0; i0 < mtot; i0 += 32) {
@@ -319,17 +322,17 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         const uint32_t em = __ballot_sync(kFullS, end);
         const uint32_t below = sm & lanemask_le_s();
         const uint32_t st = below ? i0 + 31 - __clz(below) : carry;
-        __syncwarp();  // all reads of this chunk precede the compaction writes
-        if (end) {
-          const uint32_t c = i - st + 1;
-          const uint32_t d = nd + __popc(em & lanemask_lt_s());
-          arr[d] = x;
-          cnt16[d] = (uint16_t)c;
+        const uint32_t c = end ? i - st + 1 : 0u;
+        const uint32_t ones = __ballot_sync(kFullS, c == 1);
+        if (lane == 0 && ones) atomicAdd(&hcnt[1], __popc(ones));
+        const uint32_t mm = __ballot_sync(kFullS, c >= 2);
+        if (c >= 2) {
+          mlist[nm + __popc(mm & lanemask_lt_s())] = (i << 16) | c;
           atomicAdd(&hcnt[c < CM ? c : CM], 1u);
         }
+        nm += __popc(mm);
         nd += __popc(em);
         if (sm) carry = i0 + 31 - __clz(sm);
-        __syncwarp();
       }
     }
     __syncwarp();
@@ -380,21 +383,23 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     }
     __syncwarp();
 
-    // ---- Q3c: one pass over the distinct ids in ascending order: a count above c* is
-    //      written at its count's cursor (so equal counts stay in id order); the first
-    //      `need` ids tied at c* follow all of them ----
+    // ---- Q3c: (1) the listed runs of >= 2, ascending id: a count above c* is written at
+    //      its count's cursor (equal counts stay in id order), ties at c* >= 2 take the
+    //      first `need` slots after all of them; (2) the runs of one id (count 1), scanned
+    //      in ascending order only as far as needed: count 1 is above c* when c* = 0 (every
+    //      distinct id fits) and a tie when c* = 1. ----
     uint32_t* oid = a.out_ids + q * k;
     uint32_t* ocnt = a.out_counts + q * k;
-    uint32_t nh = 0, nt = 0;
-    for (uint32_t d0 = 0; d0 < nd && (nt < need || nh < nhi); d0 += 32) {
-      const uint32_t d = d0 + lane;
-      const uint32_t c = d < nd ? cnt16[d] : 0u;
-      const uint32_t x = d < nd ? arr[d] : 0u;
-      const bool up = c > cstar;
-      const bool tie = cstar > 0 && c == cstar;
+    uint32_t nt = 0;
+    for (uint32_t j0 = 0; j0 < nm; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t e = j < nm ? mlist[j] : 0u;
+      const uint32_t c = e & 0xFFFFu;
+      const uint32_t x = j < nm ? arr[e >> 16] : 0u;
+      const bool up = j < nm && c > cstar;
+      const bool tie = j < nm && cstar >= 2 && c == cstar;
       uint32_t um = __ballot_sync(kFullS, up);
-      nh += __popc(um);
-      while (um) {  // one group per distinct count in this chunk (usually 0-2)
+      while (um) {  // one group per distinct count in this chunk
         const uint32_t c0 = __shfl_sync(kFullS, c, __ffs(um) - 1);
         const uint32_t m = __ballot_sync(kFullS, up && c == c0);
         const uint32_t base = hcnt[c0 < CM ? c0 : CM];
@@ -415,6 +420,31 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         ocnt[nhi + rank] = c;
       }
       nt += __popc(mt);
+    }
+    if (cstar <= 1) {
+      const bool all1 = cstar == 0;
+      uint32_t base1 = all1 ? hcnt[1] : 0u;  // count-1 cursor (descending-count prefix)
+      for (uint32_t i0 = 0; i0 < mtot && (all1 || nt < need); i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint32_t x = i < mtot ? arr[i] : kEmpty;
+        const bool single = i < mtot && (i == 0 || arr[i - 1] != x) && (i + 1 == mtot || arr[i + 1] != x);
+        const uint32_t sg = __ballot_sync(kFullS, single);
+        if (all1) {
+          if (single) {
+            const uint32_t pos = base1 + __popc(sg & lanemask_lt_s());
+            oid[pos] = x;
+            ocnt[pos] = 1;
+          }
+          base1 += __popc(sg);
+        } else {
+          const uint32_t rank = nt + __popc(sg & lanemask_lt_s());
+          if (single && rank < need) {
+            oid[nhi + rank] = x;
+            ocnt[nhi + rank] = 1;
+          }
+          nt += __popc(sg);
+        }
+      }
     }
     __syncwarp();
     if (nt > need) nt = need;
