@@ -197,6 +197,80 @@ __global__ void __launch_bounds__(256) k_fill_tm(const uint32_t* __restrict__ ad
   }
 }
 
+// Shared-memory build passes (tables whose bucket counters fit shared memory, e.g. webspam /
+// url: 2^15 buckets).  Global L2 atomics cap k_count / k_fill_new at ~1 atomic per L2 slice
+// per clock; here each CTA owns one table and a contiguous slice of the rows (S slices per
+// table), histograms its transposed address column in shared memory, and publishes the
+// slice histogram (hbuf) plus the table's arrival totals.  The scatter pass then starts each
+// slice's bucket cursors at the bucket's old kept count plus the earlier slices' counts, so
+// the pool positions are disjoint without global atomics.
+constexpr uint32_t kSmemBuildThreads = 1024;
+constexpr uint32_t kSmemBuildMaxRange = 40960;  // 160 KB of u32 counters
+
+__global__ void __launch_bounds__(kSmemBuildThreads) k_count_smem(const uint32_t* __restrict__ addrsT, uint64_t n,
+                                                                  uint32_t t0, uint32_t range, uint32_t S,
+                                                                  uint32_t* __restrict__ cursor,
+                                                                  uint32_t* __restrict__ hbuf,
+                                                                  unsigned long long* err) {
+  extern __shared__ uint32_t hsm[];  // [range]
+  const uint32_t j = blockIdx.x / S, c = blockIdx.x - j * S;
+  const uint64_t r0 = n * c / S, r1 = n * (c + 1) / S;
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) hsm[b] = 0;
+  __syncthreads();
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4ull * blockDim.x) {
+    uint32_t a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = r + u * blockDim.x < r1 ? col[r + u * blockDim.x] : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (a[u] == kEmpty) continue;
+      if (a[u] >= range) atomicAdd(err, 1ull);
+      else atomicAdd(&hsm[a[u]], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* hb = hbuf + (uint64_t)blockIdx.x * range;
+  uint32_t* cur = cursor + (uint64_t)(t0 + j) * range;
+  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
+    const uint32_t v = hsm[b];
+    hb[b] = v;
+    if (v) atomicAdd(&cur[b], v);
+  }
+}
+
+__global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t* __restrict__ addrsT, uint64_t n,
+                                                                 uint32_t t0, uint32_t range, uint32_t S,
+                                                                 uint32_t id_base, const uint32_t* __restrict__ cursor,
+                                                                 const uint32_t* __restrict__ hbuf,
+                                                                 const uint64_t* __restrict__ pool_off,
+                                                                 uint32_t* __restrict__ pool) {
+  // [range] this slice's next pool position in each bucket, relative to the table's pool start
+  // (a table's pool holds < 2^32 entries: its rows' arrivals plus its old kept ids)
+  extern __shared__ uint32_t csm[];
+  const uint32_t j = blockIdx.x / S, c = blockIdx.x - j * S;
+  const uint64_t r0 = n * c / S, r1 = n * (c + 1) / S;
+  const uint64_t tb = (uint64_t)(t0 + j) * range;
+  const uint64_t pbase = pool_off[tb];
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
+    // the bucket's old kept ids come first (k_pool_sizes left their count in cursor)
+    uint32_t base = (uint32_t)(pool_off[tb + b] - pbase) + cursor[tb + b];
+    for (uint32_t c2 = 0; c2 < c; ++c2) base += hbuf[(uint64_t)(j * S + c2) * range + b];
+    csm[b] = base;
+  }
+  __syncthreads();
+  uint32_t* tpool = pool + pbase;
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4ull * blockDim.x) {
+    uint32_t a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = r + u * blockDim.x < r1 ? col[r + u * blockDim.x] : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a[u] < range) tpool[atomicAdd(&csm[a[u]], 1u)] = id_base + (uint32_t)(r + u * blockDim.x);
+  }
+}
+
 __global__ void k_pool_sizes(uint32_t nb, uint32_t R, const uint64_t* __restrict__ goff_old,
                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ arrivals,
                              uint64_t* __restrict__ pool_cnt, uint64_t* __restrict__ keep_cnt) {
@@ -666,6 +740,14 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const ui
 
 }  // namespace
 
+uint32_t smem_build_slices(uint32_t W) {
+  // about one wave of one 1024-thread CTA per SM: S row slices per table
+  const uint32_t s = W ? 148u / W : 1u;
+  return s < 1 ? 1u : (s > 16 ? 16u : s);
+}
+
+bool smem_build_fits(uint32_t range) { return range <= kSmemBuildMaxRange; }
+
 size_t build_scan_tmp_bytes(uint64_t nb) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
@@ -696,9 +778,23 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
   cudaMemsetAsync(a.big_count, 0, 3 * sizeof(uint32_t), s);  // big, mid, register-path list counters
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
-  const bool tm = a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (see k_count_tm)
+  const bool sm_build = a.hbuf != nullptr && a.addrsT != nullptr && a.n && W && !a.shared;  // k_count_smem
+  const bool tm = !sm_build && a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (k_count_tm)
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
-  if (tm) {
+  const uint32_t S = smem_build_slices(W);
+  if (sm_build) {
+    static bool attr_sm = false;
+    if (!attr_sm) {
+      cudaFuncSetAttribute(k_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemBuildMaxRange * 4));
+      cudaFuncSetAttribute(k_fill_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemBuildMaxRange * 4));
+      attr_sm = true;
+    }
+    k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
+                                                                   a.addrsT);
+    k_count_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.cursor,
+                                                                      a.hbuf, a.err);
+    launches += 2;
+  } else if (tm) {
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
     k_count_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.cursor,
@@ -721,7 +817,11 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);
     launches++;
   }
-  if (tm) {
+  if (sm_build) {
+    k_fill_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.id_base,
+                                                                     a.cursor, a.hbuf, a.pool_off, a.pool);
+    launches++;
+  } else if (tm) {
     k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,
                                                       a.cursor, a.pool_off, a.pool);
     launches++;

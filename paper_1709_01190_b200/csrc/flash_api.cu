@@ -107,6 +107,7 @@ struct flash_index {
   DevBuf addrsT;              // build: window addresses transposed to [W][n] (table-major passes)
   DevBuf qhuge;               // query: global count tables of the L*R > 8192 class (kept clean)
   DevBuf raddr, qraddr;       // shared mode: rows' / queries' distinct reservoir indices
+  DevBuf hbuf;                // build: slice histograms of the shared-memory passes
   DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   unsigned long long* err = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -227,7 +228,14 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   const char* tm_env = getenv("FLASH_BUILD_TM");
   const bool tm = !h->shared &&
                   (tm_env ? tm_env[0] == '1' : (nb * 12 > (32ull << 20) && h->range >= (1u << 18)));
-  if (tm && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
+  // shared-memory passes when a table's bucket counters fit shared memory (the default
+  // there; FLASH_BUILD_SMEM=0 disables them, tests)
+  const char* sm_env = getenv("FLASH_BUILD_SMEM");
+  const bool smb = !tm && !h->shared && t1 > t0 && n > 0 && smem_build_fits(h->range) &&
+                   !(sm_env && sm_env[0] == '0');
+  if ((tm || smb) && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
+  if (smb)
+    TRY(ensure(h->hbuf, sizeof(uint32_t) * (size_t)(t1 - t0) * smem_build_slices(t1 - t0) * h->range));
 
   Phase ph(h, 1, s);
   BuildArgs a;
@@ -235,7 +243,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.addrs = addrs;
   a.astride = cols ? t1 - t0 : h->L;  // cols: addrs holds only the window's columns
   a.acol0 = cols ? t0 : 0;
-  a.addrsT = (tm && t1 > t0) ? h->addrsT.as<uint32_t>() : nullptr;
+  a.addrsT = ((tm || smb) && t1 > t0) ? h->addrsT.as<uint32_t>() : nullptr;
+  a.hbuf = smb ? h->hbuf.as<uint32_t>() : nullptr;
   a.shared = h->shared;
   a.n = n;
   a.id_base = id_base;
@@ -405,7 +414,7 @@ void flash_destroy(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge, &h->raddr, &h->qraddr,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge, &h->raddr, &h->qraddr, &h->hbuf,
                     &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);

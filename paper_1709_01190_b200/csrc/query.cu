@@ -62,14 +62,28 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
     const uint64_t q = q0 + lane;
     uint64_t M = 0;
     if (q < nq) {
-      for (uint32_t t = 0; t < L; ++t) {
-        const uint32_t a = direct ? (uint32_t)q : addrs[q * L + t];
-        if (a < (shared ? shared : range)) {
-          const uint64_t i = shared ? (uint64_t)a : (uint64_t)t * range + a;
-          M += goff[i + 1] - goff[i];
-        } else if (a != kEmpty) {
-          atomicAdd(err, 1ull);
+      const uint32_t lim = shared ? shared : range;
+      // 8 tables per step: the address loads, then the offset loads, all independent, so
+      // each lane has up to 16 loads in flight instead of one dependent pair per table
+      for (uint32_t t0 = 0; t0 < L; t0 += 8) {
+        uint32_t a[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u)
+          a[u] = t0 + u < L ? (direct ? (uint32_t)q : addrs[q * L + t0 + u]) : kEmpty;
+        uint64_t lo[8], hi[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+          lo[u] = hi[u] = 0;
+          if (a[u] < lim) {
+            const uint64_t i = shared ? (uint64_t)a[u] : (uint64_t)(t0 + u) * range + a[u];
+            lo[u] = goff[i];
+            hi[u] = goff[i + 1];
+          } else if (a[u] != kEmpty) {
+            atomicAdd(err, 1ull);
+          }
         }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) M += hi[u] - lo[u];
       }
     }
     int cls = 0;

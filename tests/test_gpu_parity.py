@@ -122,12 +122,17 @@ BUILD_CASES = [
 ]
 
 
-@pytest.mark.parametrize("tm", ["0", "1"], ids=["rowmajor", "tablemajor"])
+BUILD_SCHEDULES = {"rowmajor": ("0", "0"), "tablemajor": ("1", "1"), "smem": ("0", "1")}
+
+
+@pytest.mark.parametrize("sched", list(BUILD_SCHEDULES))
 @pytest.mark.parametrize("name,make,K,L,R,rng", BUILD_CASES, ids=[c[0] for c in BUILD_CASES])
-def test_tables_bit_exact(monkeypatch, name, make, K, L, R, rng, tm):
-    """Both build schedules: row-major passes, and the table-major passes (transposed
-    addresses, table-ordered grid) used for indexes whose bucket arrays outgrow L2."""
-    monkeypatch.setenv("FLASH_BUILD_TM", tm)
+def test_tables_bit_exact(monkeypatch, name, make, K, L, R, rng, sched):
+    """Every build schedule: row-major global-atomic passes, the table-major passes
+    (transposed addresses, table-ordered grid: large tables), and the shared-memory
+    passes (a CTA per table slice: tables whose counters fit shared memory)."""
+    monkeypatch.setenv("FLASH_BUILD_TM", BUILD_SCHEDULES[sched][0])
+    monkeypatch.setenv("FLASH_BUILD_SMEM", BUILD_SCHEDULES[sched][1])
     rp, col = make()
     n = rp.size - 1
     seed = 0xB0 + R
@@ -160,9 +165,10 @@ def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch, mode):
             _check_tables(idx, T)
 
 
-@pytest.mark.parametrize("tm", ["0", "1"], ids=["rowmajor", "tablemajor"])
-def test_incremental_inserts_equal_one_build(monkeypatch, tm):
-    monkeypatch.setenv("FLASH_BUILD_TM", tm)
+@pytest.mark.parametrize("sched", list(BUILD_SCHEDULES))
+def test_incremental_inserts_equal_one_build(monkeypatch, sched):
+    monkeypatch.setenv("FLASH_BUILD_TM", BUILD_SCHEDULES[sched][0])
+    monkeypatch.setenv("FLASH_BUILD_SMEM", BUILD_SCHEDULES[sched][1])
     rp, col = shape_slice("url", 5000)
     n = rp.size - 1
     K, L, R, rng, seed = 3, 20, 16, 1 << 9, 99
