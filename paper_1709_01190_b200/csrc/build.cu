@@ -347,9 +347,30 @@ __device__ __forceinline__ void push_big(uint32_t i, uint32_t* big_list, uint32_
   if ((threadIdx.x & 31) == 0) big_list[atomicAdd(big_count, 1u)] = i;
 }
 
-// B2, buckets with <= 32 members (the vast majority): one warp per bucket, keys in
-// registers, no shared memory (full occupancy).  Larger buckets are listed for
-// k_select_warp (or the exact CTA path when FLASH_DEBUG_FORCE_BIG is set).
+// Ascending sort of each aligned w-lane segment (w = 8, 16 or 32) of one u32 key per lane:
+// the bitonic network restricted to stages k <= w, the last stage ascending in every segment.
+__device__ __forceinline__ uint32_t warp_sort_seg(uint32_t key, uint32_t w) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+    if (k > w) break;
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t other = __shfl_xor_sync(kFull, key, j);
+      const bool up = (lane & k & (w - 1)) == 0;
+      const bool lower = (lane & j) == 0;
+      key = (lower == up) ? min(key, other) : max(key, other);
+    }
+  }
+  return key;
+}
+
+// B2, buckets with <= 32 members (the vast majority): a warp takes 4 consecutive buckets at
+// a time and sorts those that keep every member (m <= R) together — 4 segments of 8 lanes,
+// 2 rounds of 2 x 16 lanes, or 4 rounds of 32 lanes, by the largest of them — keys in
+// registers, no shared memory.  A bucket with more than R (<= 32) members sorts its
+// (prio, id) keys with the whole warp first.  Larger buckets are listed for k_select_mid /
+// k_select_warp / k_select_big (or the exact CTA path when FLASH_DEBUG_FORCE_BIG is set).
 __global__ void __launch_bounds__(256)
 k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
                const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
@@ -359,28 +380,60 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
                uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb; i += nw) {
-    const uint64_t p0 = pool_off[i];
-    const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
-    if (m == 0) continue;
-    if (m > 32) {  // > 2048 members: the CTA path streams them with 256 threads
-      if (force_big || m > 2048) push_big(i, big_list, big_count);
-      else if (m <= kMidMax && R <= kMidMax) push_big(i, reg_list, reg_count);
-      else push_big(i, mid_list, mid_count);
-      continue;
+  const uint32_t ngroups = (nb + 3) / 4;
+  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups; g += nw) {
+    const uint32_t i0 = g * 4;
+    const uint64_t pl = lane <= 4 && i0 + lane <= nb ? pool_off[i0 + lane] : 0ull;
+    const uint64_t gl = lane < 4 && i0 + lane < nb ? goff[i0 + lane] : 0ull;
+    uint64_t p[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) p[u] = __shfl_sync(kFull, pl, u);
+    uint32_t m[4], mx = 0;
+    bool plain[4];  // <= 32 members, all kept: sorted together below
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      m[u] = i0 + u < nb ? (uint32_t)(p[u + 1] - p[u]) : 0u;
+      plain[u] = m[u] > 0 && m[u] <= 32 && m[u] <= R;
+      if (plain[u]) mx = max(mx, m[u]);
     }
-    const uint32_t keep = m < R ? m : R;
-    uint32_t* out = ids_out + goff[i];
-    uint32_t id = lane < m ? pool[p0 + lane] : kEmpty;
-    if (m > R) {  // bottom-R by (prio, id)
-      const uint32_t t = i / range, b = i - t * range;
-      const uint64_t tb = prio_bucket_key(keys, t, b);
-      uint64_t key = lane < m ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
-      key = warp_sort32(key);
-      id = lane < keep ? (uint32_t)key : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u;
+      if (m[u] > 32) {  // > 2048 members: the CTA path streams them with 256 threads
+        if (force_big || m[u] > 2048) push_big(i, big_list, big_count);
+        else if (m[u] <= kMidMax && R <= kMidMax) push_big(i, reg_list, reg_count);
+        else push_big(i, mid_list, mid_count);
+      } else if (m[u] > R) {  // bottom-R by (prio, id), whole warp
+        const uint32_t keep = R;
+        uint32_t* out = ids_out + __shfl_sync(kFull, gl, u);
+        uint32_t id = lane < m[u] ? pool[p[u] + lane] : kEmpty;
+        const uint32_t t = i / range, b = i - t * range;
+        const uint64_t tb = prio_bucket_key(keys, t, b);
+        uint64_t key = lane < m[u] ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
+        key = warp_sort32(key);
+        id = lane < keep ? (uint32_t)key : kEmpty;
+        id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
+        if (lane < keep) out[lane] = id;
+      }
     }
-    id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
-    if (lane < keep) out[lane] = id;
+    if (mx == 0) continue;
+    const uint32_t w = mx <= 8 ? 8u : (mx <= 16 ? 16u : 32u);
+    const uint32_t per = 32 / w;  // buckets per round
+    for (uint32_t u0 = 0; u0 < 4; u0 += per) {
+      const uint32_t u = u0 + lane / w, e = lane & (w - 1);
+      uint32_t mu = 0, id = kEmpty;
+      uint64_t pu = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (v == (int)u && plain[v]) {
+          mu = m[v];
+          pu = p[v];
+        }
+      if (e < mu) id = pool[pu + e];
+      id = warp_sort_seg(id, w);  // ascending id within each bucket's segment (R#10)
+      const uint64_t ou = __shfl_sync(kFull, gl, u & 3);
+      if (e < mu) ids_out[ou + e] = id;
+    }
   }
 }
 
@@ -844,7 +897,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   uint32_t* mid_count = a.big_count + 1;
   uint32_t* reg_list = reinterpret_cast<uint32_t*>(a.pool_cnt);  // free once pool_off is scanned
   uint32_t* reg_count = a.big_count + 2;
-  const unsigned small_blocks = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 64 ? ((uint64_t)nb + 7) / 8 : 148ull * 64);
+  const uint64_t small_warps = ((uint64_t)nb + 3) / 4;  // 4 buckets per warp step
+  const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < 148ull * 64 ? (small_warps + 7) / 8 : 148ull * 64);
   k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
                                              a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
                                              a.big_count);
