@@ -24,6 +24,8 @@ namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kSelThreads = 256;
+constexpr int kBigThreads = 1024;     // k_select_big: one wide CTA per large bucket
+constexpr uint32_t kWarpMax = 512;    // buckets above this go to the CTA path
 constexpr uint32_t kWarpCap = 1024;   // per-warp sort buffer (u64 keys)
 constexpr uint32_t kBigCap = 4096;    // CTA path: kept ids sorted in smem (R <= kBigCap)
 constexpr uint32_t kMidMax = 256;     // register path (k_select_mid): m, R <= kMidMax
@@ -399,8 +401,8 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t i = i0 + u;
-      if (m[u] > 32) {  // > 2048 members: the CTA path streams them with 256 threads
-        if (force_big || m[u] > 2048) push_big(i, big_list, big_count);
+      if (m[u] > 32) {  // > kWarpMax members: the CTA path streams them with 1024 threads
+        if (force_big || m[u] > kWarpMax) push_big(i, big_list, big_count);
         else if (m[u] <= kMidMax && R <= kMidMax) push_big(i, reg_list, reg_count);
         else push_big(i, mid_list, mid_count);
       } else if (m[u] > R) {  // bottom-R by (prio, id), whole warp
@@ -649,7 +651,7 @@ k_select_warp(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restr
 // keeps ~R + 6 sqrt(R) + 16 candidates in shared memory; if at least `keep` and at most
 // kBigCap survive, a CTA bitonic sort by (prio, id) picks the bottom-R.  Otherwise an
 // exact radix select of the keep-th smallest (prio, id), 8 bits at a time, decides.
-__global__ void __launch_bounds__(kSelThreads)
+__global__ void __launch_bounds__(kBigThreads)
 k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const uint64_t* __restrict__ pool_off,
              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
              uint32_t* __restrict__ ids_out, const uint32_t* __restrict__ big_list,
@@ -908,7 +910,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   k_select_warp<<<148 * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
                                                       a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;
-  k_select_big<<<148 * 2, kSelThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
+  k_select_big<<<148, kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
                                               a.ids_new, a.big_list, a.big_count);
   launches += 1;
   return launches;
