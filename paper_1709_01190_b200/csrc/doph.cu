@@ -231,7 +231,7 @@ __host__ __device__ __forceinline__ uint32_t sparse_warp_words(uint32_t B) {
 }
 
 template <bool kCodes, bool kAddrs>
-__global__ void __launch_bounds__(kThreads) k_doph_sparse(const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __restrict__ row_ptr,
                                                           const uint32_t* __restrict__ col_idx,
                                                           uint64_t n_rows, uint32_t K, uint32_t L,
                                                           uint32_t range, HashKeys keys,
