@@ -61,6 +61,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def clk_mhz_for_peak():
+    """SM clock for issue-rate peaks: nvidia-smi's max SM clock, else the B200 boost clock."""
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout.split()
+        return float(out[0])
+    except Exception:
+        return 1965.0
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -423,12 +433,16 @@ def run_ours(args):
         build_ms = per_step["build"]
         dominant = max(("hash", hash_ms), ("build", build_ms), ("query", query_ms), key=lambda x: x[1])[0]
         traffic = {}  # ncu --set full DRAM bytes of one graph, summed per kernel name
+        issue = {}    # ncu warp instructions and durations per kernel name
         try:
             with open(TRAFFIC_PATH) as f:
                 for d in json.load(f):
                     nm = d["kernel"].split("::")[-1].split("<")[0]
                     if d.get("dram_traffic_bytes") is not None:
                         traffic[nm] = traffic.get(nm, 0.0) + d["dram_traffic_bytes"]
+                    if d.get("warp_inst") is not None and d.get("duration_ms"):
+                        w, t = issue.get(nm, (0.0, 0.0))
+                        issue[nm] = (w + d["warp_inst"], t + d["duration_ms"])
         except Exception:
             pass
         q_traffic = None
@@ -443,6 +457,14 @@ def run_ours(args):
                     "hbm_view": {"algorithmic_bytes": 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local,
                                  "achieved_GBps": (4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local)
                                  / (query_ms * 1e-3) / 1e9}}
+            if "k_query_sort" in issue:
+                # instruction-issue view from the committed ncu capture: warp instructions
+                # issued per second by the sort kernels vs 4 schedulers x 148 SMs x clock
+                w, t = issue["k_query_sort"]
+                peak_issue = 4 * 148 * clk_mhz_for_peak() * 1e6
+                roof["issue_view"] = {"kernel": "k_query_sort (all classes, ncu)", "warp_inst": w,
+                                      "warp_inst_per_query": w / n_local, "achieved_warp_inst_per_s": w / (t * 1e-3),
+                                      "peak_warp_inst_per_s": peak_issue, "frac": w / (t * 1e-3) / peak_issue}
         elif dominant == "build":
             bbytes = 8 * L * n_local * 2 + 12 * L * n_local
             roof = {"kernel": "build (k_count..k_select_big)", "bound": "hbm",
