@@ -382,8 +382,13 @@ def test_table_windows_assemble_to_the_full_index():
                 assert np.array_equal(off, o_off) and np.array_equal(ids_t, o_ids_t) and np.array_equal(arr_t, o_arr)
 
 
-@pytest.mark.parametrize("G,L,tm", [(2, 50, "0"), (3, 50, "1"), (8, 50, "0"), (5, 4, "1")])
-def test_candidate_exchange_loopback_equals_oracle_graph(monkeypatch, G, L, tm):
+EXCHANGE_CASES = [(2, 50, "0", 128, 1 << 12, 64), (3, 50, "1", 128, 1 << 12, 64), (8, 50, "0", 128, 1 << 12, 64),
+                  (5, 4, "1", 128, 1 << 12, 64), (7, 13, "0", 5, 300, 17), (4, 64, "0", 32, 1 << 10, 128),
+                  (6, 6, "1", 2, 64, 9), (3, 1, "0", 64, 128, 20)]
+
+
+@pytest.mark.parametrize("G,L,tm,R,rng,k", EXCHANGE_CASES)
+def test_candidate_exchange_loopback_equals_oracle_graph(monkeypatch, G, L, tm, R, rng, k):
     """The table-partitioned multi-GPU path (north_star (d), dist.knn_graph_candidate_exchange)
     with G virtual ranks on one GPU: every C-ABI step runs for real (owner-blocked hash,
     window build from the address all-to-all's layout, window gather, count/top-k over
@@ -394,7 +399,7 @@ def test_candidate_exchange_loopback_equals_oracle_graph(monkeypatch, G, L, tm):
     monkeypatch.setenv("FLASH_BUILD_TM", tm)
     rp, col = shape_slice("webspam", 1500)
     n = rp.size - 1
-    K, R, rng, seed, k = 4, 128, 1 << 12, 0x5EED0002, 64
+    K, seed = 4, 0x5EED0002
     o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
     bounds = fdist.shard_bounds(np.diff(rp), G)
     wins = [fdist.table_window(L, G, g) for g in range(G)]
