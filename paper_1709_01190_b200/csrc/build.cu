@@ -814,11 +814,7 @@ int launch_shared_reservoirs(const uint32_t* addrs, uint64_t n, uint32_t L, uint
                              const HashKeys& keys, uint32_t* out, unsigned long long* err, cudaStream_t s) {
   if (n == 0) return 0;
   const size_t smem = (size_t)8 * L * sizeof(uint32_t);
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_shared_reservoirs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)k_shared_reservoirs, smem);
   const uint64_t want = (n + 7) / 8;
   const unsigned blocks = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
   k_shared_reservoirs<<<blocks, 256, smem, s>>>(addrs, n, L, range, P, keys, out, err);
@@ -838,12 +834,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
   const uint32_t S = smem_build_slices(W);
   if (sm_build) {
-    static bool attr_sm = false;
-    if (!attr_sm) {
-      cudaFuncSetAttribute(k_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemBuildMaxRange * 4));
-      cudaFuncSetAttribute(k_fill_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemBuildMaxRange * 4));
-      attr_sm = true;
-    }
+    ensure_smem_attr((const void*)k_count_smem, (size_t)kSmemBuildMaxRange * 4);
+    ensure_smem_attr((const void*)k_fill_smem, (size_t)kSmemBuildMaxRange * 4);
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
     k_count_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.cursor,
@@ -885,12 +877,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                            a.id_base, a.cursor, a.pool_off, a.pool);
     launches++;
   }
-  static bool attr = false;
   const size_t sel_smem = (size_t)(kSelThreads / 32) * kWarpCap * sizeof(uint64_t);
-  if (!attr) {
-    cudaFuncSetAttribute(k_select_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_select_warp, sel_smem);
   // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
   // =2: and the CTA path skips its filter (exact radix select).  Tests only.
   const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");

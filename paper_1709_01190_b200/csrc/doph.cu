@@ -330,12 +330,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int64_t skip_le = -1;
   if (B <= kSparseMaxB) {  // rows with <= kSparseNnz nonzeros: the table-driven kernel
     const size_t smem = ((size_t)(B * B + 3) / 4 + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
-    static bool attr_s = false;
-    if (!attr_s) {
-      cudaFuncSetAttribute(k_doph_sparse<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      cudaFuncSetAttribute(k_doph_sparse<C, A>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      attr_s = true;
-    }
+    ensure_smem_attr((const void*)k_doph_sparse<C, A>, 100 * 1024, true);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
@@ -351,14 +346,9 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int wpb = (int)((96 * 1024) / per_warp);
   wpb = wpb < 1 ? 1 : (wpb > kThreads / 32 ? kThreads / 32 : wpb);
   const size_t smem = per_warp * wpb;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // the column stream bypasses L1 (no_allocate): give the whole carveout to shared memory,
-    // so the per-warp bin arrays never cap the resident warps below the thread limit
-    cudaFuncSetAttribute(k_doph<C, A>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = smem;
-  }
+  // the column stream bypasses L1 (no_allocate): give the whole carveout to shared memory,
+  // so the per-warp bin arrays never cap the resident warps below the thread limit
+  ensure_smem_attr((const void*)k_doph<C, A>, smem, true);
   uint64_t blocks = (n_rows + wpb - 1) / wpb;  // one warp per row: the block scheduler balances
   // the skewed row lengths; with the sparse kernel in use, a grid-stride cap keeps the launch
   // from scheduling millions of CTAs that would only skip sparse rows

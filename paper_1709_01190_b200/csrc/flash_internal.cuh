@@ -71,6 +71,10 @@ __device__ __forceinline__ uint32_t prio_of(uint64_t tb, uint32_t id) {
   return (uint32_t)(mix64(tb ^ (uint64_t)id) >> 32);
 }
 
+// Set a kernel's dynamic shared-memory limit (and optionally the max carveout) once per
+// (kernel, device) for at least `bytes` (util.cu).
+bool ensure_smem_attr(const void* func, size_t bytes, bool carveout_max = false);
+
 // ---------------------------------------------------------------------------
 // Launchers (each returns the number of kernels it launched).
 // ---------------------------------------------------------------------------

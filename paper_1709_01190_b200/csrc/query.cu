@@ -524,13 +524,7 @@ template <int LOG2S, int NT, bool GLOBAL>
 int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t hist_len,
                  uint8_t* gtab, cudaStream_t s) {
   const size_t smem = class_smem(LOG2S, a.L > a.cmax ? a.L : a.cmax, a.k, hist_len, GLOBAL);
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query<LOG2S, NT, GLOBAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return 0;
-    attr = smem;
-  }
+  if (!ensure_smem_attr((const void*)k_query<LOG2S, NT, GLOBAL>, smem)) return 0;
   uint64_t grid;
   if (GLOBAL) {
     grid = kHugeCtas;  // one table slice each (query_huge_table_bytes)

@@ -466,13 +466,7 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
   const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
   const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
   const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * kWarps;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(k_query_sort<MCAP, BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return 0;
-    attr = smem;
-  }
+  if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL>, smem)) return 0;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL>, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
