@@ -797,7 +797,7 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const ui
 
 uint32_t smem_build_slices(uint32_t W) {
   // about one wave of one 1024-thread CTA per SM: S row slices per table
-  const uint32_t s = W ? 148u / W : 1u;
+  const uint32_t s = W ? device_sms() / W : 1u;
   return s < 1 ? 1u : (s > 16 ? 16u : s);
 }
 
@@ -816,7 +816,7 @@ int launch_shared_reservoirs(const uint32_t* addrs, uint64_t n, uint32_t L, uint
   const size_t smem = (size_t)8 * L * sizeof(uint32_t);
   ensure_smem_attr((const void*)k_shared_reservoirs, smem);
   const uint64_t want = (n + 7) / 8;
-  const unsigned blocks = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
+  const unsigned blocks = (unsigned)(want < (uint64_t)device_sms() * 16 ? want : (uint64_t)device_sms() * 16);
   k_shared_reservoirs<<<blocks, 256, smem, s>>>(addrs, n, L, range, P, keys, out, err);
   return 1;
 }
@@ -824,8 +824,8 @@ int launch_shared_reservoirs(const uint32_t* addrs, uint64_t n, uint32_t L, uint
 int launch_build(const BuildArgs& a, cudaStream_t s) {
   const uint32_t nb = a.shared ? a.shared : a.L * a.range;
   int launches = 0;
-  const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < 148ull * 32 ? (a.n + 7) / 8 : 148ull * 32);
-  const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < 148ull * 32 ? ((uint64_t)nb + 256) / 256 : 148ull * 32);
+  const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < (uint64_t)device_sms() * 32 ? (a.n + 7) / 8 : (uint64_t)device_sms() * 32);
+  const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < (uint64_t)device_sms() * 32 ? ((uint64_t)nb + 256) / 256 : (uint64_t)device_sms() * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
   cudaMemsetAsync(a.big_count, 0, 3 * sizeof(uint32_t), s);  // big, mid, register-path list counters
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
@@ -860,7 +860,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.keep_cnt, a.goff_new, (int64_t)nb + 1, s);
   // (the two CUB scans launch library kernels; they are not counted as ours)
   if (a.goff_old) {
-    const unsigned wb = (unsigned)(((uint64_t)nb + 7) / 8 < 148ull * 32 ? ((uint64_t)nb + 7) / 8 : 148ull * 32);
+    const unsigned wb = (unsigned)(((uint64_t)nb + 7) / 8 < (uint64_t)device_sms() * 32 ? ((uint64_t)nb + 7) / 8 : (uint64_t)device_sms() * 32);
     k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);
     launches++;
   }
@@ -888,17 +888,17 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   uint32_t* reg_list = reinterpret_cast<uint32_t*>(a.pool_cnt);  // free once pool_off is scanned
   uint32_t* reg_count = a.big_count + 2;
   const uint64_t small_warps = ((uint64_t)nb + 3) / 4;  // 4 buckets per warp step
-  const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < 148ull * 64 ? (small_warps + 7) / 8 : 148ull * 64);
+  const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < (uint64_t)device_sms() * 64 ? (small_warps + 7) / 8 : (uint64_t)device_sms() * 64);
   k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
                                              a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
                                              a.big_count);
-  k_select_mid<<<148 * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, a.pool, a.goff_new,
+  k_select_mid<<<device_sms() * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, a.pool, a.goff_new,
                                        a.ids_new, a.big_list, a.big_count);
   launches += 1;
-  k_select_warp<<<148 * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
+  k_select_warp<<<device_sms() * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
                                                       a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;
-  k_select_big<<<148, kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
+  k_select_big<<<device_sms(), kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
                                               a.ids_new, a.big_list, a.big_count);
   launches += 1;
   return launches;

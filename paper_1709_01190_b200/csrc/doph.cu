@@ -334,7 +334,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    uint64_t blocks = 148ull * per_sm;
+    uint64_t blocks = (uint64_t)device_sms() * per_sm;
     const uint64_t need = (n_rows + kThreads - 1) / kThreads;  // 32 rows per warp-chunk
     if (blocks > need) blocks = need;
     k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,

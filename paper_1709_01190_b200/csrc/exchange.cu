@@ -99,7 +99,7 @@ int launch_window_sizes(const uint32_t* addrs, uint64_t n, uint32_t t0, uint32_t
                         size_t scan_tmp_bytes, unsigned long long* err, cudaStream_t s) {
   if (n == 0) return 0;
   const uint64_t want = (n + 255) / 256;
-  const unsigned blocks = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
+  const unsigned blocks = (unsigned)(want < (uint64_t)device_sms() * 16 ? want : (uint64_t)device_sms() * 16);
   k_window_sizes<<<blocks, 256, 0, s>>>(addrs, n, t0, t1 - t0, range, goff, sizes, err);
   launch_scan_sizes(sizes, n, off, scan_tmp, scan_tmp_bytes, s);
   return 1;
@@ -110,7 +110,7 @@ int launch_window_gather(const uint32_t* addrs, uint64_t n, uint32_t t0, uint32_
                          cudaStream_t s) {
   if (n == 0 || t1 == t0) return 0;
   const uint64_t want = (n + 7) / 8;
-  const unsigned blocks = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
+  const unsigned blocks = (unsigned)(want < (uint64_t)device_sms() * 16 ? want : (uint64_t)device_sms() * 16);
   k_window_gather<<<blocks, 256, 0, s>>>(addrs, n, t0, t1 - t0, range, goff, ids, off, out);
   return 1;
 }

@@ -74,6 +74,8 @@ __device__ __forceinline__ uint32_t prio_of(uint64_t tb, uint32_t id) {
 // Set a kernel's dynamic shared-memory limit (and optionally the max carveout) once per
 // (kernel, device) for at least `bytes` (util.cu).
 bool ensure_smem_attr(const void* func, size_t bytes, bool carveout_max = false);
+// SM count of the current device (cached per device; 148 on B200)
+uint32_t device_sms();
 
 // ---------------------------------------------------------------------------
 // Launchers (each returns the number of kernels it launched).

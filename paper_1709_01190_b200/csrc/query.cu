@@ -532,7 +532,7 @@ int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<LOG2S, NT, GLOBAL>, NT, smem);
     if (per_sm < 1) per_sm = 1;
-    grid = 148ull * per_sm;
+    grid = (uint64_t)device_sms() * per_sm;
   }
   if (grid > a.nq) grid = a.nq;
   k_query<LOG2S, NT, GLOBAL><<<(unsigned)grid, NT, smem, s>>>(a, list, count, hist_len, gtab);
@@ -576,7 +576,7 @@ int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream
   cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kClasses, s);
   const uint64_t warps = (a.nq + 31) / 32;
   uint64_t blocks = (warps + 7) / 8;
-  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (blocks > (uint64_t)device_sms() * 16) blocks = (uint64_t)device_sms() * 16;
   const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
   k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, a.direct, a.shared, max_m, a.k,
                                                  a.out_ids, a.out_counts, lists, counts, a.err);

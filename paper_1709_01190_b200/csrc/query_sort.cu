@@ -470,7 +470,7 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL>, 32 * kWarps, smem);
   if (per_sm < 1) per_sm = 1;
-  uint64_t grid = 148ull * per_sm;
+  uint64_t grid = (uint64_t)device_sms() * per_sm;
   const uint64_t need = (a.nq + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   k_query_sort<MCAP, BL><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count, shift);

@@ -29,4 +29,23 @@ bool ensure_smem_attr(const void* func, size_t bytes, bool carveout_max) {
   return true;
 }
 
+// Streaming-multiprocessor count of the current device (148 on B200), cached per device:
+// persistent grids are sized as a multiple of it.
+uint32_t device_sms() {
+  static std::mutex mu;
+  static std::map<int, uint32_t> sms;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148;
+  }
+  sms[dev] = (uint32_t)n;
+  return (uint32_t)n;
+}
+
 }  // namespace flash
