@@ -162,7 +162,10 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
       // Pass 2: the probe chains of the empty bins, dynamically balanced over the lanes:
       // a lane that finds its donor takes the next listed bin, so every step of the
       // warp-uniform loop advances ~32 chains (a probe count per bin is geometric; a
-      // static bin-per-lane split would wait for the longest chain of each round).
+      // static bin-per-lane split would wait for the longest chain of each round).  Each
+      // step evaluates 4 consecutive probes of the lane's chain (independent hashes and
+      // loads) and takes the first hit in chain order, amortising the bookkeeping.
+      constexpr uint32_t kBatch = 4;  // divides kProbes
       uint32_t e = lane, a = 1, next = 32;
       uint32_t i = e < ne ? elist[e] : 0u;
       while (__any_sync(0xFFFFFFFFu, e < ne)) {
@@ -170,12 +173,18 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
         bool hit = false;
         uint32_t x = kEmpty;
         if (active) {
-          const uint32_t j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B);
-          x = v[j];
+          uint32_t jl = 0;
+#pragma unroll
+          for (uint32_t u = 0; u < kBatch; ++u) {
+            const uint32_t j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | (a + u))), B);
+            const uint32_t y = v[j];
+            if (x == kEmpty) x = y;  // the first hit in chain order wins
+            jl = j;
+          }
           hit = x != kEmpty;
-          if (!hit && a == kProbes) {  // chain exhausted: circular scan from its last bin
+          if (!hit && a + kBatch > kProbes) {  // chain exhausted: circular scan from its last bin
             for (uint32_t m = 1; m <= B; ++m) {
-              uint32_t jj = j + m;
+              uint32_t jj = jl + m;
               if (jj >= B) jj -= B;
               x = v[jj];
               if (x != kEmpty) break;
@@ -190,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
           a = 1;
           if (e < ne) i = elist[e];
         } else if (active) {
-          ++a;
+          a += kBatch;
         }
         next += __popc(done);
       }
