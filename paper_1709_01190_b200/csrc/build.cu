@@ -241,12 +241,38 @@ __global__ void __launch_bounds__(kSmemBuildThreads) k_count_smem(const uint32_t
   }
 }
 
+// Each slice's first pool position in every bucket of its table, relative to the table's pool
+// start: the bucket's offset, then its old kept ids (their count is in cursor after
+// k_pool_sizes), then the earlier slices' arrivals — an exclusive scan over the slices,
+// written over the slice histograms.
+__global__ void k_slice_bases(uint32_t W, uint32_t t0, uint32_t range, uint32_t S,
+                              const uint32_t* __restrict__ cursor, const uint64_t* __restrict__ pool_off,
+                              uint32_t* __restrict__ hbuf) {
+  const uint64_t total = (uint64_t)W * range;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)(x / range), b = (uint32_t)(x - (uint64_t)j * range);
+    const uint64_t tb = (uint64_t)(t0 + j) * range;
+    uint32_t run = (uint32_t)(pool_off[tb + b] - pool_off[tb]) + cursor[tb + b];
+    uint32_t* h = hbuf + (uint64_t)j * S * range + b;
+    for (uint32_t c0 = 0; c0 < S; c0 += 8) {  // 8 independent loads in flight
+      uint32_t v[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) v[u] = c0 + u < S ? h[(uint64_t)(c0 + u) * range] : 0u;
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        if (c0 + u < S) h[(uint64_t)(c0 + u) * range] = run;
+        run += v[u];
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t* __restrict__ addrsT, uint64_t n,
                                                                  uint32_t t0, uint32_t range, uint32_t S,
                                                                  uint32_t id_base, const uint32_t* __restrict__ cursor,
                                                                  const uint32_t* __restrict__ hbuf,
                                                                  const uint64_t* __restrict__ pool_off,
-                                                                 uint32_t* __restrict__ pool) {
+                                                                 uint32_t* __restrict__ pool, int prefixed) {
   // [range] this slice's next pool position in each bucket, relative to the table's pool start
   // (a table's pool holds < 2^32 entries: its rows' arrivals plus its old kept ids)
   extern __shared__ uint32_t csm[];
@@ -255,11 +281,15 @@ __global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t*
   const uint64_t tb = (uint64_t)(t0 + j) * range;
   const uint64_t pbase = pool_off[tb];
   const uint32_t* col = addrsT + (uint64_t)j * n;
-  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
-    // the bucket's old kept ids come first (k_pool_sizes left their count in cursor)
-    uint32_t base = (uint32_t)(pool_off[tb + b] - pbase) + cursor[tb + b];
-    for (uint32_t c2 = 0; c2 < c; ++c2) base += hbuf[(uint64_t)(j * S + c2) * range + b];
-    csm[b] = base;
+  if (prefixed) {  // k_slice_bases turned the slice histograms into each slice's first positions
+    for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) csm[b] = hbuf[(uint64_t)(j * S + c) * range + b];
+  } else {  // few slices: the same scan, here
+    for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
+      // the bucket's old kept ids come first (k_pool_sizes left their count in cursor)
+      uint32_t base = (uint32_t)(pool_off[tb + b] - pbase) + cursor[tb + b];
+      for (uint32_t c2 = 0; c2 < c; ++c2) base += hbuf[(uint64_t)(j * S + c2) * range + b];
+      csm[b] = base;
+    }
   }
   __syncthreads();
   uint32_t* tpool = pool + pbase;
@@ -795,10 +825,18 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const ui
 
 }  // namespace
 
-uint32_t smem_build_slices(uint32_t W) {
-  // about one wave of one 1024-thread CTA per SM: S row slices per table
-  const uint32_t s = W ? device_sms() / W : 1u;
-  return s < 1 ? 1u : (s > 16 ? 16u : s);
+uint32_t smem_build_slices(uint32_t W, uint64_t n) {
+  // S row slices per table: about one wave of 1024-thread CTAs (one per SM) when every
+  // table's pool region (4 B per row) fits L2 together; otherwise enough slices that the
+  // CTAs resident at once cover only the few tables whose regions fit ~96 MB of L2, so
+  // the scattered pool writes stay in L2 (the grid is table-major)
+  const uint32_t sms = device_sms();
+  const uint64_t region = 4 * (n ? n : 1);
+  uint64_t tc = (96ull << 20) / region;  // tables whose regions fit L2 at once
+  if (tc < 1) tc = 1;
+  uint64_t s = W ? sms / W : 1u;
+  if (tc < W) s = (sms + tc - 1) / tc;
+  return (uint32_t)(s < 1 ? 1 : (s > 64 ? 64 : s));
 }
 
 bool smem_build_fits(uint32_t range) { return range <= kSmemBuildMaxRange; }
@@ -832,7 +870,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const bool sm_build = a.hbuf != nullptr && a.addrsT != nullptr && a.n && W && !a.shared;  // k_count_smem
   const bool tm = !sm_build && a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (k_count_tm)
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
-  const uint32_t S = smem_build_slices(W);
+  const uint32_t S = smem_build_slices(W, a.n);
   if (sm_build) {
     ensure_smem_attr((const void*)k_count_smem, (size_t)kSmemBuildMaxRange * 4);
     ensure_smem_attr((const void*)k_fill_smem, (size_t)kSmemBuildMaxRange * 4);
@@ -865,8 +903,15 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     launches++;
   }
   if (sm_build) {
+    const bool prefixed = S > 4;  // many slices: scan them once up front
+    if (prefixed) {
+      const uint64_t sb = ((uint64_t)W * a.range + 255) / 256;
+      k_slice_bases<<<(unsigned)(sb < (uint64_t)device_sms() * 16 ? sb : (uint64_t)device_sms() * 16), 256, 0,
+                      s>>>(W, a.t0, a.range, S, a.cursor, a.pool_off, a.hbuf);
+      launches++;
+    }
     k_fill_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.id_base,
-                                                                     a.cursor, a.hbuf, a.pool_off, a.pool);
+                                                                     a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
     launches++;
   } else if (tm) {
     k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,

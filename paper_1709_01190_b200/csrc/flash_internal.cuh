@@ -128,7 +128,7 @@ struct BuildArgs {
   size_t scan_tmp_bytes;
 };
 size_t build_scan_tmp_bytes(uint64_t nb);
-uint32_t smem_build_slices(uint32_t W);  // row slices per table of the shared-memory passes
+uint32_t smem_build_slices(uint32_t W, uint64_t n);  // row slices per table (shared-memory passes)
 bool smem_build_fits(uint32_t range);
 int launch_build(const BuildArgs& a, cudaStream_t s);
 
