@@ -292,14 +292,33 @@ __global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t*
     }
   }
   __syncthreads();
+  // Rows go in chunks of blockDim with a barrier between chunks, so a bucket's entries from
+  // different chunks land in row (= id) order; only rows of one chunk that share a bucket
+  // (rare: ~blockDim^2 / 2range pairs per chunk) may land out of order.  k_select_small
+  // then finds most buckets already ascending and skips their sort.  The next chunks'
+  // addresses are loaded ahead (4 chunks in flight).
   uint32_t* tpool = pool + pbase;
-  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4ull * blockDim.x) {
-    uint32_t a[4];
+  const uint32_t bd = blockDim.x;
+  uint32_t a[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = r + u * blockDim.x < r1 ? col[r + u * blockDim.x] : kEmpty;
+  for (int u = 0; u < 4; ++u) {
+    const uint64_t r = r0 + threadIdx.x + (uint64_t)u * bd;
+    a[u] = r < r1 ? col[r] : kEmpty;
+  }
+  for (uint64_t base = r0; base < r1; base += 4ull * bd) {
+    uint32_t nx[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (a[u] < range) tpool[atomicAdd(&csm[a[u]], 1u)] = id_base + (uint32_t)(r + u * blockDim.x);
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t r = base + 4ull * bd + threadIdx.x + (uint64_t)u * bd;
+      nx[u] = r < r1 ? col[r] : kEmpty;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (a[u] < range) tpool[atomicAdd(&csm[a[u]], 1u)] = id_base + (uint32_t)(base + threadIdx.x + (uint64_t)u * bd);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = nx[u];
   }
 }
 
@@ -397,23 +416,27 @@ __device__ __forceinline__ uint32_t warp_sort_seg(uint32_t key, uint32_t w) {
   return key;
 }
 
-// B2, buckets with <= 32 members (the vast majority): a warp takes 4 consecutive buckets at
-// a time and sorts those that keep every member (m <= R) together — 4 segments of 8 lanes,
-// 2 rounds of 2 x 16 lanes, or 4 rounds of 32 lanes, by the largest of them — keys in
-// registers, no shared memory.  A bucket with more than R (<= 32) members sorts its
-// (prio, id) keys with the whole warp first.  Larger buckets are listed for k_select_mid /
-// k_select_warp / k_select_big (or the exact CTA path when FLASH_DEBUG_FORCE_BIG is set).
-__global__ void __launch_bounds__(256)
-k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
-               const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
-               const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
-               uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
-               uint32_t* __restrict__ reg_list, uint32_t* __restrict__ reg_count,
-               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+// B2, buckets with <= 32 members (the vast majority).  A warp takes 32 consecutive buckets
+// at a time.  When all of them keep every member (m <= 32 and m <= R: their pool range and
+// output range are contiguous and equal) it stages the range in shared memory with
+// coalesced loads, each lane insertion-sorts its bucket there (the chunk-ordered scatter of
+// k_fill_smem leaves buckets nearly ascending, so this is ~m steps), and the warp stores the
+// range back coalesced.  Otherwise the chunk goes 4 buckets at a time through
+// select_group4: buckets that keep every member are sorted together in registers (4
+// segments of 8 lanes, 2 rounds of 2 x 16 lanes or 4 rounds of 32 lanes, by the largest);
+// a bucket with more than R (<= 32) members sorts its (prio, id) keys with the whole warp;
+// larger buckets are listed for k_select_mid / k_select_warp / k_select_big (or the exact
+// CTA path when FLASH_DEBUG_FORCE_BIG is set).
+constexpr uint32_t kSmallChunk = 32;                 // buckets per warp step
+constexpr uint32_t kSmallBuf = kSmallChunk * 32;     // ids staged per warp
+__device__ __forceinline__ void select_group4(uint32_t g, uint32_t nb, uint32_t range, uint32_t R, const HashKeys& keys,
+                                              int force_big, const uint64_t* __restrict__ pool_off,
+                                              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
+                                              uint32_t* __restrict__ ids_out, uint32_t* __restrict__ mid_list,
+                                              uint32_t* __restrict__ mid_count, uint32_t* __restrict__ reg_list,
+                                              uint32_t* __restrict__ reg_count, uint32_t* __restrict__ big_list,
+                                              uint32_t* __restrict__ big_count) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  const uint32_t ngroups = (nb + 3) / 4;
-  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups; g += nw) {
     const uint32_t i0 = g * 4;
     const uint64_t pl = lane <= 4 && i0 + lane <= nb ? pool_off[i0 + lane] : 0ull;
     const uint64_t gl = lane < 4 && i0 + lane < nb ? goff[i0 + lane] : 0ull;
@@ -448,7 +471,7 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
         if (lane < keep) out[lane] = id;
       }
     }
-    if (mx == 0) continue;
+    if (mx == 0) return;
     const uint32_t w = mx <= 8 ? 8u : (mx <= 16 ? 16u : 32u);
     const uint32_t per = 32 / w;  // buckets per round
     for (uint32_t u0 = 0; u0 < 4; u0 += per) {
@@ -462,9 +485,59 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
           pu = p[v];
         }
       if (e < mu) id = pool[pu + e];
-      id = warp_sort_seg(id, w);  // ascending id within each bucket's segment (R#10)
+      // ascending id within each bucket's segment (R#10); the ordered scatter of
+      // k_fill_smem leaves most buckets sorted already
+      const uint32_t up = __shfl_up_sync(kFull, id, 1);
+      if (__any_sync(kFull, e > 0 && e < mu && up > id)) id = warp_sort_seg(id, w);
       const uint64_t ou = __shfl_sync(kFull, gl, u & 3);
       if (e < mu) ids_out[ou + e] = id;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
+               const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
+               const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
+               uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
+               uint32_t* __restrict__ reg_list, uint32_t* __restrict__ reg_count,
+               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  __shared__ uint32_t sbuf[256 / 32][kSmallBuf];
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* buf = sbuf[threadIdx.x >> 5];
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t ngroups = (nb + 3) / 4;
+  const uint32_t nchunks = (nb + kSmallChunk - 1) / kSmallChunk;
+  for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nw) {
+    const uint32_t i0 = c * kSmallChunk, i = i0 + lane;
+    const uint64_t pl = pool_off[i < nb ? i : nb];
+    const uint64_t pe = pool_off[i < nb ? i + 1 : nb];
+    const uint32_t m = (uint32_t)(pe - pl);
+    if (__all_sync(kFull, m <= 32 && m <= R)) {
+      const uint64_t p0 = __shfl_sync(kFull, pl, 0);
+      const uint32_t T = (uint32_t)(__shfl_sync(kFull, pe, 31) - p0);  // <= kSmallBuf
+      const uint64_t g0 = goff[i0];
+#pragma unroll 4
+      for (uint32_t j = lane; j < T; j += 32) buf[j] = pool[p0 + j];
+      __syncwarp();
+      const uint32_t s0 = (uint32_t)(pl - p0), e0 = s0 + m;
+      for (uint32_t a = s0 + 1; a < e0; ++a) {  // ascending id within the bucket (R#10)
+        const uint32_t x = buf[a];
+        uint32_t b = a;
+        while (b > s0 && buf[b - 1] > x) {
+          buf[b] = buf[b - 1];
+          --b;
+        }
+        buf[b] = x;
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (uint32_t j = lane; j < T; j += 32) ids_out[g0 + j] = buf[j];
+      __syncwarp();
+    } else {
+      const uint32_t gend = min((c + 1) * (kSmallChunk / 4), ngroups);
+      for (uint32_t g = c * (kSmallChunk / 4); g < gend; ++g)
+        select_group4(g, nb, range, R, keys, force_big, pool_off, pool, goff, ids_out, mid_list, mid_count, reg_list,
+                      reg_count, big_list, big_count);
     }
   }
 }
@@ -932,7 +1005,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   uint32_t* mid_count = a.big_count + 1;
   uint32_t* reg_list = reinterpret_cast<uint32_t*>(a.pool_cnt);  // free once pool_off is scanned
   uint32_t* reg_count = a.big_count + 2;
-  const uint64_t small_warps = ((uint64_t)nb + 3) / 4;  // 4 buckets per warp step
+  const uint64_t small_warps = ((uint64_t)nb + kSmallChunk - 1) / kSmallChunk;  // 32 buckets per warp step
   const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < (uint64_t)device_sms() * 64 ? (small_warps + 7) / 8 : (uint64_t)device_sms() * 64);
   k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
                                              a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,

@@ -465,7 +465,8 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
   // digit = the top BL bits of the id range [0, max_id]
   const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
   const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
-  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * kWarps;
+  static const size_t pad = [] { const char* e = getenv("FLASH_QSORT_PAD"); return e ? (size_t)atol(e) : (size_t)0; }();
+  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * kWarps + pad;
   if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL>, smem)) return 0;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL>, 32 * kWarps, smem);
