@@ -92,7 +92,7 @@ __device__ __forceinline__ void warp_sort_range(uint32_t* arr, uint32_t lo, uint
 
 __host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins, uint32_t L, uint32_t CM) {
   size_t b = (size_t)mcap * 4            // ids, sorted in place by bin
-             + (size_t)(kBins > mcap ? kBins : mcap) * 2  // u16 bin counters, later distinct counts
+             + (size_t)(kBins * 2 > mcap ? kBins * 2 : mcap)  // u16 bin counters, later the u16 run list
              + (size_t)L * 8              // base of each non-empty segment (bucket)
              + ((size_t)mcap / 32 + 2) * 4  // bucket-start bitmap
              + (size_t)(CM + 1) * 4;      // count histogram
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   uint8_t* my = sms + sort_slice_bytes(MCAP, kBins, L, CM) * wib;
   uint32_t* arr = reinterpret_cast<uint32_t*>(my);                  // [MCAP]
   uint32_t* binw = arr + MCAP;                                      // [kBins/2] packed u16
-  constexpr uint32_t CW = (kBins > MCAP ? kBins : MCAP) / 2;        // words of the u16 area
+  constexpr uint32_t CW = (kBins * 2 > MCAP ? kBins * 2 : MCAP) / 4;  // words of the u16 area
   // nbase[j]: address of candidate position 0 if it lay in the j-th non-empty bucket,
   // so candidate p of that bucket is nbase[j][p] (one wide multiply-add per gather)
   const uint32_t** nbase = reinterpret_cast<const uint32_t**>(binw + CW);  // [L]
@@ -307,9 +307,13 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
 
     // ---- Q3a: run lengths of equal ids are the multiplicities (R#11).  The count histogram
     //      is built on the way (runs of one id, the bulk, aggregated per warp); runs of two
-    //      or more are listed as (end index << 16 | count), in ascending id order, in the
+    //      or more are listed by their end index (and count), in ascending id order, in the
     //      area of the finished bin counters.  The sorted array itself is left in place. ----
-    uint32_t* mlist = binw;
+    // (kBins >= MCAP: the area holds MCAP/2 (end << 16 | count) words; otherwise only u16 end
+    // indices fit, and the count is recovered by walking back over the run)
+    constexpr bool kList16 = MCAP > kBins;
+    uint16_t* mlist16 = reinterpret_cast<uint16_t*>(binw);
+    uint32_t* mlist32 = binw;
     uint32_t nd = 0, nm = 0;
     {
       uint32_t carry = 0;  // start index of the run open at the chunk boundary
@@ -327,7 +331,9 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
         if (lane == 0 && ones) atomicAdd(&hcnt[1], __popc(ones));
         const uint32_t mm = __ballot_sync(kFullS, c >= 2);
         if (c >= 2) {
-          mlist[nm + __popc(mm & lanemask_lt_s())] = (i << 16) | c;
+          const uint32_t slot = nm + __popc(mm & lanemask_lt_s());
+          if (kList16) mlist16[slot] = (uint16_t)i;
+          else mlist32[slot] = (i << 16) | c;
           atomicAdd(&hcnt[c < CM ? c : CM], 1u);
         }
         nm += __popc(mm);
@@ -393,9 +399,20 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
     uint32_t nt = 0;
     for (uint32_t j0 = 0; j0 < nm; j0 += 32) {
       const uint32_t j = j0 + lane;
-      const uint32_t e = j < nm ? mlist[j] : 0u;
-      const uint32_t c = e & 0xFFFFu;
-      const uint32_t x = j < nm ? arr[e >> 16] : 0u;
+      uint32_t x = 0, c = 0;
+      if (j < nm) {
+        if (kList16) {  // the run ends at e; walk back over it for its length
+          const uint32_t e = mlist16[j];
+          x = arr[e];
+          uint32_t b = e;
+          while (b > 0 && arr[b - 1] == x) --b;
+          c = e - b + 1;
+        } else {
+          const uint32_t e = mlist32[j];
+          x = arr[e >> 16];
+          c = e & 0xFFFFu;
+        }
+      }
       const bool up = j < nm && c > cstar;
       const bool tie = j < nm && cstar >= 2 && c == cstar;
       uint32_t um = __ballot_sync(kFullS, up);
