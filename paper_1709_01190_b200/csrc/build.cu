@@ -10,11 +10,13 @@
 // scatter is erased by the per-bucket (prio, id) selection and the final id sort.
 //
 // Kernels: k_count (B1 histogram) -> k_pool_sizes -> 2 scans -> k_fill_old / k_fill_new
-// (scatter every member into a bucket-contiguous pool) -> k_select_small (one warp per
-// bucket with <= 32 members, keys in registers) -> k_select_warp (one warp per bucket
-// with 33..2048 members: priority-threshold filter to ~R+6sqrt(R) survivors, shared-
-// memory bitonic sort) -> k_select_big (one CTA per larger or leftover bucket: the same
-// filter with the whole CTA, exact radix select on the priority as the fallback).
+// (scatter every member into a bucket-contiguous pool; or the shared-memory / table-major
+// variants) -> k_select_small (buckets with <= 32 members: a warp per 32 buckets, staged
+// in shared memory and insertion-sorted) -> k_select_mid (33..256 members, registers) ->
+// k_select_warp (one warp per bucket up to 512 members: priority-threshold filter to
+// ~R+6sqrt(R) survivors, shared-memory bitonic sort) -> k_select_big (one CTA per larger or
+// leftover bucket: the same filter with the whole CTA, exact radix select on the priority
+// as the fallback).
 #include <cub/device/device_scan.cuh>
 
 #include "flash_internal.cuh"
@@ -398,100 +400,43 @@ __device__ __forceinline__ void push_big(uint32_t i, uint32_t* big_list, uint32_
   if ((threadIdx.x & 31) == 0) big_list[atomicAdd(big_count, 1u)] = i;
 }
 
-// Ascending sort of each aligned w-lane segment (w = 8, 16 or 32) of one u32 key per lane:
-// the bitonic network restricted to stages k <= w, the last stage ascending in every segment.
-__device__ __forceinline__ uint32_t warp_sort_seg(uint32_t key, uint32_t w) {
-  const uint32_t lane = threadIdx.x & 31;
-#pragma unroll
-  for (uint32_t k = 2; k <= 32; k <<= 1) {
-    if (k > w) break;
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t other = __shfl_xor_sync(kFull, key, j);
-      const bool up = (lane & k & (w - 1)) == 0;
-      const bool lower = (lane & j) == 0;
-      key = (lower == up) ? min(key, other) : max(key, other);
-    }
-  }
-  return key;
-}
-
 // B2, buckets with <= 32 members (the vast majority).  A warp takes 32 consecutive buckets
 // at a time.  When all of them keep every member (m <= 32 and m <= R: their pool range and
 // output range are contiguous and equal) it stages the range in shared memory with
 // coalesced loads, each lane insertion-sorts its bucket there (the chunk-ordered scatter of
 // k_fill_smem leaves buckets nearly ascending, so this is ~m steps), and the warp stores the
-// range back coalesced.  Otherwise the chunk goes 4 buckets at a time through
-// select_group4: buckets that keep every member are sorted together in registers (4
-// segments of 8 lanes, 2 rounds of 2 x 16 lanes or 4 rounds of 32 lanes, by the largest);
-// a bucket with more than R (<= 32) members sorts its (prio, id) keys with the whole warp;
-// larger buckets are listed for k_select_mid / k_select_warp / k_select_big (or the exact
-// CTA path when FLASH_DEBUG_FORCE_BIG is set).
+// range back coalesced.  In a mixed chunk each lane stages, sorts and writes its own
+// all-kept bucket; a bucket with more than R (<= 32) members sorts its (prio, id) keys with
+// the whole warp; larger buckets are listed for k_select_mid / k_select_warp / k_select_big
+// (or the exact CTA path when FLASH_DEBUG_FORCE_BIG is set).
 constexpr uint32_t kSmallChunk = 32;                 // buckets per warp step
 constexpr uint32_t kSmallBuf = kSmallChunk * 32;     // ids staged per warp
-__device__ __forceinline__ void select_group4(uint32_t g, uint32_t nb, uint32_t range, uint32_t R, const HashKeys& keys,
-                                              int force_big, const uint64_t* __restrict__ pool_off,
-                                              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
-                                              uint32_t* __restrict__ ids_out, uint32_t* __restrict__ mid_list,
-                                              uint32_t* __restrict__ mid_count, uint32_t* __restrict__ reg_list,
-                                              uint32_t* __restrict__ reg_count, uint32_t* __restrict__ big_list,
-                                              uint32_t* __restrict__ big_count) {
+
+// bottom-R of bucket i (R < m <= 32) by (prio, id) with the whole warp, written ascending
+__device__ __forceinline__ void select_over_r(uint32_t i, uint32_t m, uint64_t p, uint64_t g, uint32_t range,
+                                              uint32_t R, const HashKeys& keys, const uint32_t* __restrict__ pool,
+                                              uint32_t* __restrict__ ids_out) {
   const uint32_t lane = threadIdx.x & 31;
-    const uint32_t i0 = g * 4;
-    const uint64_t pl = lane <= 4 && i0 + lane <= nb ? pool_off[i0 + lane] : 0ull;
-    const uint64_t gl = lane < 4 && i0 + lane < nb ? goff[i0 + lane] : 0ull;
-    uint64_t p[5];
-#pragma unroll
-    for (int u = 0; u < 5; ++u) p[u] = __shfl_sync(kFull, pl, u);
-    uint32_t m[4], mx = 0;
-    bool plain[4];  // <= 32 members, all kept: sorted together below
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      m[u] = i0 + u < nb ? (uint32_t)(p[u + 1] - p[u]) : 0u;
-      plain[u] = m[u] > 0 && m[u] <= 32 && m[u] <= R;
-      if (plain[u]) mx = max(mx, m[u]);
+  uint32_t id = lane < m ? pool[p + lane] : kEmpty;
+  const uint32_t t = i / range, b = i - t * range;
+  const uint64_t tb = prio_bucket_key(keys, t, b);
+  uint64_t key = lane < m ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
+  key = warp_sort32(key);
+  id = lane < R ? (uint32_t)key : kEmpty;
+  id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
+  if (lane < R) ids_out[g + lane] = id;
+}
+
+__device__ __forceinline__ void insertion_sort(uint32_t* buf, uint32_t s0, uint32_t e0) {
+  for (uint32_t a = s0 + 1; a < e0; ++a) {  // ascending id within the bucket (R#10)
+    const uint32_t x = buf[a];
+    uint32_t b = a;
+    while (b > s0 && buf[b - 1] > x) {
+      buf[b] = buf[b - 1];
+      --b;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = i0 + u;
-      if (m[u] > 32) {  // > kWarpMax members: the CTA path streams them with 1024 threads
-        if (force_big || m[u] > kWarpMax) push_big(i, big_list, big_count);
-        else if (m[u] <= kMidMax && R <= kMidMax) push_big(i, reg_list, reg_count);
-        else push_big(i, mid_list, mid_count);
-      } else if (m[u] > R) {  // bottom-R by (prio, id), whole warp
-        const uint32_t keep = R;
-        uint32_t* out = ids_out + __shfl_sync(kFull, gl, u);
-        uint32_t id = lane < m[u] ? pool[p[u] + lane] : kEmpty;
-        const uint32_t t = i / range, b = i - t * range;
-        const uint64_t tb = prio_bucket_key(keys, t, b);
-        uint64_t key = lane < m[u] ? ((uint64_t)prio_of(tb, id) << 32) | id : ~0ull;
-        key = warp_sort32(key);
-        id = lane < keep ? (uint32_t)key : kEmpty;
-        id = warp_sort32_u32(id);  // ascending id; EMPTY (> any id) sorts last
-        if (lane < keep) out[lane] = id;
-      }
-    }
-    if (mx == 0) return;
-    const uint32_t w = mx <= 8 ? 8u : (mx <= 16 ? 16u : 32u);
-    const uint32_t per = 32 / w;  // buckets per round
-    for (uint32_t u0 = 0; u0 < 4; u0 += per) {
-      const uint32_t u = u0 + lane / w, e = lane & (w - 1);
-      uint32_t mu = 0, id = kEmpty;
-      uint64_t pu = 0;
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (v == (int)u && plain[v]) {
-          mu = m[v];
-          pu = p[v];
-        }
-      if (e < mu) id = pool[pu + e];
-      // ascending id within each bucket's segment (R#10); the ordered scatter of
-      // k_fill_smem leaves most buckets sorted already
-      const uint32_t up = __shfl_up_sync(kFull, id, 1);
-      if (__any_sync(kFull, e > 0 && e < mu && up > id)) id = warp_sort_seg(id, w);
-      const uint64_t ou = __shfl_sync(kFull, gl, u & 3);
-      if (e < mu) ids_out[ou + e] = id;
-    }
+    buf[b] = x;
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -505,7 +450,6 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* buf = sbuf[threadIdx.x >> 5];
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  const uint32_t ngroups = (nb + 3) / 4;
   const uint32_t nchunks = (nb + kSmallChunk - 1) / kSmallChunk;
   for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nw) {
     const uint32_t i0 = c * kSmallChunk, i = i0 + lane;
@@ -519,25 +463,41 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
 #pragma unroll 4
       for (uint32_t j = lane; j < T; j += 32) buf[j] = pool[p0 + j];
       __syncwarp();
-      const uint32_t s0 = (uint32_t)(pl - p0), e0 = s0 + m;
-      for (uint32_t a = s0 + 1; a < e0; ++a) {  // ascending id within the bucket (R#10)
-        const uint32_t x = buf[a];
-        uint32_t b = a;
-        while (b > s0 && buf[b - 1] > x) {
-          buf[b] = buf[b - 1];
-          --b;
-        }
-        buf[b] = x;
-      }
+      insertion_sort(buf, (uint32_t)(pl - p0), (uint32_t)(pl - p0) + m);
       __syncwarp();
 #pragma unroll 4
       for (uint32_t j = lane; j < T; j += 32) ids_out[g0 + j] = buf[j];
       __syncwarp();
     } else {
-      const uint32_t gend = min((c + 1) * (kSmallChunk / 4), ngroups);
-      for (uint32_t g = c * (kSmallChunk / 4); g < gend; ++g)
-        select_group4(g, nb, range, R, keys, force_big, pool_off, pool, goff, ids_out, mid_list, mid_count, reg_list,
-                      reg_count, big_list, big_count);
+      const bool kept_all = i < nb && m <= 32 && m <= R;
+      const uint32_t ps = kept_all ? m : 0u;
+      uint32_t x = ps;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t so = x - ps;  // this lane's staging offset
+      for (uint32_t e = 0; e < ps; ++e) buf[so + e] = pool[pl + e];
+      insertion_sort(buf, so, so + ps);
+      if (ps) {
+        const uint64_t go = goff[i];
+        for (uint32_t e = 0; e < ps; ++e) ids_out[go + e] = buf[so + e];
+      }
+      if (i < nb && m > 32) {  // > kWarpMax members: the CTA path streams them with 1024 threads
+        if (force_big || m > kWarpMax) big_list[atomicAdd(big_count, 1u)] = i;
+        else if (m <= kMidMax && R <= kMidMax) reg_list[atomicAdd(reg_count, 1u)] = i;
+        else mid_list[atomicAdd(mid_count, 1u)] = i;
+      }
+      uint32_t over = __ballot_sync(kFull, i < nb && m <= 32 && m > R);
+      const uint64_t gi = (i < nb && m <= 32 && m > R) ? goff[i] : 0ull;
+      while (over) {
+        const uint32_t u = __ffs(over) - 1;
+        over &= over - 1;
+        select_over_r(i0 + u, __shfl_sync(kFull, m, u), __shfl_sync(kFull, pl, u), __shfl_sync(kFull, gi, u), range,
+                      R, keys, pool, ids_out);
+      }
+      __syncwarp();
     }
   }
 }
