@@ -203,66 +203,82 @@ __global__ void __launch_bounds__(256) k_fill_tm(const uint32_t* __restrict__ ad
 
 // Shared-memory build passes (tables whose bucket counters fit shared memory, e.g. webspam /
 // url: 2^15 buckets).  Global L2 atomics cap k_count / k_fill_new at ~1 atomic per L2 slice
-// per clock; here each CTA owns one table and a contiguous slice of the rows (S slices per
-// table), histograms its transposed address column in shared memory, and publishes the
-// slice histogram (hbuf) plus the table's arrival totals.  The scatter pass then starts each
-// slice's bucket cursors at the bucket's old kept count plus the earlier slices' counts, so
-// the pool positions are disjoint without global atomics.
+// per clock; here the W tables' (table, row) pairs — units j*n + r, table-major — are cut
+// into C equal ranges, one 1024-thread CTA each (C = one per SM when every table's pool
+// region fits L2 together, so no SM idles for want of a whole table slice).  A CTA's range
+// is one or more segments (j, [r0, r1)); for each it histograms the transposed address
+// column in shared memory and publishes the segment histogram (hbuf slot b + j: a table's
+// segments have consecutive slots, in row order) plus the table's arrival totals.  The
+// scatter pass then starts each segment's bucket cursors at the bucket's old kept count
+// plus the earlier segments' counts, so the pool positions are disjoint without global
+// atomics.
 constexpr uint32_t kSmemBuildThreads = 1024;
 constexpr uint32_t kSmemBuildMaxRange = 40960;  // 160 KB of u32 counters
 
+// the CTA whose unit range holds unit x: the largest b with floor(b*U/C) <= x
+__host__ __device__ __forceinline__ uint64_t cta_of_unit(uint64_t x, uint64_t U, uint64_t C) {
+  return ((x + 1) * C - 1) / U;
+}
+
 __global__ void __launch_bounds__(kSmemBuildThreads) k_count_smem(const uint32_t* __restrict__ addrsT, uint64_t n,
-                                                                  uint32_t t0, uint32_t range, uint32_t S,
+                                                                  uint32_t t0, uint32_t range, uint32_t W, uint32_t C,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint32_t* __restrict__ hbuf,
                                                                   unsigned long long* err) {
   extern __shared__ uint32_t hsm[];  // [range]
-  const uint32_t j = blockIdx.x / S, c = blockIdx.x - j * S;
-  const uint64_t r0 = n * c / S, r1 = n * (c + 1) / S;
-  const uint32_t* col = addrsT + (uint64_t)j * n;
-  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) hsm[b] = 0;
-  __syncthreads();
-  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4ull * blockDim.x) {
-    uint32_t a[4];
+  const uint64_t U = (uint64_t)W * n, b = blockIdx.x;
+  const uint64_t u0 = b * U / C, u1 = (b + 1) * U / C;
+  if (u0 >= u1) return;
+  for (uint32_t j = (uint32_t)(u0 / n); j <= (uint32_t)((u1 - 1) / n); ++j) {
+    const uint64_t r0 = max(u0, (uint64_t)j * n) - (uint64_t)j * n;
+    const uint64_t r1 = min(u1, (uint64_t)(j + 1) * n) - (uint64_t)j * n;
+    const uint32_t* col = addrsT + (uint64_t)j * n;
+    for (uint32_t bb = threadIdx.x; bb < range; bb += blockDim.x) hsm[bb] = 0;
+    __syncthreads();
+    for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4ull * blockDim.x) {
+      uint32_t a[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = r + u * blockDim.x < r1 ? col[r + u * blockDim.x] : kEmpty;
+      for (int u = 0; u < 4; ++u) a[u] = r + u * blockDim.x < r1 ? col[r + u * blockDim.x] : kEmpty;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (a[u] == kEmpty) continue;
-      if (a[u] >= range) atomicAdd(err, 1ull);
-      else atomicAdd(&hsm[a[u]], 1u);
+      for (int u = 0; u < 4; ++u) {
+        if (a[u] == kEmpty) continue;
+        if (a[u] >= range) atomicAdd(err, 1ull);
+        else atomicAdd(&hsm[a[u]], 1u);
+      }
     }
-  }
-  __syncthreads();
-  uint32_t* hb = hbuf + (uint64_t)blockIdx.x * range;
-  uint32_t* cur = cursor + (uint64_t)(t0 + j) * range;
-  for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
-    const uint32_t v = hsm[b];
-    hb[b] = v;
-    if (v) atomicAdd(&cur[b], v);
+    __syncthreads();
+    uint32_t* hb = hbuf + (b + j) * range;
+    uint32_t* cur = cursor + (uint64_t)(t0 + j) * range;
+    for (uint32_t bb = threadIdx.x; bb < range; bb += blockDim.x) {
+      const uint32_t v = hsm[bb];
+      hb[bb] = v;
+      if (v) atomicAdd(&cur[bb], v);
+    }
+    __syncthreads();
   }
 }
 
-// Each slice's first pool position in every bucket of its table, relative to the table's pool
-// start: the bucket's offset, then its old kept ids (their count is in cursor after
-// k_pool_sizes), then the earlier slices' arrivals — an exclusive scan over the slices,
-// written over the slice histograms.
-__global__ void k_slice_bases(uint32_t W, uint32_t t0, uint32_t range, uint32_t S,
+// Each segment's first pool position in every bucket of its table, relative to the table's
+// pool start: the bucket's offset, then its old kept ids (their count is in cursor after
+// k_pool_sizes), then the earlier segments' arrivals — an exclusive scan over the table's
+// segments, written over the segment histograms.
+__global__ void k_slice_bases(uint32_t W, uint32_t t0, uint32_t range, uint64_t n, uint32_t C,
                               const uint32_t* __restrict__ cursor, const uint64_t* __restrict__ pool_off,
                               uint32_t* __restrict__ hbuf) {
-  const uint64_t total = (uint64_t)W * range;
+  const uint64_t total = (uint64_t)W * range, U = (uint64_t)W * n;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t j = (uint32_t)(x / range), b = (uint32_t)(x - (uint64_t)j * range);
     const uint64_t tb = (uint64_t)(t0 + j) * range;
+    const uint64_t s0 = cta_of_unit((uint64_t)j * n, U, C) + j, s1 = cta_of_unit((uint64_t)(j + 1) * n - 1, U, C) + j + 1;
     uint32_t run = (uint32_t)(pool_off[tb + b] - pool_off[tb]) + cursor[tb + b];
-    uint32_t* h = hbuf + (uint64_t)j * S * range + b;
-    for (uint32_t c0 = 0; c0 < S; c0 += 8) {  // 8 independent loads in flight
+    uint32_t* h = hbuf + b;
+    for (uint64_t c0 = s0; c0 < s1; c0 += 8) {  // 8 independent loads in flight
       uint32_t v[8];
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) v[u] = c0 + u < S ? h[(uint64_t)(c0 + u) * range] : 0u;
+      for (uint32_t u = 0; u < 8; ++u) v[u] = c0 + u < s1 ? h[(c0 + u) * range] : 0u;
 #pragma unroll
       for (uint32_t u = 0; u < 8; ++u) {
-        if (c0 + u < S) h[(uint64_t)(c0 + u) * range] = run;
+        if (c0 + u < s1) h[(c0 + u) * range] = run;
         run += v[u];
       }
     }
@@ -270,57 +286,65 @@ __global__ void k_slice_bases(uint32_t W, uint32_t t0, uint32_t range, uint32_t 
 }
 
 __global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t* __restrict__ addrsT, uint64_t n,
-                                                                 uint32_t t0, uint32_t range, uint32_t S,
+                                                                 uint32_t t0, uint32_t range, uint32_t W, uint32_t C,
                                                                  uint32_t id_base, const uint32_t* __restrict__ cursor,
                                                                  const uint32_t* __restrict__ hbuf,
                                                                  const uint64_t* __restrict__ pool_off,
                                                                  uint32_t* __restrict__ pool, int prefixed) {
-  // [range] this slice's next pool position in each bucket, relative to the table's pool start
-  // (a table's pool holds < 2^32 entries: its rows' arrivals plus its old kept ids)
+  // [range] this segment's next pool position in each bucket, relative to the table's pool
+  // start (a table's pool holds < 2^32 entries: its rows' arrivals plus its old kept ids)
   extern __shared__ uint32_t csm[];
-  const uint32_t j = blockIdx.x / S, c = blockIdx.x - j * S;
-  const uint64_t r0 = n * c / S, r1 = n * (c + 1) / S;
-  const uint64_t tb = (uint64_t)(t0 + j) * range;
-  const uint64_t pbase = pool_off[tb];
-  const uint32_t* col = addrsT + (uint64_t)j * n;
-  if (prefixed) {  // k_slice_bases turned the slice histograms into each slice's first positions
-    for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) csm[b] = hbuf[(uint64_t)(j * S + c) * range + b];
-  } else {  // few slices: the same scan, here
-    for (uint32_t b = threadIdx.x; b < range; b += blockDim.x) {
-      // the bucket's old kept ids come first (k_pool_sizes left their count in cursor)
-      uint32_t base = (uint32_t)(pool_off[tb + b] - pbase) + cursor[tb + b];
-      for (uint32_t c2 = 0; c2 < c; ++c2) base += hbuf[(uint64_t)(j * S + c2) * range + b];
-      csm[b] = base;
-    }
-  }
-  __syncthreads();
-  // Rows go in chunks of blockDim with a barrier between chunks, so a bucket's entries from
-  // different chunks land in row (= id) order; only rows of one chunk that share a bucket
-  // (rare: ~blockDim^2 / 2range pairs per chunk) may land out of order.  k_select_small
-  // then finds most buckets already ascending and skips their sort.  The next chunks'
-  // addresses are loaded ahead (4 chunks in flight).
-  uint32_t* tpool = pool + pbase;
+  const uint64_t U = (uint64_t)W * n, cb = blockIdx.x;
+  const uint64_t u0 = cb * U / C, u1 = (cb + 1) * U / C;
+  if (u0 >= u1) return;
   const uint32_t bd = blockDim.x;
-  uint32_t a[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint64_t r = r0 + threadIdx.x + (uint64_t)u * bd;
-    a[u] = r < r1 ? col[r] : kEmpty;
-  }
-  for (uint64_t base = r0; base < r1; base += 4ull * bd) {
-    uint32_t nx[4];
+  for (uint32_t j = (uint32_t)(u0 / n); j <= (uint32_t)((u1 - 1) / n); ++j) {
+    const uint64_t r0 = max(u0, (uint64_t)j * n) - (uint64_t)j * n;
+    const uint64_t r1 = min(u1, (uint64_t)(j + 1) * n) - (uint64_t)j * n;
+    const uint64_t tb = (uint64_t)(t0 + j) * range;
+    const uint64_t pbase = pool_off[tb];
+    const uint32_t* col = addrsT + (uint64_t)j * n;
+    const uint64_t slot = cb + j;
+    if (prefixed) {  // k_slice_bases turned the segment histograms into first positions
+      for (uint32_t b = threadIdx.x; b < range; b += bd) csm[b] = hbuf[slot * range + b];
+    } else {  // few segments per table: the same scan, here
+      const uint64_t s0 = cta_of_unit((uint64_t)j * n, U, C) + j;
+      for (uint32_t b = threadIdx.x; b < range; b += bd) {
+        // the bucket's old kept ids come first (k_pool_sizes left their count in cursor)
+        uint32_t base = (uint32_t)(pool_off[tb + b] - pbase) + cursor[tb + b];
+        for (uint64_t s2 = s0; s2 < slot; ++s2) base += hbuf[s2 * range + b];
+        csm[b] = base;
+      }
+    }
+    __syncthreads();
+    // Rows go in chunks of blockDim with a barrier between chunks, so a bucket's entries from
+    // different chunks land in row (= id) order; only rows of one chunk that share a bucket
+    // (rare: ~blockDim^2 / 2range pairs per chunk) may land out of order.  k_select_small
+    // then finds most buckets already ascending.  The next chunks' addresses are loaded
+    // ahead (4 chunks in flight).
+    uint32_t* tpool = pool + pbase;
+    uint32_t a[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint64_t r = base + 4ull * bd + threadIdx.x + (uint64_t)u * bd;
-      nx[u] = r < r1 ? col[r] : kEmpty;
+      const uint64_t r = r0 + threadIdx.x + (uint64_t)u * bd;
+      a[u] = r < r1 ? col[r] : kEmpty;
     }
+    for (uint64_t base = r0; base < r1; base += 4ull * bd) {
+      uint32_t nx[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (a[u] < range) tpool[atomicAdd(&csm[a[u]], 1u)] = id_base + (uint32_t)(base + threadIdx.x + (uint64_t)u * bd);
-      __syncthreads();
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t r = base + 4ull * bd + threadIdx.x + (uint64_t)u * bd;
+        nx[u] = r < r1 ? col[r] : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (a[u] < range)
+          tpool[atomicAdd(&csm[a[u]], 1u)] = id_base + (uint32_t)(base + threadIdx.x + (uint64_t)u * bd);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = nx[u];
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = nx[u];
   }
 }
 
@@ -858,18 +882,26 @@ k_select_big(uint32_t range, uint32_t R, HashKeys keys, int exact_only, const ui
 
 }  // namespace
 
-uint32_t smem_build_slices(uint32_t W, uint64_t n) {
-  // S row slices per table: about one wave of 1024-thread CTAs (one per SM) when every
-  // table's pool region (4 B per row) fits L2 together; otherwise enough slices that the
-  // CTAs resident at once cover only the few tables whose regions fit ~96 MB of L2, so
-  // the scattered pool writes stay in L2 (the grid is table-major)
+uint32_t smem_build_ctas(uint32_t W, uint64_t n) {
+  // CTAs over the W*n (table, row) units: one per SM (or one per table if W is larger)
+  // when every table's pool region (4 B per row) fits L2 together; otherwise S equal row
+  // slices per table, S large enough that the CTAs resident at once cover only the few
+  // tables whose regions fit ~96 MB of L2, so the scattered pool writes stay in L2 (the
+  // units are table-major)
   const uint32_t sms = device_sms();
   const uint64_t region = 4 * (n ? n : 1);
   uint64_t tc = (96ull << 20) / region;  // tables whose regions fit L2 at once
   if (tc < 1) tc = 1;
-  uint64_t s = W ? sms / W : 1u;
-  if (tc < W) s = (sms + tc - 1) / tc;
-  return (uint32_t)(s < 1 ? 1 : (s > 64 ? 64 : s));
+  uint64_t c;
+  if (tc >= W) {
+    c = W > sms ? W : sms;
+  } else {
+    uint64_t s = (sms + tc - 1) / tc;
+    c = (uint64_t)W * (s < 1 ? 1 : (s > 64 ? 64 : s));
+  }
+  // every CTA must own at least one unit (an empty one would leave its hbuf slot unwritten)
+  const uint64_t units = (uint64_t)W * (n ? n : 1);
+  return (uint32_t)(c < units ? c : units);
 }
 
 bool smem_build_fits(uint32_t range) { return range <= kSmemBuildMaxRange; }
@@ -903,13 +935,13 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const bool sm_build = a.hbuf != nullptr && a.addrsT != nullptr && a.n && W && !a.shared;  // k_count_smem
   const bool tm = !sm_build && a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (k_count_tm)
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
-  const uint32_t S = smem_build_slices(W, a.n);
+  const uint32_t C = smem_build_ctas(W, a.n);
   if (sm_build) {
     ensure_smem_attr((const void*)k_count_smem, (size_t)kSmemBuildMaxRange * 4);
     ensure_smem_attr((const void*)k_fill_smem, (size_t)kSmemBuildMaxRange * 4);
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
-    k_count_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.cursor,
+    k_count_smem<<<C, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, W, C, a.cursor,
                                                                       a.hbuf, a.err);
     launches += 2;
   } else if (tm) {
@@ -936,15 +968,15 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     launches++;
   }
   if (sm_build) {
-    const bool prefixed = S > 4;  // many slices: scan them once up front
+    const bool prefixed = C > 4 * W;  // many segments per table: scan them once up front
     if (prefixed) {
       const uint64_t sb = ((uint64_t)W * a.range + 255) / 256;
       k_slice_bases<<<(unsigned)(sb < (uint64_t)device_sms() * 16 ? sb : (uint64_t)device_sms() * 16), 256, 0,
-                      s>>>(W, a.t0, a.range, S, a.cursor, a.pool_off, a.hbuf);
+                      s>>>(W, a.t0, a.range, a.n, C, a.cursor, a.pool_off, a.hbuf);
       launches++;
     }
-    k_fill_smem<<<W * S, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, S, a.id_base,
-                                                                     a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
+    k_fill_smem<<<C, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, W, C, a.id_base,
+                                                                 a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
     launches++;
   } else if (tm) {
     k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,

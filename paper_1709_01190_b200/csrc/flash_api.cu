@@ -235,7 +235,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
                    !(sm_env && sm_env[0] == '0');
   if ((tm || smb) && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
   if (smb)
-    TRY(ensure(h->hbuf, sizeof(uint32_t) * (size_t)(t1 - t0) * smem_build_slices(t1 - t0, n) * h->range));
+    TRY(ensure(h->hbuf, sizeof(uint32_t) * ((size_t)(t1 - t0) + smem_build_ctas(t1 - t0, n)) * h->range));
 
   Phase ph(h, 1, s);
   BuildArgs a;

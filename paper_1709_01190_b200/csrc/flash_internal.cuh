@@ -101,7 +101,7 @@ struct BuildArgs {
   const uint32_t* addrs;  // row r, table t at addrs[r*astride + t - acol0]
   uint32_t astride, acol0;  // [n][L]: L, 0; a column window [n][t1-t0]: t1-t0, t0
   uint32_t* addrsT;         // scratch [t1-t0][n] for the table-major / shared-memory passes, or null
-  uint32_t* hbuf;           // scratch [t1-t0][S][range] slice histograms: shared-memory passes, or null
+  uint32_t* hbuf;           // scratch [C + (t1-t0)][range] segment histograms: shared-memory passes, or null
   uint32_t shared;          // 0: bucket (t, a) is t*range + a; else addrs hold shared-reservoir
                             // indices < shared (k_shared_reservoirs output) used as the bucket
   uint64_t n;
@@ -128,7 +128,7 @@ struct BuildArgs {
   size_t scan_tmp_bytes;
 };
 size_t build_scan_tmp_bytes(uint64_t nb);
-uint32_t smem_build_slices(uint32_t W, uint64_t n);  // row slices per table (shared-memory passes)
+uint32_t smem_build_ctas(uint32_t W, uint64_t n);  // CTAs of the shared-memory passes (hbuf: (C + W) slots)
 bool smem_build_fits(uint32_t range);
 int launch_build(const BuildArgs& a, cudaStream_t s);
 
