@@ -502,7 +502,7 @@ int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, c
   if (mcap <= 768) return launch_sort_t<768, 10>(a, list, count, s);
   if (mcap <= 1024) return launch_sort_t<1024, 10>(a, list, count, s);
   if (mcap <= 1280) return launch_sort_t<1280, 10>(a, list, count, s);
-  if (mcap <= 1536) return launch_sort_t<1536, 11>(a, list, count, s);
+  if (mcap <= 1536) return launch_sort_t<1536, 10>(a, list, count, s);
   if (mcap <= 2048) return launch_sort_t<2048, 11>(a, list, count, s);
   return launch_sort_t<3072, 11>(a, list, count, s);
 }
