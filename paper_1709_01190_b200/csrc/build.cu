@@ -348,9 +348,13 @@ __global__ void __launch_bounds__(kSmemBuildThreads) k_fill_smem(const uint32_t*
   }
 }
 
+// Per bucket: pool size m (old kept ids + new arrivals) and kept count; buckets with
+// m > early_min go to early_list (their k_select_big can start as soon as the pool is filled).
 __global__ void k_pool_sizes(uint32_t nb, uint32_t R, const uint64_t* __restrict__ goff_old,
                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ arrivals,
-                             uint64_t* __restrict__ pool_cnt, uint64_t* __restrict__ keep_cnt) {
+                             uint64_t* __restrict__ pool_cnt, uint64_t* __restrict__ keep_cnt,
+                             uint64_t early_min, uint32_t* __restrict__ early_list,
+                             uint32_t* __restrict__ early_count) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= nb; i += gridDim.x * blockDim.x) {
     if (i == nb) { pool_cnt[nb] = 0; keep_cnt[nb] = 0; continue; }
     const uint64_t old = goff_old ? goff_old[i + 1] - goff_old[i] : 0;
@@ -360,6 +364,7 @@ __global__ void k_pool_sizes(uint32_t nb, uint32_t R, const uint64_t* __restrict
     pool_cnt[i] = m;
     keep_cnt[i] = m < R ? m : R;
     cursor[i] = (uint32_t)old;
+    if (m > early_min) early_list[atomicAdd(early_count, 1u)] = i;
   }
 }
 
@@ -464,7 +469,7 @@ __device__ __forceinline__ void insertion_sort(uint32_t* buf, uint32_t s0, uint3
 }
 
 __global__ void __launch_bounds__(256)
-k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big,
+k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force_big, int early_listed,
                const uint64_t* __restrict__ pool_off, const uint32_t* __restrict__ pool,
                const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out,
                uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
@@ -509,7 +514,9 @@ k_select_small(uint32_t nb, uint32_t range, uint32_t R, HashKeys keys, int force
         for (uint32_t e = 0; e < ps; ++e) ids_out[go + e] = buf[so + e];
       }
       if (i < nb && m > 32) {  // > kWarpMax members: the CTA path streams them with 1024 threads
-        if (force_big || m > kWarpMax) big_list[atomicAdd(big_count, 1u)] = i;
+        if (force_big || m > kWarpMax) {
+          if (!early_listed) big_list[atomicAdd(big_count, 1u)] = i;  // else k_pool_sizes listed it
+        }
         else if (m <= kMidMax && R <= kMidMax) reg_list[atomicAdd(reg_count, 1u)] = i;
         else mid_list[atomicAdd(mid_count, 1u)] = i;
       }
@@ -930,7 +937,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const unsigned rows_blocks = (unsigned)((a.n + 7) / 8 < (uint64_t)device_sms() * 32 ? (a.n + 7) / 8 : (uint64_t)device_sms() * 32);
   const unsigned nb_blocks = (unsigned)(((uint64_t)nb + 256) / 256 < (uint64_t)device_sms() * 32 ? ((uint64_t)nb + 256) / 256 : (uint64_t)device_sms() * 32);
   cudaMemsetAsync(a.cursor, 0, sizeof(uint32_t) * (size_t)nb, s);
-  cudaMemsetAsync(a.big_count, 0, 3 * sizeof(uint32_t), s);  // big, mid, register-path list counters
+  cudaMemsetAsync(a.big_count, 0, 4 * sizeof(uint32_t), s);  // big, mid, register-path, early list counters
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
   const bool sm_build = a.hbuf != nullptr && a.addrsT != nullptr && a.n && W && !a.shared;  // k_count_smem
   const bool tm = !sm_build && a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (k_count_tm)
@@ -955,7 +962,15 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                         a.err);
     launches++;
   }
-  k_pool_sizes<<<nb_blocks, 256, 0, s>>>(nb, a.R, a.goff_old, a.cursor, a.arrivals, a.pool_cnt, a.keep_cnt);
+  // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
+  // =2: and the CTA path skips its filter (exact radix select).  Tests only.
+  const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");
+  const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
+  // buckets with > kWarpMax members are listed here and selected on the side stream
+  const bool early = a.early_list && a.side_stream && !force_big;
+  uint32_t* early_count = a.big_count + 3;
+  k_pool_sizes<<<nb_blocks, 256, 0, s>>>(nb, a.R, a.goff_old, a.cursor, a.arrivals, a.pool_cnt, a.keep_cnt,
+                                         early ? (uint64_t)kWarpMax : ~0ull, a.early_list, early_count);
   launches++;
   size_t tmp = a.scan_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.pool_cnt, a.pool_off, (int64_t)nb + 1, s);
@@ -989,17 +1004,22 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   }
   const size_t sel_smem = (size_t)(kSelThreads / 32) * kWarpCap * sizeof(uint64_t);
   ensure_smem_attr((const void*)k_select_warp, sel_smem);
-  // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
-  // =2: and the CTA path skips its filter (exact radix select).  Tests only.
-  const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");
-  const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
+  if (early) {  // the early-listed big buckets, concurrently with the kernels below
+    cudaStream_t side = static_cast<cudaStream_t>(a.side_stream);
+    cudaEventRecord(static_cast<cudaEvent_t>(a.side_fork), s);
+    cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(a.side_fork), 0);
+    k_select_big<<<device_sms(), kBigThreads, 0, side>>>(a.range, a.R, a.keys, 0, a.pool_off, a.pool, a.goff_new,
+                                                        a.ids_new, a.early_list, early_count);
+    cudaEventRecord(static_cast<cudaEvent_t>(a.side_join), side);
+    launches += 1;
+  }
   uint32_t* mid_list = a.cursor;  // free once k_fill_new is done
   uint32_t* mid_count = a.big_count + 1;
   uint32_t* reg_list = reinterpret_cast<uint32_t*>(a.pool_cnt);  // free once pool_off is scanned
   uint32_t* reg_count = a.big_count + 2;
   const uint64_t small_warps = ((uint64_t)nb + kSmallChunk - 1) / kSmallChunk;  // 32 buckets per warp step
   const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < (uint64_t)device_sms() * 64 ? (small_warps + 7) / 8 : (uint64_t)device_sms() * 64);
-  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, a.pool_off, a.pool, a.goff_new,
+  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, early, a.pool_off, a.pool, a.goff_new,
                                              a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
                                              a.big_count);
   k_select_mid<<<device_sms() * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, a.pool, a.goff_new,
@@ -1009,8 +1029,9 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                                       a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;
   k_select_big<<<device_sms(), kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
-                                              a.ids_new, a.big_list, a.big_count);
+                                              a.ids_new, a.big_list, a.big_count);  // the late list
   launches += 1;
+  if (early) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.side_join), 0);
   return launches;
 }
 

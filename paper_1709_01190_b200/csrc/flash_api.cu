@@ -115,6 +115,8 @@ struct flash_index {
   cudaEvent_t order_ev = nullptr;
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> copy_events;
+  cudaStream_t side_stream = nullptr;  // build: k_select_big of the early-listed buckets
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
 
   // profiling
   int profiling = 0;
@@ -218,7 +220,12 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
   TRY(ensure(h->pool, sizeof(uint32_t) * pool_cap));
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * kept_cap));
-  TRY(ensure(h->big_list, sizeof(uint32_t) * (nb + 3)));
+  TRY(ensure(h->big_list, sizeof(uint32_t) * (2 * nb + 4)));  // late list, 4 counters, early list
+  if (!h->side_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->side_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->side_join, cudaEventDisableTiming));
+  }
   TRY(ensure(h->scan_tmp, build_scan_tmp_bytes(nb)));
   // Table-major passes once the per-bucket arrays (cursor + pool offset, 12 B per bucket)
   // no longer fit comfortably in L2 and each table has enough buckets that the resident
@@ -267,6 +274,10 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.ids_new = h->ids[nxt].as<uint32_t>();
   a.big_list = h->big_list.as<uint32_t>();
   a.big_count = h->big_list.as<uint32_t>() + nb;
+  a.early_list = h->big_list.as<uint32_t>() + nb + 4;
+  a.side_stream = h->side_stream;
+  a.side_fork = h->side_fork;
+  a.side_join = h->side_join;
   a.scan_tmp = h->scan_tmp.p;
   a.scan_tmp_bytes = h->scan_tmp.cap;
   h->launches += launch_build(a, s);
@@ -410,6 +421,9 @@ void flash_destroy(flash_index* h) {
   for (auto e : h->copy_events) cudaEventDestroy(e);
 
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  if (h->side_fork) cudaEventDestroy(h->side_fork);
+  if (h->side_join) cudaEventDestroy(h->side_join);
   cudaFree(h->arrivals);
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,

@@ -122,7 +122,11 @@ struct BuildArgs {
   uint32_t* pool;             // [pool capacity]
   uint32_t* ids_new;          // [kept capacity]
   uint32_t* big_list;         // [nb] bucket indices for the CTA path
-  uint32_t* big_count;        // [2]: CTA-path list count, warp-path (mid) list count
+  uint32_t* big_count;        // [4]: CTA-path, warp-path (mid), register-path and early list counts
+  uint32_t* early_list;       // [nb] buckets with > 512 members, listed by k_pool_sizes, or null
+  void* side_stream;          // with early_list: k_select_big runs these on this stream,
+  void* side_fork;            //   concurrently with the other select kernels (events fork /
+  void* side_join;            //   join it with the caller's stream)
   unsigned long long* err;    // device error counter
   void* scan_tmp;
   size_t scan_tmp_bytes;
