@@ -16,7 +16,8 @@ CASES = [("tiny", 1000, (4, 16, 32, 1 << 15, 10), "0"),
          ("url", 3000, (4, 128, 32, 1 << 10, 128), "0"),
          ("url", 3000, (4, 64, 128, 1 << 6, 300), "1"),
          ("kdd12", 6000, (4, 32, 64, 1 << 7, 64), "1"),   # sparse DOPH, 33..256-member buckets
-         ("tiny", 4000, (2, 4, 16, 64, 20), "0")]          # register-path select, m > R
+         ("tiny", 4000, (2, 4, 16, 64, 20), "0"),          # register-path select, m > R
+         ("tiny", 3000, (4, 8, 64, 4, 10), "0")]           # > 512 members: early list, side stream
 
 for name, n, (K, L, R, rng, k), tm in CASES:
     os.environ["FLASH_BUILD_TM"] = tm
