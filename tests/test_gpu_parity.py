@@ -145,6 +145,30 @@ def test_tables_bit_exact(monkeypatch, name, make, K, L, R, rng, sched):
         assert idx.errors() == 0
 
 
+@pytest.mark.parametrize("n,K,L,R,rng", [(300, 1, 300, 8, 64),    # more tables than SMs: one CTA per table
+                                         (3, 1, 160, 4, 16),      # W*n = 480 units over 160 CTAs
+                                         (1, 2, 160, 4, 16),      # one unit (row) per CTA
+                                         (5000, 4, 3, 16, 64),    # 148 CTAs, segments span tables
+                                         (2000, 2, 8, 64, 4)])    # > 512-member buckets: side stream
+def test_smem_build_cta_mappings(monkeypatch, n, K, L, R, rng):
+    """The shared-memory passes cut the W*n (table, row) units into equal CTA ranges whose
+    segments may span tables; tables must not depend on where the cuts fall."""
+    monkeypatch.setenv("FLASH_BUILD_TM", "0")
+    monkeypatch.setenv("FLASH_BUILD_SMEM", "1")
+    rp, col = synth.generate(synth.SHAPES["tiny"].with_(N=n, seed=n + L))
+    seed = 0xC7A + L
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    T = oracle.build(L, R, rng, seed, addrs, np.arange(n, dtype=np.uint32))
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert(d_rp, d_col, 0)
+        _check_tables(idx, T)
+        idx.insert(d_rp, d_col, n)  # a second batch: old kept ids first in every pool
+        T2 = oracle.build(L, R, rng, seed, np.concatenate([addrs, addrs]), np.arange(2 * n, dtype=np.uint32))
+        _check_tables(idx, T2)
+        assert idx.errors() == 0
+
+
 @pytest.mark.parametrize("mode", ["1", "2"])
 def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch, mode):
     """FLASH_DEBUG_FORCE_BIG=1 routes every bucket with > 32 members through the CTA
