@@ -130,6 +130,24 @@ class OracleIndex:
         return torch.from_numpy(ids.view(np.int32)), torch.from_numpy(cnt.view(np.int32))
 
 
+class OraclePoolIndex(OracleIndex):
+    """Reservoir sharing (F < 1, R#23) stand-in: the replicated schedule needs only
+    hash / insert / query, which the pool oracle provides."""
+    def __init__(self, K, L, R, range_, seed, F):
+        super().__init__(K, L, R, range_, seed)
+        self.P = oracle.pool_size(F, L, range_)
+
+    def insert_addrs(self, addrs, id_base):
+        a = addrs.numpy().view(np.uint32)
+        ids = (np.arange(a.shape[0], dtype=np.int64) + id_base).astype(np.uint32)
+        self.T = oracle.build_pool(self.L, self.R, self.range, self.P, self.seed, a, ids)
+
+    def query_addrs(self, addrs, k, exclude):
+        ids, cnt = oracle.query_pool(self.T, self.seed, addrs.numpy().view(np.uint32), k,
+                                     exclude=exclude.numpy().astype(np.int64).astype(np.uint32))
+        return torch.from_numpy(ids.view(np.int32)), torch.from_numpy(cnt.view(np.int32))
+
+
 def _shape():
     return synth.SHAPES["tiny"].with_(N=700, seed=11)
 
@@ -143,9 +161,12 @@ def _worker(rank, world, port, out_dir, mode="replicated"):
         lens = np.diff(synth.generate(shape)[0])
         bounds = fdist.shard_bounds(lens, world)
         rp, col = synth.generate(shape, rows=(bounds[rank], bounds[rank + 1]))
-        idx = OracleIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"])
+        if mode == "replicated_pool":
+            idx = OraclePoolIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"], POOL_F)
+        else:
+            idx = OracleIndex(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"])
         fn = {"replicated": fdist.knn_graph_replicated, "sharded": fdist.knn_graph_sharded_build,
-              "exchange": fdist.knn_graph_candidate_exchange}[mode]
+              "exchange": fdist.knn_graph_candidate_exchange, "replicated_pool": fdist.knn_graph_replicated}[mode]
         ids, cnt = fn(idx, torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)), CFG["k"], bounds, rank)
         np.save(os.path.join(out_dir, f"ids_{rank}.npy"), ids.numpy())
         np.save(os.path.join(out_dir, f"cnt_{rank}.npy"), cnt.numpy())
@@ -167,6 +188,27 @@ def test_distributed_graph_equals_single_process(tmp_path, world, mode):
     rp, col = synth.generate(shape)
     want_ids, want_cnt = oracle.knn_graph(CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"], rp, col,
                                           CFG["k"])
+    got_ids = np.concatenate([np.load(tmp_path / f"ids_{r}.npy") for r in range(world)]).view(np.uint32)
+    got_cnt = np.concatenate([np.load(tmp_path / f"cnt_{r}.npy") for r in range(world)]).view(np.uint32)
+    assert np.array_equal(got_ids, want_ids)
+    assert np.array_equal(got_cnt, want_cnt)
+
+
+POOL_F = 0.2
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_graph_with_reservoir_sharing_equals_single_process(tmp_path, world):
+    """F < 1 (reservoir sharing, R#23) across processes: the replicated schedule (every rank
+    builds the same shared-pool tables from the all-gathered addresses) must give the
+    single-process pool graph row for row."""
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), "replicated_pool"), nprocs=world, join=True)
+    rp, col = synth.generate(_shape())
+    K, L, R, rng, seed, k = CFG["K"], CFG["L"], CFG["R"], CFG["range_"], CFG["seed"], CFG["k"]
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    n = addrs.shape[0]
+    T = oracle.build_pool(L, R, rng, oracle.pool_size(POOL_F, L, rng), seed, addrs, np.arange(n, dtype=np.uint32))
+    want_ids, want_cnt = oracle.query_pool(T, seed, addrs, k, exclude=np.arange(n, dtype=np.uint32))
     got_ids = np.concatenate([np.load(tmp_path / f"ids_{r}.npy") for r in range(world)]).view(np.uint32)
     got_cnt = np.concatenate([np.load(tmp_path / f"cnt_{r}.npy") for r in range(world)]).view(np.uint32)
     assert np.array_equal(got_ids, want_ids)
