@@ -528,7 +528,11 @@ SHAPE_CFG = {
     "kdd12": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0004, k=128, q=10_000, qseed=14),
     # the friendster 20-NN graph from scratch (the paper
     # gives no K/L/R for it: kdd12's K=4, L=32, R=64, 2^20 for a dataset of that scale)
-    "friendster": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0005, k=20, graph=True),
+    "friendster": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0005, k=20, graph=True,
+                       paper="friendster 20-NN graph from scratch: 1578 s on 2x Xeon E5-2660 v4, 56 threads (P:505)"),
+    # the 10 K-query url line is latency-scale, so also the full url graph
+    # (Q = N = 2.39 M queries, ~L*R = 4096 candidates each: the CTA-per-query class)
+    "url-graph": dict(shape="url", K=4, L=128, R=32, range_=1 << 15, seed=0x5EED0003, k=128, graph=True),
 }
 
 
@@ -623,13 +627,13 @@ def run_shape_graph(args, cfg, shape):
                           "peak_kind": peak_kind, "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
                           "algorithmic_bytes": hash_bytes},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": f"synthetic (synth/, {args.workload} shape, seed {shape.seed})",
-        "config": {"workload": f"{args.workload}-shaped approximate {k}-NN graph from scratch",
+        "data": f"synthetic (synth/, {shape.name} shape, seed {shape.seed})",
+        "config": {"workload": f"{shape.name}-shaped approximate {k}-NN graph from scratch",
                    "N": shape.N, "D": shape.D, "nnz": nnz, "nnz_per_row": round(nnz / shape.N, 1),
                    "K": cfg["K"], "L": cfg["L"], "R": cfg["R"], "range": cfg["range_"], "k": k,
                    "seed": cfg["seed"], "parallelism": "1 GPU",
                    "l2_policy": f"inputs larger than L2 (col_idx {4 * nnz / 1e9:.1f} GB vs 126 MB L2); no flush"},
-        "paper": "friendster 20-NN graph from scratch: 1578 s on 2x Xeon E5-2660 v4, 56 threads (P:505)",
+        "paper": cfg.get("paper"),
         "gpu_launches": launches, "clocks": clk.summary(),
         "data_stats": {"nnz_mean": float(lens.mean()), "nnz_p99": float(np.percentile(lens, 99)),
                        "nnz_max": int(lens.max())},
@@ -647,7 +651,7 @@ def run_shape(args):
     rank, world, local = dist_env()
     assert world == 1, "--workload url/kdd12 runs on one GPU"
     cfg = SHAPE_CFG[args.workload]
-    shape = synth.SHAPES[args.workload]
+    shape = synth.SHAPES[cfg.get("shape", args.workload)]
     if cfg.get("graph"):
         return run_shape_graph(args, cfg, shape)
     torch.cuda.set_device(local)
@@ -794,8 +798,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
     ap.add_argument("--quality-queries", type=int, default=1000)
-    ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster"], default="webspam",
-                    help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines")
+    ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster", "url-graph"], default="webspam",
+                    help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines; "
+                         "friendster / url-graph = full k-NN graphs of those shapes")
     args = ap.parse_args()
     if args.workload != "webspam" and args.impl == "ours":
         print(json.dumps(run_shape(args)), flush=True)

@@ -41,14 +41,14 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
 // Query size classes by M (candidates): the first kSortClasses run one query per warp
 // (query_sort.cu; a smaller class uses less shared memory per warp, so more warps per
 // SM); M <= 4096 and <= 8192 run one query per CTA with 2^13 / 2^14 count slots (below).
-constexpr int kSortClasses = 6;
+constexpr int kSortClasses = 7;
 __host__ __device__ constexpr uint32_t class_max(int c) {
   return c == 0 ? 768u : c == 1 ? 1024u : c == 2 ? 1280u : c == 3 ? 1536u : c == 4 ? 2048u
          : c == 5 ? 3072u : c == 6 ? 4096u : c == 7 ? 8192u : 32768u;
 }
 // the last class (M <= 32768, indexes with L*R > 8192) keeps its count table of 2^16 slots
 // in a per-CTA region of global memory (L2-resident), since it exceeds shared memory
-constexpr int kClasses = kSortClasses + 3;
+constexpr int kClasses = kSortClasses + 2;
 constexpr uint32_t kHugeLog2 = 16;
 constexpr uint32_t kHugeCtas = 148;
 
@@ -589,8 +589,7 @@ int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
     const uint32_t* lc = lists + (uint64_t)c * a.nq;
     if (c < kSortClasses) n += launch_query_sort(a, class_max(c), lc, counts + c, s);
-    else if (c == kSortClasses) n += launch_class<13, 256, false>(a, lc, counts + c, hist_len, nullptr, s);
-    else if (c == kSortClasses + 1) n += launch_class<14, 256, false>(a, lc, counts + c, hist_len, nullptr, s);
+    else if (c == kSortClasses) n += launch_class<14, 256, false>(a, lc, counts + c, hist_len, nullptr, s);
     else n += launch_class<kHugeLog2, 256, true>(a, lc, counts + c, hist_len, huge_tab, s);
   }
   return n;

@@ -504,7 +504,8 @@ int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, c
   if (mcap <= 1280) return launch_sort_t<1280, 10>(a, list, count, s);
   if (mcap <= 1536) return launch_sort_t<1536, 10>(a, list, count, s);
   if (mcap <= 2048) return launch_sort_t<2048, 11>(a, list, count, s);
-  return launch_sort_t<3072, 11>(a, list, count, s);
+  if (mcap <= 3072) return launch_sort_t<3072, 11>(a, list, count, s);
+  return launch_sort_t<4096, 11>(a, list, count, s);
 }
 
 }  // namespace flash

@@ -30,5 +30,6 @@ timeout 600 python bench.py > "$OUT/${TAG}_bench.json" 2> "$OUT/bench.log"
 timeout 600 python bench.py --workload url --steps 3 --warmup 3 > "$OUT/${TAG}_bench_url.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --workload kdd12 --steps 3 --warmup 3 > "$OUT/${TAG}_bench_kdd12.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --workload friendster --steps 3 --warmup 3 > "$OUT/${TAG}_bench_friendster.json" 2>> "$OUT/bench.log"
+timeout 900 python bench.py --workload url-graph --steps 3 --warmup 3 > "$OUT/${TAG}_bench_url_graph.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/${TAG}_bench_reference.json" 2>> "$OUT/bench.log"
 ls -la "$OUT"
