@@ -450,7 +450,7 @@ def run_ours(args):
             q_traffic = sum(traffic.get(nm, 0.0) for nm in ("k_query_plan", "k_query_sort", "k_query"))
         if dominant == "query" and n_cand is not None:
             # the count kernel is bound by per-candidate shared-memory work, not by HBM
-            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query for M > 3072)",
+            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query for M > 4096)",
                     "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
                     "peak": SMEM_RMW_PEAK, "unit": "candidate-updates/s", "peak_kind": "measured (smem RMW microbench)",
                     "traffic": q_traffic, "candidates": n_cand,

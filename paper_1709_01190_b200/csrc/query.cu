@@ -1,9 +1,10 @@
 // query.cu — Q1-Q3: the querying phase (Alg. 3) on sm_100a.
 //
 // k_query_plan: one lane per query sums the sizes M of its L addressed buckets and
-//   files the query into a size class: M <= 1024 / 1536 / 3072 go to the warp-per-query
-//   radix-partition kernel (query_sort.cu), larger M to the CTA kernel below (count
-//   table of 2^13 / 2^14 slots, load factor <= 1/2).
+//   files the query into a size class: M <= 768 / 1024 / 1280 / 1536 / 2048 / 3072 / 4096
+//   go to the warp-per-query radix-partition kernel (query_sort.cu), larger M to the CTA
+//   kernel below (count table of 2^14 slots, load factor <= 1/2; 2^16 slots in global
+//   memory above 8192).
 // k_query<LOG2S, NT>: one CTA owns one query at a time (persistent over its class list):
 //   Q1 gather   warp 0 scans the L bucket sizes into prefix offsets; each warp then walks
 //               its own contiguous chunk of the flattened candidate positions p (4 loads in
@@ -40,7 +41,7 @@ __device__ __forceinline__ uint32_t lanemask_lt_q() {
 
 // Query size classes by M (candidates): the first kSortClasses run one query per warp
 // (query_sort.cu; a smaller class uses less shared memory per warp, so more warps per
-// SM); M <= 4096 and <= 8192 run one query per CTA with 2^13 / 2^14 count slots (below).
+// SM, up to MCAP 4096); M <= 8192 runs one query per CTA with 2^14 count slots (below).
 constexpr int kSortClasses = 7;
 __host__ __device__ constexpr uint32_t class_max(int c) {
   return c == 0 ? 768u : c == 1 ? 1024u : c == 2 ? 1280u : c == 3 ? 1536u : c == 4 ? 2048u
