@@ -253,6 +253,27 @@ def test_query_topk_bit_exact(name, make, K, L, R, rng, k):
         assert np.array_equal(flash.as_u32(g_cnt), o_cnt2)
 
 
+@pytest.mark.parametrize("few", ["0", "1000000000"])
+def test_query_4096_class_both_kernels(monkeypatch, few):
+    """Queries with 3072 < M <= 4096 candidates run the warp-per-query sort class when there
+    are many queries and the CTA-per-query kernel when there are few (FLASH_QUERY_FEW sets
+    the cut; 0 forces the sort class, a huge value the CTA kernel): both bit-exact."""
+    monkeypatch.setenv("FLASH_QUERY_FEW", few)
+    rp, col = shape_slice("url", 6000)
+    K, L, R, rng, k = 4, 128, 32, 1 << 6, 128  # 64 buckets: all saturate, M = L*R = 4096
+    n = rp.size - 1
+    seed = 0x4096
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    ids = np.arange(n, dtype=np.uint32)
+    T = oracle.build(L, R, rng, seed, addrs, ids)
+    o_ids, o_cnt = oracle.query(T, addrs, k, exclude=ids)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        g_ids, g_cnt = idx.knn_graph(d_rp, d_col, k)
+        assert np.array_equal(flash.as_u32(g_ids), o_ids)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
+
+
 GRAPH_CASES = [
     ("tiny", lambda: synth.generate("tiny"), 4, 16, 32, 1 << 15, 10),
     ("edge", edge_csr, 4, 16, 32, 1 << 15, 10),
