@@ -99,8 +99,8 @@ __host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins
   return (b + 15) & ~(size_t)15;
 }
 
-template <int MCAP, int BINS_LOG2>
-__global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t* __restrict__ qlist,
+template <int MCAP, int BINS_LOG2, int NW>
+__global__ void __launch_bounds__(32 * NW) k_query_sort(QueryArgs a, const uint32_t* __restrict__ qlist,
                                                    const uint32_t* __restrict__ qcount, uint32_t shift) {
   constexpr uint32_t NBW = MCAP / 32 + 2;
   constexpr uint32_t kBins = 1u << BINS_LOG2;
@@ -476,23 +476,50 @@ __global__ void __launch_bounds__(128) k_query_sort(QueryArgs a, const uint32_t*
   }
 }
 
-template <int MCAP, int BL>
-int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
-  constexpr int kWarps = 4;
+// NW warps per CTA (one query each).
+template <int MCAP, int BL, int NW>
+int launch_sort_nw(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
   // digit = the top BL bits of the id range [0, max_id]
   const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
   const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
+  // FLASH_QSORT_PAD (diagnostic): extra shared memory per CTA, to probe how the kernel's
+  // time depends on resident warps
   static const size_t pad = [] { const char* e = getenv("FLASH_QSORT_PAD"); return e ? (size_t)atol(e) : (size_t)0; }();
-  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * kWarps + pad;
-  if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL>, smem)) return 0;
+  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * NW + pad;
+  if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL, NW>, smem)) return 0;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL>, 32 * kWarps, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL, NW>, 32 * NW, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)device_sms() * per_sm;
-  const uint64_t need = (a.nq + kWarps - 1) / kWarps;
+  const uint64_t need = (a.nq + NW - 1) / NW;
   if (grid > need) grid = need;
-  k_query_sort<MCAP, BL><<<(unsigned)grid, 32 * kWarps, smem, s>>>(a, list, count, shift);
+  k_query_sort<MCAP, BL, NW><<<(unsigned)grid, 32 * NW, smem, s>>>(a, list, count, shift);
   return 1;
+}
+
+// Resident warps per SM of an NW-warp CTA of this class (0 if it does not fit).
+template <int MCAP, int BL, int NW>
+int resident_warps(const QueryArgs& a) {
+  const size_t smem = sort_slice_bytes(MCAP, 1u << BL, a.L, a.cmax) * NW;
+  if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL, NW>, smem)) return 0;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL, NW>, 32 * NW, smem);
+  return per_sm * NW;
+}
+
+// 4 warps per CTA, or 5 where that packs more warps into an SM's shared memory (the slice
+// size depends on L: e.g. MCAP 4096 at L = 128 is 22.5 KB per warp — 2 CTAs of 4 = 8
+// warps per SM, 2 CTAs of 5 = 10).  Cached per (class, L, cmax).
+template <int MCAP, int BL>
+int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+  static thread_local uint64_t key = ~0ull;
+  static thread_local bool five = false;
+  const uint64_t k2 = ((uint64_t)a.L << 32) | a.cmax;
+  if (k2 != key) {
+    five = resident_warps<MCAP, BL, 5>(a) > resident_warps<MCAP, BL, 4>(a);
+    key = k2;
+  }
+  return five ? launch_sort_nw<MCAP, BL, 5>(a, list, count, s) : launch_sort_nw<MCAP, BL, 4>(a, list, count, s);
 }
 
 }  // namespace
