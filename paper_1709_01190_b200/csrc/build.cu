@@ -977,6 +977,14 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   tmp = a.scan_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.keep_cnt, a.goff_new, (int64_t)nb + 1, s);
   // (the two CUB scans launch library kernels; they are not counted as ours)
+  cudaStream_t side = static_cast<cudaStream_t>(a.side_stream);
+  bool side_used = false;
+  if (a.after_scan && side) {  // e.g. the graph's query planning, beside the scatter/selects
+    cudaEventRecord(static_cast<cudaEvent_t>(a.side_fork), s);
+    cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(a.side_fork), 0);
+    a.after_scan(a.after_scan_ctx, side);
+    side_used = true;
+  }
   if (a.goff_old) {
     const unsigned wb = (unsigned)(((uint64_t)nb + 7) / 8 < (uint64_t)device_sms() * 32 ? ((uint64_t)nb + 7) / 8 : (uint64_t)device_sms() * 32);
     k_fill_old<<<wb, 256, 0, s>>>(nb, a.goff_old, a.ids_old, a.pool_off, a.pool);
@@ -1005,12 +1013,11 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const size_t sel_smem = (size_t)(kSelThreads / 32) * kWarpCap * sizeof(uint64_t);
   ensure_smem_attr((const void*)k_select_warp, sel_smem);
   if (early) {  // the early-listed big buckets, concurrently with the kernels below
-    cudaStream_t side = static_cast<cudaStream_t>(a.side_stream);
     cudaEventRecord(static_cast<cudaEvent_t>(a.side_fork), s);
     cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(a.side_fork), 0);
     k_select_big<<<device_sms(), kBigThreads, 0, side>>>(a.range, a.R, a.keys, 0, a.pool_off, a.pool, a.goff_new,
                                                         a.ids_new, a.early_list, early_count);
-    cudaEventRecord(static_cast<cudaEvent_t>(a.side_join), side);
+    side_used = true;
     launches += 1;
   }
   uint32_t* mid_list = a.cursor;  // free once k_fill_new is done
@@ -1031,7 +1038,10 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   k_select_big<<<device_sms(), kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
                                               a.ids_new, a.big_list, a.big_count);  // the late list
   launches += 1;
-  if (early) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.side_join), 0);
+  if (side_used) {  // join everything queued on the side stream
+    cudaEventRecord(static_cast<cudaEvent_t>(a.side_join), side);
+    cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.side_join), 0);
+  }
   return launches;
 }
 

@@ -198,7 +198,8 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
 
 flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
                              cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX, bool cols = false,
-                             bool converted = false) {
+                             bool converted = false, void (*after_scan)(void*, cudaStream_t) = nullptr,
+                             void* after_scan_ctx = nullptr) {
   if (t1 > h->L) t1 = h->L;
   const uint64_t nb = nbuckets(h);
   if (h->shared && !converted) {  // table addresses -> each row's distinct shared reservoirs
@@ -278,6 +279,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.side_stream = h->side_stream;
   a.side_fork = h->side_fork;
   a.side_join = h->side_join;
+  a.after_scan = after_scan;
+  a.after_scan_ctx = after_scan_ctx;
   a.scan_tmp = h->scan_tmp.p;
   a.scan_tmp_bytes = h->scan_tmp.cap;
   h->launches += launch_build(a, s);
@@ -300,9 +303,36 @@ flash_status ensure_huge_table(flash_index* h, cudaStream_t s) {
   return FLASH_OK;
 }
 
+QueryArgs query_args(const flash_index* h, const uint32_t* addrs, uint64_t nq, uint32_t k, const uint32_t* exclude,
+                     int exclude_self, uint32_t self_base, uint32_t* out_ids, uint32_t* out_counts, int cur) {
+  QueryArgs a;
+  memset(&a, 0, sizeof a);
+  a.addrs = addrs;
+  a.nq = nq;
+  a.goff = h->goff[cur].as<uint64_t>();
+  a.ids = h->ids[cur].as<uint32_t>();
+  a.L = h->L;
+  a.range = h->range;
+  a.k = k;
+  a.cmax = h->L;
+  a.direct = 0;
+  a.shared = h->shared;
+  a.exclude = exclude;
+  a.exclude_self = exclude_self;
+  a.self_base = self_base;
+  a.out_ids = out_ids;
+  a.out_counts = out_counts;
+  a.err = h->err;
+  a.table_log2 = h->table_log2;
+  a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
+  a.max_id = (uint32_t)h->max_id;
+  return a;
+}
+
 flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64_t nq, uint32_t k,
                             const uint32_t* exclude, int exclude_self, uint32_t self_base,
-                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s, bool converted = false) {
+                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s, bool converted = false,
+                            bool planned = false) {
   flash_index* h = const_cast<flash_index*>(hc);
   if (h->shared && !converted && h->have_tables) {  // each distinct reservoir aggregated once
     TRY(ensure(h->qraddr, sizeof(uint32_t) * nq * h->L));
@@ -321,26 +351,8 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
   TRY(ensure(h->qscratch, query_scratch_bytes(nq)));
   TRY(ensure_huge_table(h, s));
   Phase ph(h, 2, s);
-  QueryArgs a;
-  a.addrs = addrs;
-  a.nq = nq;
-  a.goff = h->goff[h->cur].as<uint64_t>();
-  a.ids = h->ids[h->cur].as<uint32_t>();
-  a.L = h->L;
-  a.range = h->range;
-  a.k = k;
-  a.cmax = h->L;
-  a.direct = 0;
-  a.shared = h->shared;
-  a.exclude = exclude;
-  a.exclude_self = exclude_self;
-  a.self_base = self_base;
-  a.out_ids = out_ids;
-  a.out_counts = out_counts;
-  a.err = h->err;
-  a.table_log2 = h->table_log2;
-  a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
-  a.max_id = (uint32_t)h->max_id;
+  QueryArgs a = query_args(h, addrs, nq, k, exclude, exclude_self, self_base, out_ids, out_counts, h->cur);
+  a.planned = planned ? 1 : 0;
   h->launches += launch_query(a, h->qscratch.p, h->qhuge.p, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
@@ -584,10 +596,30 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
   TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
   uint32_t* addrs = h->addrs.as<uint32_t>();
   TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
-  TRY(do_insert_addrs(h, addrs, n_rows, 0, s));
-  if (h->shared)  // the rows' distinct reservoirs are the queries' too
+  if (h->shared) {  // the rows' distinct reservoirs are the queries' too
+    TRY(do_insert_addrs(h, addrs, n_rows, 0, s));
     return do_query_addrs(h, h->raddr.as<uint32_t>(), n_rows, k, nullptr, 1, 0, out_ids, out_counts, s, true);
-  return do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s);
+  }
+  // The queries' size-class plan needs only their addresses and the new bucket offsets, so
+  // it runs on the build's side stream as soon as the offsets are scanned, beside the
+  // scatter and selects; the build joins it before returning.
+  TRY(ensure(h->qscratch, query_scratch_bytes(n_rows)));
+  TRY(ensure_huge_table(h, s));
+  struct PlanCtx {
+    flash_index* h;
+    QueryArgs a;
+    void* scratch;
+    uint64_t launches;
+  } ctx{h, query_args(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, h->cur), h->qscratch.p, 0};
+  auto plan = [](void* c, cudaStream_t side) {
+    PlanCtx* p = static_cast<PlanCtx*>(c);
+    // a fresh handle builds into goff[cur]; allocated by now
+    p->a.goff = p->h->goff[p->h->cur].as<uint64_t>();
+    p->launches += launch_query_plan(p->a, p->scratch, side);
+  };
+  TRY(do_insert_addrs(h, addrs, n_rows, 0, s, 0, UINT32_MAX, false, false, plan, &ctx));
+  h->launches += ctx.launches;
+  return do_query_addrs(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, s, false, true);
 }
 
 flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx,

@@ -130,6 +130,11 @@ struct BuildArgs {
   unsigned long long* err;    // device error counter
   void* scan_tmp;
   size_t scan_tmp_bytes;
+  // optional: called once the new bucket offsets (goff_new) are final, with the side stream
+  // already ordered after them (flash_knn_graph plans its queries there, concurrently with
+  // the scatter and selects); the build joins the side stream before it returns
+  void (*after_scan)(void* ctx, cudaStream_t side);
+  void* after_scan_ctx;
 };
 size_t build_scan_tmp_bytes(uint64_t nb);
 uint32_t smem_build_ctas(uint32_t W, uint64_t n);  // CTAs of the shared-memory passes (hbuf: (C + W) slots)
@@ -157,11 +162,14 @@ struct QueryArgs {
   uint32_t table_log2;      // worst-case count-table slots = 2^table_log2 (from L*R)
   int packed;               // every inserted id < 2^24-1 and L <= 255: u32 (id, count) entries
   uint32_t max_id;          // largest id inserted (the sort kernel's digit range)
+  int planned;              // launch_query_plan already ran for these queries (skip it)
 };
 // scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
 // huge_tab: query_huge_table_bytes() of global memory initialised once with
 // query_huge_table_init (kept clean by the kernels), needed only when L*R > 8192
 int launch_query(const QueryArgs& a, void* scratch, void* huge_tab, cudaStream_t s);
+// the size-class planning step of launch_query alone (needs only addrs and goff)
+int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s);
 size_t query_huge_table_bytes();
 void query_huge_table_init(void* gtab, cudaStream_t s);
 size_t query_scratch_bytes(uint64_t nq);

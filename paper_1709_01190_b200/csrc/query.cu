@@ -570,8 +570,7 @@ void query_huge_table_init(void* gtab, cudaStream_t s) {
 
 size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * kClasses + kClasses); }
 
-int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream_t s) {
-  uint8_t* huge_tab = static_cast<uint8_t*>(huge_tab_v);
+int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (a.nq == 0) return 0;
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* counts = lists + a.nq * kClasses;
@@ -582,13 +581,23 @@ int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream
   const uint64_t max_m = 1ull << (a.table_log2 - 1);  // M <= L*R <= 2^(table_log2 - 1)
   k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.L, a.range, a.direct, a.shared, max_m, a.k,
                                                  a.out_ids, a.out_counts, lists, counts, a.err);
+  return 1;
+}
+
+int launch_query(const QueryArgs& a, void* scratch, void* huge_tab_v, cudaStream_t s) {
+  uint8_t* huge_tab = static_cast<uint8_t*>(huge_tab_v);
+  if (a.nq == 0) return 0;
+  uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
+  uint32_t* counts = lists + a.nq * kClasses;
+  const uint64_t max_m = 1ull << (a.table_log2 - 1);
+  const int planned = a.planned ? 0 : launch_query_plan(a, scratch, s);
   const uint32_t hist_len = (a.cmax + 1) > 1024 ? a.cmax + 1 : 1024;
   // The class kernels are persistent over their device-side query lists and run back to
   // back on the caller's stream (measured: overlapping them on side streams is slower,
   // since kernels with different shared-memory footprints then share the SMs).
   const char* few_env = getenv("FLASH_QUERY_FEW");  // tests: force either 4096-class kernel
   const uint64_t few = few_env ? strtoull(few_env, nullptr, 10) : kFewQueries;
-  int n = 1;
+  int n = planned;
   for (int c = 0; c < kClasses; ++c) {
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
     const uint32_t* lc = lists + (uint64_t)c * a.nq;
