@@ -32,4 +32,7 @@ timeout 900 python bench.py --workload kdd12 --steps 3 --warmup 3 > "$OUT/${TAG}
 timeout 900 python bench.py --workload friendster --steps 3 --warmup 3 > "$OUT/${TAG}_bench_friendster.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --workload url-graph --steps 3 --warmup 3 > "$OUT/${TAG}_bench_url_graph.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/${TAG}_bench_reference.json" 2>> "$OUT/bench.log"
+# 4. the K x L x R sweep (80 graphs, ~1 min)
+timeout 1200 python tools/sweep.py --out "$OUT/${TAG}_sweep.json" > /dev/null 2>> "$OUT/bench.log"
+python tools/sweep_table.py "$OUT/${TAG}_sweep.json" > "$OUT/${TAG}_sweep.txt"
 ls -la "$OUT"
