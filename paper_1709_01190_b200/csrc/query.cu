@@ -52,7 +52,7 @@ __host__ __device__ constexpr uint32_t class_max(int c) {
 constexpr int kClasses = kSortClasses + 2;
 constexpr uint32_t kHugeLog2 = 16;
 constexpr uint64_t kFewQueries = 65536;  // below: the 3072 < M <= 4096 class runs CTA-per-query
-constexpr uint32_t kHugeCtas = 148;
+constexpr uint32_t kHugeCtas = 296;  // 2 per SM: 114 MB of slices, about the L2 (148: 2.24 s, 592: 2.25 s for the K=2, L=128, R=256 graph; 296: 2.10 s)
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              uint32_t L, uint32_t range, int direct, uint32_t shared, uint64_t mmax, uint32_t k,
