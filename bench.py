@@ -12,9 +12,10 @@ R=128, range=2^15, k=128 (synthetic, synth/ seed 2).
 `value` = N / graph time (queries/s over the whole graph; every row is a query),
 device-timed with CUDA events, max over ranks.  `e2e` = the same metric through
 flash_knn_graph_host (pinned host CSR in, host top-k out, copies inside the timed
-region).  N>1: one rank per GPU (torchrun), replicated tables (paper_1709_01190_b200
-/dist.py knn_graph_sharded_build: row-sharded hash and query, table-sharded build,
-built tables all-gathered), strong scaling of the fixed graph.
+region).  N>1: one rank per GPU (torchrun), the library's multi-GPU handle
+(flash_create_dist: tables partitioned over the GPUs, addresses and candidate lists
+stored into the peers' buffers, NCCL barriers; --mode sharded: the torch.distributed
+sharded-build schedule of dist.py instead), strong scaling of the fixed graph.
 
 The reference arm (--impl reference) and `cpu_baseline` time the CPU oracle (oracle/)
 as it stands on the host cores (OpenMP, all cores) on the same workload: hash + build
@@ -84,7 +85,7 @@ def workload_config(shape, nnz, args):
         "N": shape.N, "D": shape.D, "nnz": int(nnz), "nnz_per_row": round(nnz / shape.N, 1),
         "K": K, "L": L, "R": R, "range": RANGE, "k": TOPK, "seed": SEED,
         "parallelism": ((f"rows x{args.gpus} (hash, count/top-k); tables x{args.gpus} (build, gather); "
-                         "all-to-all addresses + candidates") if args.mode == "exchange" else
+                         "addresses + candidates as peer stores (flash_create_dist)") if args.mode == "exchange" else
                         (f"rows x{args.gpus} (hash, query); tables x{args.gpus} (build); "
                          "all-gather addresses + built tables")) if args.gpus > 1 else "1 GPU",
         "l2_policy": "inputs larger than L2 (col_idx 5.2 GB vs 126 MB L2); no flush",
@@ -156,13 +157,13 @@ def gen_local(shape, bounds, rank):
     return rp_t, col_t, nnz
 
 
-def query_work(idx_tables, addrs_np):
-    """Candidates gathered per query (the sum of its L bucket sizes) and the bucket-arrival
-    histogram (log2 bins) of the built tables."""
+def query_work(idx_tables, addrs_np, tables=None):
+    """Candidates gathered per query (the sum of its bucket sizes over `tables`, default all
+    L) and the bucket-arrival histogram (log2 bins) of those tables."""
     per_q = np.zeros(addrs_np.shape[0], dtype=np.int64)
     hist = np.zeros(34, dtype=np.int64)
     over_r = 0
-    for t in range(L):
+    for t in (range(L) if tables is None else tables):
         off, _, arr = idx_tables(t)
         sizes = np.diff(off.astype(np.int64))
         a = addrs_np[:, t]
@@ -342,19 +343,19 @@ def run_ours(args):
     d_col = h_col.to(dev, non_blocking=True)
     out_ids = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
     out_cnt = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
-    idx = flash.FlashIndex(K, L, R, RANGE, SEED)
+    # N > 1: the library's multi-GPU handle (tables partitioned over the GPUs, candidates to
+    # the query owners; north_star (d)), or the torch.distributed sharded-build schedule
+    use_dist_handle = world > 1 and args.mode == "exchange"
+    idx = (fdist.create_dist_index(K, L, R, RANGE, SEED) if use_dist_handle
+           else flash.FlashIndex(K, L, R, RANGE, SEED))
     stream = torch.cuda.current_stream()
-    # N > 1: tables partitioned over the GPUs with the candidate all-to-all (north_star (d),
-    # default) or the sharded build + table all-gather
-    graph_fn = (fdist.knn_graph_candidate_exchange if args.mode == "exchange"
-                else fdist.knn_graph_sharded_build)
 
     def step():
         idx.clear()
-        if world == 1:
+        if world == 1 or use_dist_handle:
             flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, TOPK, out_ids, out_cnt)
             return out_ids, out_cnt
-        return graph_fn(idx, d_rp, d_col, TOPK, bounds, rank)
+        return fdist.knn_graph_sharded_build(idx, d_rp, d_col, TOPK, bounds, rank)
 
     for _ in range(args.warmup):
         step()
@@ -396,12 +397,12 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         t = time.perf_counter()
-        if world == 1:
+        if world == 1 or use_dist_handle:
             flash.flash_knn_graph_host(idx.h, h_rp_local, h_col, n_local, TOPK, h_ids, h_cnt)
         else:
             d_rp2 = h_rp_local.to(dev, non_blocking=True)
             d_col2 = h_col.to(dev, non_blocking=True)
-            ids_, cnt_ = graph_fn(idx, d_rp2, d_col2, TOPK, bounds, rank)
+            ids_, cnt_ = fdist.knn_graph_sharded_build(idx, d_rp2, d_col2, TOPK, bounds, rank)
             h_ids.copy_(ids_, non_blocking=True)
             h_cnt.copy_(cnt_, non_blocking=True)
             torch.cuda.synchronize()
@@ -413,21 +414,45 @@ def run_ours(args):
         dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
     e2e_ms_max = float(e2e_local.item())
 
-    # work counts for the roofline (graph of the last step; rank-local)
+    # work counts for the roofline (graph of the last step).  N > 1: every rank sees only its
+    # table window, so the rows' addresses are all-gathered (evaluation only) and each rank
+    # sums its window's bucket sizes for every query; the sums are all-reduced.
     idx.clear()
     step()
     torch.cuda.synchronize()
-    addrs_np = flash.as_u32(idx.hash_addrs(d_rp, d_col))
-    per_q, arrivals = query_work(lambda t: idx.table(t), addrs_np)  # this rank's queries
-    n_cand = int(per_q.sum())
+    addrs_local = idx.hash_addrs(d_rp, d_col)
+    counts = [bounds[g + 1] - bounds[g] for g in range(world)]
+    addrs_np = flash.as_u32(fdist.all_gather_rows(addrs_local, counts) if world > 1 else addrs_local)
+    _, _, w0, w1 = idx.dist_info() if use_dist_handle else (0, 1, 0, L)
+    per_q, arrivals = query_work(lambda t: idx.table(t), addrs_np, range(w0, w1))
+    x1_bytes = x2_bytes = 0
+    per_step = {name: phase_ms[i] / max(phase_calls[i], 1) * (phase_calls[i] / args.steps)
+                for i, name in enumerate(["hash", "build", "query", "copy"])}
+    if use_dist_handle:
+        own = np.zeros(shape.N, dtype=bool)
+        own[bounds[rank]:bounds[rank + 1]] = True
+        # bytes this rank stores into the other GPUs per graph: its rows' addresses for the
+        # other windows (X1) and its window's candidates of the other ranks' queries (X2)
+        xb = torch.tensor([4 * n_local * (L - (w1 - w0)), 4 * int(per_q[~own].sum())], dtype=torch.int64,
+                          device=dev)
+        dist.all_reduce(xb, op=dist.ReduceOp.MAX)
+        x1_bytes, x2_bytes = int(xb[0].item()), int(xb[1].item())
+        pq = torch.from_numpy(per_q).to(dev)
+        dist.all_reduce(pq)  # windows partition the tables: the sum is each query's candidates
+        per_q = pq.cpu().numpy()
+    if world > 1:  # phase times: the slowest rank
+        pt = torch.tensor([per_step[k] for k in ("hash", "build", "query", "copy")], dtype=torch.float64, device=dev)
+        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        per_step = dict(zip(("hash", "build", "query", "copy"), pt.tolist()))
+    n_cand = int(per_q.sum())  # every query of the graph (all ranks)
 
     result = None
     if rank == 0:
         hbm_peak, peak_kind = peaks()
-        per_step = {name: phase_ms[i] / max(phase_calls[i], 1) * (phase_calls[i] / args.steps)
-                    for i, name in enumerate(["hash", "build", "query", "copy"])}
-        # algorithmic bytes per launch
-        hash_bytes = 4 * nnz_local + 8 * (n_local + 1) + 4 * L * n_local
+        N = shape.N
+        # algorithmic bytes, whole graph over all GPUs
+        hash_bytes = 4 * nnz_total + 8 * (N + 1) + 4 * L * N
+        query_bytes = (4 * L + 8 * L + 8 * TOPK) * N + 4 * n_cand
         hash_ms = per_step["hash"]
         query_ms = per_step["query"]
         build_ms = per_step["build"]
@@ -445,40 +470,41 @@ def run_ours(args):
                         issue[nm] = (w + d["warp_inst"], t + d["duration_ms"])
         except Exception:
             pass
-        q_traffic = None
-        if "k_query_sort" in traffic:
-            q_traffic = sum(traffic.get(nm, 0.0) for nm in ("k_query_sort", "k_query"))
-        if dominant == "query" and n_cand is not None:
-            # the count kernel is bound by per-candidate shared-memory work, not by HBM
-            roof = {"kernel": "query phase: k_query_sort<MCAP,BL> size classes (+ k_query for M > 4096; k_query_plan overlaps the build)",
-                    "bound": "alu", "achieved": n_cand / (query_ms * 1e-3),
-                    "peak": SMEM_RMW_PEAK, "unit": "candidate-updates/s", "peak_kind": "measured (smem RMW microbench)",
-                    "traffic": q_traffic, "candidates": n_cand,
-                    "hbm_view": {"algorithmic_bytes": 4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local,
-                                 "achieved_GBps": (4 * L * n_local + 16 * L * n_local + 4 * n_cand + 8 * TOPK * n_local)
-                                 / (query_ms * 1e-3) / 1e9}}
-            if "k_query_sort" in issue:
+        peak_all = hbm_peak * world  # GB/s over the job's GPUs
+        if dominant == "query":
+            q_traffic = (sum(traffic.get(nm, 0.0) for nm in ("k_query_sort", "k_query", "k_query_csort", "k_query_plan"))
+                         if "k_query_sort" in traffic and world == 1 else None)
+            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query / "
+                              "k_query_csort for M > 4096)" + ("; + k_dist_gather peer stores" if world > 1 else ""),
+                    "bound": "hbm", "achieved": query_bytes / (query_ms * 1e-3) / 1e9, "peak": peak_all,
+                    "unit": "GB/s", "peak_kind": peak_kind, "traffic": q_traffic, "algorithmic_bytes": query_bytes,
+                    "bytes_formula": "(4L + 8L + 8k) B/query + 4 B/candidate (SURVEY 8(d))", "candidates": n_cand,
+                    # diagnostics: the count step needs >= 1 shared-memory RMW per candidate
+                    "smem_view": {"achieved_candidates_per_s": n_cand / (query_ms * 1e-3), "peak": SMEM_RMW_PEAK * world,
+                                  "frac": n_cand / (query_ms * 1e-3) / (SMEM_RMW_PEAK * world),
+                                  "peak_kind": "measured smem RMW microbench (profiles/r01_microbench_smem.txt)"}}
+            if "k_query_sort" in issue and world == 1:
                 # instruction-issue view from the committed ncu capture: warp instructions
                 # issued per second by the sort kernels vs 4 schedulers x 148 SMs x clock
                 w, t = issue["k_query_sort"]
                 peak_issue = 4 * 148 * clk_mhz_for_peak() * 1e6
                 roof["issue_view"] = {"kernel": "k_query_sort (all classes, ncu)", "warp_inst": w,
-                                      "warp_inst_per_query": w / n_local, "achieved_warp_inst_per_s": w / (t * 1e-3),
+                                      "warp_inst_per_query": w / N, "achieved_warp_inst_per_s": w / (t * 1e-3),
                                       "peak_warp_inst_per_s": peak_issue, "frac": w / (t * 1e-3) / peak_issue}
         elif dominant == "build":
-            bbytes = 8 * L * n_local * 2 + 12 * L * n_local
+            bbytes = 8 * L * N * 2 + 12 * L * N
             roof = {"kernel": "build (k_count..k_select_big)", "bound": "hbm",
-                    "achieved": bbytes / (build_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "achieved": bbytes / (build_ms * 1e-3) / 1e9, "peak": peak_all, "unit": "GB/s",
                     "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": bbytes}
         else:
             roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
-                    "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
-                    "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
+                    "peak": peak_all, "unit": "GB/s", "peak_kind": peak_kind,
+                    "traffic": traffic.get("k_doph") if world == 1 else None, "algorithmic_bytes": hash_bytes}
         hash_roof = {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
-                     "traffic": traffic.get("k_doph"), "algorithmic_bytes": hash_bytes}
+                     "peak": peak_all, "unit": "GB/s", "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / peak_all,
+                     "traffic": traffic.get("k_doph") if world == 1 else None, "algorithmic_bytes": hash_bytes}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        value = shape.N / (ms_step * 1e-3)
+        value = N / (ms_step * 1e-3)
         h2d = 8 * (n_local + 1) + 4 * nnz_local
         d2h = 8 * n_local * TOPK
         result = {
@@ -490,8 +516,8 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": ms_step,
             "graph_time_s": ms_step * 1e-3,
-            "hash_nnz_per_s": nnz_local / (hash_ms * 1e-3) * world if hash_ms else None,
-            "queries_per_s": shape.N / (ms_step * 1e-3),
+            "hash_nnz_per_s": nnz_total / (hash_ms * 1e-3) if hash_ms else None,
+            "queries_per_s": N / (ms_step * 1e-3),
             "phase_ms_per_step": per_step,
             "hash_roofline": hash_roof,
             "higher_is_better": True,
@@ -501,14 +527,17 @@ def run_ours(args):
             "data": "synthetic (synth/, webspam shape, seed 2)",
             "config": workload_config(shape, nnz_total, args),
             "roofline": roof,
-            "e2e": {"value": shape.N / (e2e_ms_max * 1e-3), "unit": "queries/s",
-                    "ms_per_step": e2e_ms_max, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "flash_knn_graph_host (pinned host buffers)" if world == 1 else
+            "e2e": {"value": N / (e2e_ms_max * 1e-3), "unit": "queries/s",
+                    "ms_per_step": e2e_ms_max, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                    "api": "flash_knn_graph_host (pinned host buffers)" if (world == 1 or use_dist_handle) else
                            f"host copies + dist {args.mode} graph"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        result["candidates_per_query"] = {"mean": n_cand / n_local, "p99": float(np.percentile(per_q, 99)),
+        if world > 1:
+            result["exchange_bytes_per_gpu"] = {"x1_addresses": x1_bytes, "x2_candidates": x2_bytes,
+                                                "note": "max over ranks, stored into peer GPUs per graph"}
+        result["candidates_per_query"] = {"mean": n_cand / N, "p99": float(np.percentile(per_q, 99)),
                                           "max": int(per_q.max())}
         result["bucket_arrivals"] = arrivals
         if world == 1 and not args.no_quality:
@@ -736,6 +765,39 @@ def run_shape(args):
     }
 
 
+def host_cpu():
+    """lscpu model / sockets and the OpenMP thread count the oracle runs with."""
+    info = {"model": None, "sockets": None}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip())
+    except Exception:
+        pass
+    info["omp_threads"] = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return info
+
+
+def tiny_one_thread_s():
+    """the tiny graph on the oracle with ONE thread (a subprocess with
+    OMP_NUM_THREADS=1; median of 3)."""
+    code = ("import sys,time,statistics; sys.path.insert(0, %r); import oracle, synth; "
+            "rp, col = synth.generate('tiny'); ts = []\n"
+            "for _ in range(3):\n t = time.perf_counter(); "
+            "oracle.knn_graph(4, 16, 32, 1 << 15, 0x5EED0001, rp, col, 10); ts.append(time.perf_counter() - t)\n"
+            "print(statistics.median(ts))") % ROOT
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, OMP_NUM_THREADS="1"))
+        return float(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 def cpu_baseline(sample_queries: int, steps: int = 1):
     """The oracle as it stands on the host cores: full hash + build, a query sample."""
     import oracle
@@ -743,7 +805,8 @@ def cpu_baseline(sample_queries: int, steps: int = 1):
     shape = synth.SHAPES["webspam"]
     rp, col = synth.generate(shape)
     n = rp.size - 1
-    cores = os.cpu_count()
+    cpu = host_cpu()
+    cores = cpu["omp_threads"]
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -763,7 +826,8 @@ def cpu_baseline(sample_queries: int, steps: int = 1):
             "sample": f"hash+build of all {n} rows, top-{TOPK} for {sample_queries} sampled rows, "
                       f"query time extrapolated x{n / sample_queries:.1f}",
             "graph_s_extrapolated": g, "hash_s": times[-1][1], "build_s": times[-1][2],
-            "query_sample_s": times[-1][3]}, times
+            "query_sample_s": times[-1][3], "cpu_model": cpu["model"], "sockets": cpu["sockets"],
+            "nnz": int(rp[-1]), "tiny_graph_1_thread_s": tiny_one_thread_s()}, times
 
 
 def run_reference(args):
@@ -779,7 +843,7 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": g * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (synth/, webspam shape, seed 2)",
-        "config": workload_config(shape, int(0), args) | {"nnz": None},
+        "config": workload_config(shape, cb["nnz"], args),
         "cpu_baseline": cb,
         "e2e": {"value": shape.N / g, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

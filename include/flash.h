@@ -50,7 +50,7 @@ typedef enum {
     FLASH_EINVAL = 1, /* bad argument; nothing enqueued */
     FLASH_ENOMEM = 2, /* device allocation failed */
     FLASH_ECUDA = 3,  /* CUDA runtime error (message in flash_last_error) */
-    FLASH_ENCCL = 4,  /* reserved for the distributed exchange */
+    FLASH_ENCCL = 4,  /* NCCL failed (multi-GPU handle; message in flash_last_error) */
     FLASH_ESTATE = 5  /* call not valid in the handle's state */
 } flash_status;
 
@@ -116,10 +116,12 @@ flash_status flash_table_arrays(const flash_index *h, const uint64_t **goff, con
                                 const uint32_t **arrivals, uint64_t *n_ids);
 
 /* Replace the index content with copies of device arrays in flash_table_arrays' layout
- * (arrivals may be NULL: zeros).  max_id: the largest id the tables hold (ids are
- * 0..max_id in a k-NN graph).  Stream-ordered. */
+ * (arrivals may be NULL: zeros).  The offsets are validated first (goff[0] == 0,
+ * non-decreasing, goff[L*range] == n_ids; else FLASH_EINVAL and the index is unchanged) and
+ * the largest imported id is taken from ids (it sets the query kernels' digit range): both
+ * on the device, then the call synchronizes `stream` once. */
 flash_status flash_import_tables(flash_index *h, const uint64_t *goff, const uint32_t *ids, uint64_t n_ids,
-                                 const uint32_t *arrivals, uint32_t max_id, void *stream);
+                                 const uint32_t *arrivals, void *stream);
 
 /* Querying phase (Alg. 3) for n_q CSR query rows: aggregate the L addressed
  * buckets, count each candidate's multiplicity (full count, R#11), drop exclude[q] (if
@@ -197,10 +199,54 @@ flash_status flash_window_gather(const flash_index *h, const uint32_t *addrs, ui
  * occurs at most once per table, so counts are <= the handle's L, and a query has at most
  * L*R candidates (a query with more is counted in the device error counter, flash_check,
  * and gets k pads).  max_id bounds every candidate id.  cand may be NULL when every size is
- * 0.  1 <= n_seg <= 4096, n_q < 2^31.  The handle's tables are not used. */
+ * 0 (a query with candidates then counts as an error and gets k pads).  1 <= n_seg <= 4096,
+ * n_q < 2^31.  The handle's tables are not used. */
 flash_status flash_count_topk(const flash_index *h, const uint32_t *cand, const uint32_t *seg_sizes,
                               uint32_t n_seg, uint64_t n_q, uint32_t k, const uint32_t *exclude, uint32_t max_id,
                               uint32_t *out_ids, uint32_t *out_counts, void *stream);
+
+/* ---- Multi-GPU handle (north_star (d)) ---------------
+ * One handle per GPU (rank g of `world`, one node).  The L tables are partitioned over the
+ * ranks by floor blocks — rank g owns [floor(g*L/world), floor((g+1)*L/world)) — and every
+ * query is answered on the rank that passed its row (queries are data-parallel, P:322
+ * §3.4).  On such a handle flash_insert, flash_query_topk, flash_knn_graph(_host) are
+ * COLLECTIVE: every rank calls them, in the same order, with its own contiguous row shard
+ * (n_rows may differ per rank and may be 0):
+ *   - flash_knn_graph: the shards in rank order are rows 0..N-1 of ONE graph (global ids =
+ *     rank offset + local row); out_ids / out_counts [n_rows][k] are this rank's rows.
+ *   - flash_insert: rank g's rows get ids id_base_g + r (id_base per rank).
+ *   - flash_query_topk: this rank's queries against the whole (distributed) index;
+ *     exclude [n_q] per local query.
+ * Results are byte-identical to a single-GPU handle with the same (K, L, R, range, seed) fed
+ * the concatenated shards.  Row addresses travel to the table owners and candidate lists to
+ * the query owners as stores into the peers' memory (NVLink P2P), separated by stream-ordered
+ * barriers; the host synchronizes once per call to exchange the shard sizes.
+ * flash_get_table works for the rank's own tables; flash_clear is local; flash_hash works on
+ * the rank's rows (all L tables); the single-GPU step calls (flash_insert_addrs*,
+ * flash_query_addrs, flash_table_arrays, flash_import_tables, flash_count_topk, window calls)
+ * return FLASH_ESTATE. */
+#define FLASH_UNIQUE_ID_BYTES 128
+
+/* NCCL bootstrap id (host buffer of FLASH_UNIQUE_ID_BYTES): rank 0 creates it and hands it to
+ * every rank out of band (e.g. torch.distributed broadcast). */
+flash_status flash_get_unique_id(void *unique_id);
+
+/* Collective over `world` processes (one GPU each, the current device): rank `rank` of a
+ * multi-GPU handle with an NCCL communicator owned by the handle.  NCCL (libnccl.so.2) is
+ * loaded at run time; FLASH_ENCCL if it is missing or fails.  Peer buffers are mapped with
+ * CUDA IPC, so the ranks must share a node.  0 <= rank < world <= 4096. */
+flash_status flash_create_dist(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed, int rank,
+                               int world, const void *unique_id, flash_index **out);
+
+/* The same for `world` virtual ranks in ONE process: out[g] (host array [world]) is rank g's
+ * handle, on device devices[g] (host array, or NULL: every rank on the current device; peer
+ * access is enabled between distinct devices).  Each rank's collective calls must come from
+ * its own host thread (they wait for each other), each on its own stream. */
+flash_status flash_create_dist_local(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed, int world,
+                                     const int *devices, flash_index **out);
+
+/* rank, world and table window [t_begin, t_end) of a handle (a plain handle: 0, 1, [0, L)). */
+flash_status flash_dist_info(const flash_index *h, int *rank, int *world, uint32_t *t_begin, uint32_t *t_end);
 
 /* Drop every inserted id (stream-ordered): the handle returns to its freshly created
  * state (arrivals zero, no tables), keeping K, L, R, range and seed. */

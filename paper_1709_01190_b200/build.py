@@ -16,7 +16,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 SO = os.path.join(PKG, "libflash.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["doph.cu", "build.cu", "query.cu", "query_sort.cu", "exchange.cu", "util.cu", "flash_api.cu"]
+SOURCES = ["doph.cu", "build.cu", "query.cu", "query_sort.cu", "exchange.cu", "util.cu", "flash_api.cu", "dist.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -43,7 +43,7 @@ def build_variant(name: str, defines: list[str]) -> str:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         subprocess.check_call([NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", o])
         objs.append(o)
-    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs])
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, "-ldl"])
     return out
 
 
@@ -72,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _stale(SO, objs):
         subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                               "-o", SO, *objs])
+                               "-o", SO, *objs, "-ldl"])
     return SO
 
 

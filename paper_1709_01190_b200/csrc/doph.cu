@@ -58,10 +58,12 @@ __device__ __forceinline__ void bin_min(uint32_t* v, uint32_t B, const HashKeys&
 }
 
 // H3 for one row (lanes over tables): fmix32 fold of each table's K-tuple, multiply-high to
-// [0, range).  world > 1 writes owner-blocked (flash_hash_blocked).
+// [0, range).  out.world > 1 writes owner-blocked (flash_hash_blocked), or with out.peers
+// straight into each table owner's window-address buffer (the multi-GPU X1 exchange fused
+// into the hash: P2P stores over NVLink when the owner is another GPU).
 __device__ __forceinline__ void write_addrs(const uint32_t* code, bool nonempty, uint32_t K, uint32_t L,
-                                            uint32_t range, const HashKeys& keys, uint32_t* __restrict__ addrs,
-                                            uint64_t n_rows, uint64_t r, uint32_t world, uint32_t lane) {
+                                            uint32_t range, const HashKeys& keys, const AddrOut& out,
+                                            uint64_t n_rows, uint64_t r, uint32_t lane) {
   for (uint32_t t = lane; t < L; t += 32) {
     uint32_t a = kEmpty;
     if (nonempty) {
@@ -69,12 +71,15 @@ __device__ __forceinline__ void write_addrs(const uint32_t* code, bool nonempty,
       for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
       a = __umulhi(x, range);
     }
-    if (world == 1) {
-      addrs[r * L + t] = a;
+    if (out.world == 1) {
+      out.addrs[r * L + t] = a;
     } else {  // owner-blocked: table t goes to the block of the rank whose window holds it
-      const uint32_t g = ((t + 1) * world - 1) / L;
-      const uint32_t g0 = (g * L) / world, g1 = ((g + 1) * L) / world;
-      addrs[n_rows * g0 + r * (g1 - g0) + (t - g0)] = a;
+      const uint32_t g = ((t + 1) * out.world - 1) / L;
+      const uint32_t g0 = (g * L) / out.world, g1 = ((g + 1) * L) / out.world;
+      if (out.peers)
+        out.peers[g][(out.row0 + r) * (g1 - g0) + (t - g0)] = a;
+      else
+        out.addrs[n_rows * g0 + r * (g1 - g0) + (t - g0)] = a;
     }
   }
 }
@@ -84,8 +89,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
                                                    const uint32_t* __restrict__ col_idx,
                                                    uint64_t n_rows, uint32_t K, uint32_t L,
                                                    uint32_t range, HashKeys keys,
-                                                   uint32_t* __restrict__ codes,
-                                                   uint32_t* __restrict__ addrs, uint32_t world,
+                                                   uint32_t* __restrict__ codes, AddrOut out,
                                                    int64_t skip_le) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
       for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = code[i];
 
     // ---- H3: L table addresses ----
-    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
+    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, out, n_rows, r, lane);
     __syncwarp();
   };
 
@@ -244,8 +248,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
                                                           const uint32_t* __restrict__ col_idx,
                                                           uint64_t n_rows, uint32_t K, uint32_t L,
                                                           uint32_t range, HashKeys keys,
-                                                          uint32_t* __restrict__ codes,
-                                                          uint32_t* __restrict__ addrs, uint32_t world) {
+                                                          uint32_t* __restrict__ codes, AddrOut out) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
     __syncwarp();
     if (kCodes)
       for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = code[i];
-    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, addrs, n_rows, r, world, lane);
+    if (kAddrs) write_addrs(code, nonempty, K, L, range, keys, out, n_rows, r, lane);
     __syncwarp();
    }
   }
@@ -332,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
 
 template <bool C, bool A>
 int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
-             uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-             uint32_t world, cudaStream_t s) {
+             uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
+             cudaStream_t s) {
   const uint32_t B = K * L;
   int launched = 0;
   int64_t skip_le = -1;
@@ -347,7 +350,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     const uint64_t need = (n_rows + kThreads - 1) / kThreads;  // 32 rows per warp-chunk
     if (blocks > need) blocks = need;
     k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                                 codes, addrs, world);
+                                                                 codes, out);
     ++launched;
     skip_le = kSparseNnz;
   }
@@ -365,19 +368,19 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return launched;
   k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                         codes, addrs, world, skip_le);
+                                                         codes, out, skip_le);
   return launched + 1;
 }
 
 }  // namespace
 
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
-                uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-                uint32_t world, cudaStream_t s) {
-  if (codes && addrs)
-    return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
-  if (codes) return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
-  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, addrs, world, s);
+                uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
+                cudaStream_t s) {
+  const bool addrs = out.addrs || out.peers;
+  if (codes && addrs) return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
+  if (codes) return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
+  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
 }
 
 }  // namespace flash

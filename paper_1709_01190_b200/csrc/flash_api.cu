@@ -1,5 +1,6 @@
 // flash_api.cu — the C ABI of libflash.so (include/flash.h): handle, validation,
-// handle-owned device arena, phase orchestration, profiling counters.
+// handle-owned device arena, phase orchestration, profiling counters.  The multi-GPU
+// handle's collective calls live in dist.cu.
 //
 // Every entry point validates on the host before enqueueing anything, enqueues on the
 // caller's stream, and returns without synchronizing (except where flash.h says so).
@@ -16,14 +17,42 @@
 #include <string>
 #include <vector>
 
+#include "dist.cuh"
 #include "flash.h"
 #include "flash_internal.cuh"
+#include "handle.cuh"
 
 using namespace flash;
+using namespace flash::api;
 
 namespace {
-
 thread_local std::string g_last_error;
+
+__global__ void k_table_off(const uint64_t* goff, uint32_t t, uint32_t range, uint32_t* off) {
+  const uint64_t base = goff[(uint64_t)t * range];
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= range; b += gridDim.x * blockDim.x)
+    off[b] = (uint32_t)(goff[(uint64_t)t * range + b] - base);
+}
+
+// flash_import_tables' consistency check: goff[0] == 0, goff non-decreasing, goff[nb] ==
+// n_ids (bad[0] counts violations), and the largest imported id (bad[1]).
+__global__ void k_import_check(const uint64_t* __restrict__ goff, uint64_t nb, const uint32_t* __restrict__ ids,
+                               uint64_t n_ids, unsigned long long* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long nbad = 0;
+  for (uint64_t i = i0; i < nb; i += stride)
+    if (goff[i + 1] < goff[i]) ++nbad;
+  if (i0 == 0 && (goff[0] != 0 || goff[nb] != n_ids)) ++nbad;
+  uint32_t mx = 0;
+  for (uint64_t i = i0; i < n_ids; i += stride) mx = ids[i] > mx ? ids[i] : mx;
+  if (nbad) atomicAdd(&bad[0], nbad);
+  if (mx) atomicMax(&bad[1], (unsigned long long)mx);
+}
+}  // namespace
+
+namespace flash {
+namespace api {
 
 flash_status fail(flash_status st, const char* fmt, ...) {
   char buf[512];
@@ -34,37 +63,6 @@ flash_status fail(flash_status st, const char* fmt, ...) {
   g_last_error = buf;
   return st;
 }
-
-#define CUDA_TRY(expr)                                                                 \
-  do {                                                                                 \
-    cudaError_t e_ = (expr);                                                           \
-    if (e_ != cudaSuccess) {                                                           \
-      cudaGetLastError();                                                              \
-      return fail(e_ == cudaErrorMemoryAllocation ? FLASH_ENOMEM : FLASH_ECUDA,        \
-                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
-    }                                                                                  \
-  } while (0)
-
-#define TRY(expr)                    \
-  do {                               \
-    flash_status st_ = (expr);       \
-    if (st_ != FLASH_OK) return st_; \
-  } while (0)
-
-struct PendingPhase {
-  int phase;
-  cudaEvent_t a, b;
-};
-
-// A grow-only device buffer.
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  template <typename T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-};
 
 flash_status ensure(DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
@@ -84,51 +82,6 @@ void release(DevBuf& b) {
   b.cap = 0;
 }
 
-}  // namespace
-
-struct flash_index {
-  uint32_t K, L, R, range;
-  uint32_t shared = 0;  // reservoir sharing (R#23): pool size P < L*range, or 0 (unshared)
-  uint64_t seed;
-  HashKeys keys;
-  int device;
-  uint32_t table_log2;
-  // tables: goff / ids double-buffered; `have_tables` false before the first insert
-  uint32_t* arrivals = nullptr;  // [L*range]
-  DevBuf goff[2], ids[2];
-  int cur = 0;
-  bool have_tables = false;
-  uint64_t kept_ub = 0;     // host upper bound on kept ids
-  uint64_t n_inserted = 0;  // rows passed to insert (host count)
-  uint64_t max_id = 0;      // largest id inserted so far (host count)
-  // scratch
-  DevBuf addrs, cursor, pool_cnt, pool_off, keep_cnt, pool, big_list, scan_tmp, qscratch, off_tmp;
-  DevBuf seg_off, xscan_tmp;  // flash_count_topk segment offsets; exchange scans
-  DevBuf addrsT;              // build: window addresses transposed to [W][n] (table-major passes)
-  DevBuf qhuge;               // query: global count tables of the L*R > 8192 class (kept clean)
-  DevBuf raddr, qraddr;       // shared mode: rows' / queries' distinct reservoir indices
-  DevBuf hbuf;                // build: slice histograms of the shared-memory passes
-  DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
-  unsigned long long* err = nullptr;
-  cudaStream_t last_stream = nullptr;
-  bool have_last = false;
-  cudaEvent_t order_ev = nullptr;
-  cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> copy_events;
-  cudaStream_t side_stream = nullptr;  // build: k_select_big of the early-listed buckets
-  cudaEvent_t side_fork = nullptr, side_join = nullptr;
-
-  // profiling
-  int profiling = 0;
-  std::vector<PendingPhase> pending;
-  double phase_ms[4] = {0, 0, 0, 0};
-  uint64_t phase_calls[4] = {0, 0, 0, 0};
-  uint64_t launches = 0;
-};
-
-namespace {
-
-// Order this call after everything previously enqueued on the handle.
 flash_status enter(const flash_index* hc, cudaStream_t s) {
   flash_index* h = const_cast<flash_index*>(hc);
   CUDA_TRY(cudaSetDevice(h->device));
@@ -141,27 +94,20 @@ flash_status enter(const flash_index* hc, cudaStream_t s) {
   return FLASH_OK;
 }
 
-struct Phase {
-  flash_index* h;
-  int phase;
-  cudaStream_t s;
-  cudaEvent_t a = nullptr, b = nullptr;
-  Phase(const flash_index* hc, int p, cudaStream_t st) : h(const_cast<flash_index*>(hc)), phase(p), s(st) {
-    if (h->profiling) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
-      cudaEventRecord(a, s);
-    }
+Phase::Phase(const flash_index* hc, int p, cudaStream_t st) : h(const_cast<flash_index*>(hc)), phase(p), s(st) {
+  if (h->profiling) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
   }
-  ~Phase() {
-    if (a) {
-      cudaEventRecord(b, s);
-      h->pending.push_back({phase, a, b});
-    }
+}
+Phase::~Phase() {
+  if (a) {
+    cudaEventRecord(b, s);
+    h->pending.push_back({phase, a, b});
   }
-};
+}
 
-// True when the GPU can dereference p (device, managed, or mapped host memory).
 bool device_accessible(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -178,28 +124,84 @@ bool device_accessible(const void* p) {
     if (!device_accessible(p)) return fail(FLASH_EINVAL, "%s is not a device pointer", #p); \
   } while (0)
 
-__global__ void k_table_off(const uint64_t* goff, uint32_t t, uint32_t range, uint32_t* off) {
-  const uint64_t base = goff[(uint64_t)t * range];
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= range; b += gridDim.x * blockDim.x)
-    off[b] = (uint32_t)(goff[(uint64_t)t * range + b] - base);
-}
-
-// buckets (reservoirs) the index holds: L*range, or the shared pool's P (R#23)
 uint64_t nbuckets(const flash_index* h) { return h->shared ? h->shared : (uint64_t)h->L * h->range; }
 
+flash_index* new_handle(uint32_t K, uint32_t L, uint32_t R, uint32_t range, uint64_t seed, uint32_t shared,
+                        flash_status* st, bool tables) {
+  *st = FLASH_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *st = fail(FLASH_ECUDA, "flash_create: %s", cudaGetErrorString(e));
+    return nullptr;
+  }
+  flash_index* h = new (std::nothrow) flash_index();
+  if (!h) {
+    *st = fail(FLASH_ENOMEM, "host allocation failed");
+    return nullptr;
+  }
+  h->K = K;
+  h->L = L;
+  h->R = R;
+  h->range = range;
+  h->seed = seed;
+  h->keys = derive_keys(seed);
+  h->device = dev;
+  h->shared = shared;
+  const size_t nb = !tables ? 1 : shared ? shared : (size_t)L * range;
+  e = cudaMalloc(&h->arrivals, sizeof(uint32_t) * (nb ? nb : 1));
+  if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * (nb ? nb : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess && ensure(h->zero, 16) == FLASH_OK) e = cudaMemset(h->zero.p, 0, 16);
+  if (e != cudaSuccess || !h->zero.p) {
+    cudaGetLastError();
+    free_handle(h);
+    *st = fail(e == cudaErrorMemoryAllocation ? FLASH_ENOMEM : FLASH_ECUDA, "flash_create: %s",
+               cudaGetErrorString(e));
+    return nullptr;
+  }
+  return h;
+}
+
+void free_handle(flash_index* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& p : h->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : h->copy_events) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  if (h->side_fork) cudaEventDestroy(h->side_fork);
+  if (h->side_join) cudaEventDestroy(h->side_join);
+  cudaFree(h->arrivals);
+  cudaFree(h->err);
+  for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
+                    &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->raddr, &h->qraddr, &h->hbuf, &h->h_rp, &h->h_col,
+                    &h->h_ids, &h->h_cnt, &h->zero})
+    release(*b);
+  if (h->order_ev) cudaEventDestroy(h->order_ev);
+  delete h;
+}
+
 flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n,
-                     uint32_t* codes, uint32_t* addrs, cudaStream_t s, uint32_t world = 1) {
+                     uint32_t* codes, const AddrOut& out, cudaStream_t s) {
   Phase ph(h, 0, s);
-  const_cast<flash_index*>(h)->launches +=
-      launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, addrs, world, s);
+  const_cast<flash_index*>(h)->launches += launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes,
+                                                       out, s);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }
 
-flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base,
-                             cudaStream_t s, uint32_t t0 = 0, uint32_t t1 = UINT32_MAX, bool cols = false,
-                             bool converted = false, void (*after_scan)(void*, cudaStream_t) = nullptr,
-                             void* after_scan_ctx = nullptr) {
+flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, uint32_t id_base, cudaStream_t s,
+                             uint32_t t0, uint32_t t1, bool cols, bool converted,
+                             void (*after_scan)(void*, cudaStream_t), void* after_scan_ctx) {
   if (t1 > h->L) t1 = h->L;
   const uint64_t nb = nbuckets(h);
   if (h->shared && !converted) {  // table addresses -> each row's distinct shared reservoirs
@@ -293,16 +295,6 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   return FLASH_OK;
 }
 
-// The L*R > 8192 query class keeps its count tables in global memory: allocated and
-// cleared on first use (the kernels leave them clean).
-flash_status ensure_huge_table(flash_index* h, cudaStream_t s) {
-  if ((uint64_t)h->L * h->R <= 8192 || h->qhuge.p) return FLASH_OK;
-  TRY(ensure(h->qhuge, query_huge_table_bytes()));
-  query_huge_table_init(h->qhuge.p, s);
-  CUDA_TRY(cudaGetLastError());
-  return FLASH_OK;
-}
-
 QueryArgs query_args(const flash_index* h, const uint32_t* addrs, uint64_t nq, uint32_t k, const uint32_t* exclude,
                      int exclude_self, uint32_t self_base, uint32_t* out_ids, uint32_t* out_counts, int cur) {
   QueryArgs a;
@@ -323,16 +315,26 @@ QueryArgs query_args(const flash_index* h, const uint32_t* addrs, uint64_t nq, u
   a.out_ids = out_ids;
   a.out_counts = out_counts;
   a.err = h->err;
-  a.table_log2 = h->table_log2;
-  a.packed = (h->max_id < 0xFFFFFEull && h->L <= 255) ? 1 : 0;
+  a.seg_len = nullptr;
+  a.mmax = (uint64_t)h->L * h->R;
   a.max_id = (uint32_t)h->max_id;
   return a;
 }
 
+flash_status run_query(flash_index* h, const QueryArgs& a, cudaStream_t s) {
+  const int n = launch_query(a, h->qscratch.p, s);
+  if (n < 0)
+    return fail(FLASH_ECUDA, "query kernels could not be launched for L=%u, R=%u, k=%u (shared memory)", h->L, h->R,
+                a.k);
+  h->launches += (uint64_t)n;
+  CUDA_TRY(cudaGetLastError());
+  return FLASH_OK;
+}
+
 flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64_t nq, uint32_t k,
                             const uint32_t* exclude, int exclude_self, uint32_t self_base,
-                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s, bool converted = false,
-                            bool planned = false) {
+                            uint32_t* out_ids, uint32_t* out_counts, cudaStream_t s, bool converted,
+                            bool planned) {
   flash_index* h = const_cast<flash_index*>(hc);
   if (h->shared && !converted && h->have_tables) {  // each distinct reservoir aggregated once
     TRY(ensure(h->qraddr, sizeof(uint32_t) * nq * h->L));
@@ -349,27 +351,24 @@ flash_status do_query_addrs(const flash_index* hc, const uint32_t* addrs, uint64
     return FLASH_OK;
   }
   TRY(ensure(h->qscratch, query_scratch_bytes(nq)));
-  TRY(ensure_huge_table(h, s));
   Phase ph(h, 2, s);
   QueryArgs a = query_args(h, addrs, nq, k, exclude, exclude_self, self_base, out_ids, out_counts, h->cur);
   a.planned = planned ? 1 : 0;
-  h->launches += launch_query(a, h->qscratch.p, h->qhuge.p, s);
-  CUDA_TRY(cudaGetLastError());
-  return FLASH_OK;
+  return run_query(h, a, s);
 }
 
 flash_status check_query_shape(const flash_index* h, uint32_t k) {
   if (k == 0 || k > FLASH_MAX_TOPK) return fail(FLASH_EINVAL, "k=%u outside [1, %u]", k, FLASH_MAX_TOPK);
-  if ((uint64_t)h->L * h->R > 32768)
-    return fail(FLASH_EINVAL, "L*R=%llu too large for the count tables (limit L*R <= 32768)",
-                (unsigned long long)h->L * h->R);
-  if (h->L > 4096) return fail(FLASH_EINVAL, "L=%u too large for the query kernel (limit 4096)", h->L);
-  if (query_smem_bytes(h->table_log2, h->L, k) > 227 * 1024)
+  if ((uint64_t)h->L * h->R > FLASH_MAX_CANDIDATES)
+    return fail(FLASH_EINVAL, "L*R=%llu too large for the count kernels (limit L*R <= %u)",
+                (unsigned long long)h->L * h->R, FLASH_MAX_CANDIDATES);
+  if (!query_shape_fits(h->L, h->R, k))
     return fail(FLASH_EINVAL, "query shared memory for L=%u, R=%u, k=%u exceeds 227 KB", h->L, h->R, k);
   return FLASH_OK;
 }
 
-}  // namespace
+}  // namespace api
+}  // namespace flash
 
 extern "C" {
 
@@ -393,58 +392,15 @@ flash_status flash_create_pool(uint32_t K, uint32_t L, uint32_t R, uint32_t rang
     return fail(FLASH_EINVAL, "pool=%llu exceeds L*range=%llu", (unsigned long long)pool,
                 (unsigned long long)L * range);
   const uint32_t shared = (pool == 0 || pool == (uint64_t)L * range) ? 0u : (uint32_t)pool;
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  flash_index* h = new (std::nothrow) flash_index();
-  if (!h) return fail(FLASH_ENOMEM, "host allocation failed");
-  h->K = K;
-  h->L = L;
-  h->R = R;
-  h->range = range;
-  h->seed = seed;
-  h->keys = derive_keys(seed);
-  h->device = dev;
-  h->table_log2 = query_table_log2(L, R);
-  h->shared = shared;
-  const size_t nb = shared ? shared : (size_t)L * range;
-  cudaError_t e = cudaMalloc(&h->arrivals, sizeof(uint32_t) * nb);
-  if (e == cudaSuccess) e = cudaMemset(h->arrivals, 0, sizeof(uint32_t) * nb);
-  if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    flash_destroy(h);
-    return fail(e == cudaErrorMemoryAllocation ? FLASH_ENOMEM : FLASH_ECUDA, "flash_create: %s",
-                cudaGetErrorString(e));
-  }
-  *out = h;
-  return FLASH_OK;
+  flash_status st;
+  *out = new_handle(K, L, R, range, seed, shared, &st);
+  return st;
 }
 
 void flash_destroy(flash_index* h) {
   if (!h) return;
-  cudaSetDevice(h->device);
-  cudaDeviceSynchronize();
-  for (auto& p : h->pending) {
-    cudaEventDestroy(p.a);
-    cudaEventDestroy(p.b);
-  }
-  for (auto e : h->copy_events) cudaEventDestroy(e);
-
-  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  if (h->side_stream) cudaStreamDestroy(h->side_stream);
-  if (h->side_fork) cudaEventDestroy(h->side_fork);
-  if (h->side_join) cudaEventDestroy(h->side_join);
-  cudaFree(h->arrivals);
-  cudaFree(h->err);
-  for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
-                    &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->qhuge, &h->raddr, &h->qraddr, &h->hbuf,
-                    &h->h_rp, &h->h_col, &h->h_ids, &h->h_cnt})
-    release(*b);
-  if (h->order_ev) cudaEventDestroy(h->order_ev);
-  delete h;
+  if (h->dist) dist_destroy(h);
+  free_handle(h);
 }
 
 flash_status flash_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
@@ -458,12 +414,13 @@ flash_status flash_hash(const flash_index* h, const int64_t* row_ptr, const uint
   if (addrs) REQUIRE_DEV(addrs);
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
-  return do_hash(h, row_ptr, col_idx, n_rows, codes, addrs, s);
+  return do_hash(h, row_ptr, col_idx, n_rows, codes, addr_out(addrs), s);
 }
 
 flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
                                 void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return fail(FLASH_ESTATE, "flash_insert_addrs: not a call of a multi-GPU handle");
   if (n_rows == 0) return FLASH_OK;
   REQUIRE_DEV(addrs);
   if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
@@ -476,6 +433,7 @@ flash_status flash_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t 
 flash_status flash_insert_addrs_window(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
                                        uint32_t t_begin, uint32_t t_end, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return fail(FLASH_ESTATE, "flash_insert_addrs_window: not a call of a multi-GPU handle");
   if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L) return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
   if (n_rows == 0) return FLASH_OK;
@@ -491,6 +449,7 @@ flash_status flash_table_arrays(const flash_index* hc, const uint64_t** goff, co
                                 const uint32_t** arrivals, uint64_t* n_ids) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->dist) return fail(FLASH_ESTATE, "flash_table_arrays: a multi-GPU handle holds only its table window");
   if (!h->have_tables) return fail(FLASH_ESTATE, "nothing inserted yet");
   CUDA_TRY(cudaSetDevice(h->device));
   if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
@@ -505,14 +464,31 @@ flash_status flash_table_arrays(const flash_index* hc, const uint64_t** goff, co
 }
 
 flash_status flash_import_tables(flash_index* h, const uint64_t* goff, const uint32_t* ids, uint64_t n_ids,
-                                 const uint32_t* arrivals, uint32_t max_id, void* stream) {
+                                 const uint32_t* arrivals, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return fail(FLASH_ESTATE, "flash_import_tables: not a call of a multi-GPU handle");
   REQUIRE_DEV(goff);
   if (n_ids) REQUIRE_DEV(ids);
   if (arrivals) REQUIRE_DEV(arrivals);
+  if (n_ids >= 0x100000000ull * 64) return fail(FLASH_EINVAL, "n_ids=%llu too large", (unsigned long long)n_ids);
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
   const uint64_t nb = nbuckets(h);
+  // validate the offsets and find the largest id before anything changes (synchronizes)
+  TRY(ensure(h->off_tmp, 2 * sizeof(unsigned long long)));
+  unsigned long long* chk = h->off_tmp.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(chk, 0, 2 * sizeof(unsigned long long), s));
+  const uint64_t work = nb > n_ids ? nb : n_ids;
+  const unsigned blocks = (unsigned)((work + 255) / 256 < (uint64_t)device_sms() * 8 ? (work + 255) / 256
+                                                                                   : (uint64_t)device_sms() * 8);
+  k_import_check<<<blocks ? blocks : 1, 256, 0, s>>>(goff, nb, n_ids ? ids : h->zero.as<uint32_t>(), n_ids, chk);
+  h->launches++;
+  unsigned long long hv[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hv, chk, sizeof hv, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (hv[0])
+    return fail(FLASH_EINVAL, "flash_import_tables: goff must start at 0, be non-decreasing and end at n_ids=%llu",
+                (unsigned long long)n_ids);
   const int nxt = h->have_tables ? 1 - h->cur : h->cur;
   TRY(ensure(h->goff[nxt], sizeof(uint64_t) * (nb + 1)));
   TRY(ensure(h->ids[nxt], sizeof(uint32_t) * (n_ids ? n_ids : 1)));
@@ -525,30 +501,34 @@ flash_status flash_import_tables(flash_index* h, const uint64_t* goff, const uin
   h->cur = nxt;
   h->have_tables = true;
   h->kept_ub = n_ids;
-  h->max_id = max_id;
-  h->n_inserted = (uint64_t)max_id + 1;
+  h->max_id = hv[1];
+  h->n_inserted = hv[1] + 1;
   return FLASH_OK;
 }
 
 flash_status flash_insert(flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows,
                           uint32_t id_base, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
-  if (n_rows == 0) return FLASH_OK;
-  REQUIRE_DEV(row_ptr);
-  REQUIRE_DEV(col_idx);
+  if (n_rows == 0 && !h->dist) return FLASH_OK;  // (a multi-GPU insert is collective: every rank calls)
+  if (n_rows) {
+    REQUIRE_DEV(row_ptr);
+    REQUIRE_DEV(col_idx);
+  }
   if ((uint64_t)id_base + n_rows - 1 >= 0xFFFFFFFFull)
     return fail(FLASH_EINVAL, "ids id_base..id_base+n_rows-1 must stay below 0xFFFFFFFF");
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->dist) return dist_insert(h, row_ptr, col_idx, n_rows, id_base, s);
   TRY(enter(h, s));
   TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
   uint32_t* addrs = h->addrs.as<uint32_t>();
-  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
+  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addr_out(addrs), s));
   return do_insert_addrs(h, addrs, n_rows, id_base, s);
 }
 
 flash_status flash_query_addrs(const flash_index* h, const uint32_t* addrs, uint64_t n_q, uint32_t k,
                                const uint32_t* exclude, uint32_t* out_ids, uint32_t* out_counts, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return fail(FLASH_ESTATE, "flash_query_addrs: not a call of a multi-GPU handle");
   TRY(check_query_shape(h, k));
   if (n_q == 0) return FLASH_OK;
   REQUIRE_DEV(addrs);
@@ -566,17 +546,20 @@ flash_status flash_query_topk(const flash_index* hc, const int64_t* row_ptr, con
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
   TRY(check_query_shape(h, k));
-  if (n_q == 0) return FLASH_OK;
-  REQUIRE_DEV(row_ptr);
-  REQUIRE_DEV(col_idx);
-  REQUIRE_DEV(out_ids);
-  REQUIRE_DEV(out_counts);
-  if (exclude) REQUIRE_DEV(exclude);
+  if (n_q == 0 && !h->dist) return FLASH_OK;
+  if (n_q) {
+    REQUIRE_DEV(row_ptr);
+    REQUIRE_DEV(col_idx);
+    REQUIRE_DEV(out_ids);
+    REQUIRE_DEV(out_counts);
+    if (exclude) REQUIRE_DEV(exclude);
+  }
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->dist) return dist_query_topk(h, row_ptr, col_idx, n_q, k, exclude, out_ids, out_counts, s);
   TRY(enter(h, s));
   TRY(ensure(h->addrs, sizeof(uint32_t) * n_q * h->L));
   uint32_t* addrs = h->addrs.as<uint32_t>();
-  TRY(do_hash(h, row_ptr, col_idx, n_q, nullptr, addrs, s));
+  TRY(do_hash(h, row_ptr, col_idx, n_q, nullptr, addr_out(addrs), s));
   return do_query_addrs(h, addrs, n_q, k, exclude, 0, 0, out_ids, out_counts, s);
 }
 
@@ -585,17 +568,20 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
   if (h->have_tables || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph needs a fresh handle");
   TRY(check_query_shape(h, k));
-  if (n_rows == 0) return FLASH_OK;
+  if (n_rows == 0 && !h->dist) return FLASH_OK;
   if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
-  REQUIRE_DEV(row_ptr);
-  REQUIRE_DEV(col_idx);
-  REQUIRE_DEV(out_ids);
-  REQUIRE_DEV(out_counts);
+  if (n_rows) {
+    REQUIRE_DEV(row_ptr);
+    REQUIRE_DEV(col_idx);
+    REQUIRE_DEV(out_ids);
+    REQUIRE_DEV(out_counts);
+  }
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->dist) return dist_knn_graph(h, row_ptr, col_idx, n_rows, k, out_ids, out_counts, s);
   TRY(enter(h, s));
   TRY(ensure(h->addrs, sizeof(uint32_t) * n_rows * h->L));
   uint32_t* addrs = h->addrs.as<uint32_t>();
-  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s));
+  TRY(do_hash(h, row_ptr, col_idx, n_rows, nullptr, addr_out(addrs), s));
   if (h->shared) {  // the rows' distinct reservoirs are the queries' too
     TRY(do_insert_addrs(h, addrs, n_rows, 0, s));
     return do_query_addrs(h, h->raddr.as<uint32_t>(), n_rows, k, nullptr, 1, 0, out_ids, out_counts, s, true);
@@ -604,7 +590,6 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
   // it runs on the build's side stream as soon as the offsets are scanned, beside the
   // scatter and selects; the build joins it before returning.
   TRY(ensure(h->qscratch, query_scratch_bytes(n_rows)));
-  TRY(ensure_huge_table(h, s));
   struct PlanCtx {
     flash_index* h;
     QueryArgs a;
@@ -628,10 +613,11 @@ flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const 
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
   if (h->have_tables || h->n_inserted) return fail(FLASH_ESTATE, "flash_knn_graph_host needs a fresh handle");
   TRY(check_query_shape(h, k));
-  if (n_rows == 0) return FLASH_OK;
+  if (n_rows == 0 && !h->dist) return FLASH_OK;
   if (n_rows >= 0xFFFFFFFFull) return fail(FLASH_EINVAL, "n_rows must be < 2^32-1");
-  if (!row_ptr || !col_idx || !out_ids || !out_counts) return fail(FLASH_EINVAL, "NULL buffer");
+  if (!row_ptr || (n_rows && (!col_idx || !out_ids || !out_counts))) return fail(FLASH_EINVAL, "NULL buffer");
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->dist) return dist_knn_graph_host(h, row_ptr, col_idx, n_rows, k, out_ids, out_counts, s);
   TRY(enter(h, s));
   const int64_t nnz_begin = row_ptr[0], nnz_end = row_ptr[n_rows];
   if (nnz_end < nnz_begin) return fail(FLASH_EINVAL, "row_ptr must be non-decreasing");
@@ -688,7 +674,7 @@ flash_status flash_knn_graph_host(flash_index* h, const int64_t* row_ptr, const 
     }
     CUDA_TRY(cudaEventRecord(ev, cs));
     CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
-    TRY(do_hash(h, d_rp + r0, d_col_abs, r1 - r0, nullptr, d_addrs + r0 * h->L, s));
+    TRY(do_hash(h, d_rp + r0, d_col_abs, r1 - r0, nullptr, addr_out(d_addrs + r0 * h->L), s));
     r0 = r1;
   }
   TRY(do_insert_addrs(h, d_addrs, n_rows, 0, s));
@@ -715,12 +701,13 @@ flash_status flash_hash_blocked(const flash_index* h, const int64_t* row_ptr, co
   REQUIRE_DEV(addrs);
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enter(h, s));
-  return do_hash(h, row_ptr, col_idx, n_rows, nullptr, addrs, s, world);
+  return do_hash(h, row_ptr, col_idx, n_rows, nullptr, addr_out(addrs, world), s);
 }
 
 flash_status flash_insert_addrs_cols(flash_index* h, const uint32_t* addrs, uint64_t n_rows, uint32_t id_base,
                                      uint32_t t_begin, uint32_t t_end, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return fail(FLASH_ESTATE, "flash_insert_addrs_cols: not a call of a multi-GPU handle");
   if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin >= t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) must be non-empty and inside [0, %u)", t_begin, t_end, h->L);
@@ -737,6 +724,7 @@ flash_status flash_window_sizes(const flash_index* hc, const uint32_t* addrs, ui
                                 uint32_t t_end, uint32_t* sizes, uint64_t* offsets, void* stream) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->dist) return fail(FLASH_ESTATE, "flash_window_sizes: not a call of a multi-GPU handle");
   if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
@@ -764,6 +752,7 @@ flash_status flash_window_gather(const flash_index* hc, const uint32_t* addrs, u
                                  uint32_t t_end, const uint64_t* offsets, uint32_t* out_ids, void* stream) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->dist) return fail(FLASH_ESTATE, "flash_window_gather: not a call of a multi-GPU handle");
   if (h->shared) return fail(FLASH_EINVAL, "table windows are undefined when tables share reservoirs (R#23)");
   if (t_begin > t_end || t_end > h->L)
     return fail(FLASH_EINVAL, "table window [%u, %u) outside [0, %u)", t_begin, t_end, h->L);
@@ -785,6 +774,7 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
                               uint32_t* out_ids, uint32_t* out_counts, void* stream) {
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
+  if (h->dist) return fail(FLASH_ESTATE, "flash_count_topk: not a call of a multi-GPU handle");
   TRY(check_query_shape(h, k));
   if (n_seg < 1 || n_seg > 4096) return fail(FLASH_EINVAL, "n_seg=%u outside [1, 4096]", n_seg);
   if (n_q >= 0x80000000ull) return fail(FLASH_EINVAL, "n_q must be < 2^31");
@@ -800,7 +790,6 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
   TRY(ensure(h->seg_off, sizeof(uint64_t) * (nsq + 1)));
   TRY(ensure(h->xscan_tmp, scan_u32_to_u64_tmp_bytes(nsq)));
   TRY(ensure(h->qscratch, query_scratch_bytes(n_q)));
-  TRY(ensure_huge_table(h, s));
   Phase ph(h, 2, s);
   launch_scan_sizes(seg_sizes, nsq, h->seg_off.as<uint64_t>(), h->xscan_tmp.p, h->xscan_tmp.cap, s);
   QueryArgs a;
@@ -808,8 +797,8 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
   a.addrs = nullptr;
   a.nq = n_q;
   a.goff = h->seg_off.as<uint64_t>();
-  static const uint32_t kNoCand = 0;
-  a.ids = cand ? cand : &kNoCand;  // every segment is empty when cand is NULL (never dereferenced)
+  // cand == NULL: every segment must be empty (a non-empty one would read the 16 zero bytes)
+  a.ids = cand ? cand : h->zero.as<uint32_t>();
   a.L = n_seg;
   a.range = (uint32_t)n_q;
   a.k = k;
@@ -820,17 +809,16 @@ flash_status flash_count_topk(const flash_index* hc, const uint32_t* cand, const
   a.out_ids = out_ids;
   a.out_counts = out_counts;
   a.err = h->err;
-  a.table_log2 = h->table_log2;
-  a.packed = (max_id < 0xFFFFFEu && h->L <= 255) ? 1 : 0;
+  a.seg_len = nullptr;
+  a.mmax = cand ? (uint64_t)h->L * h->R : 0;  // NULL cand: any candidate is an error (pads)
   a.max_id = max_id;
-  h->launches += launch_query(a, h->qscratch.p, h->qhuge.p, s);
-  CUDA_TRY(cudaGetLastError());
-  return FLASH_OK;
+  return run_query(h, a, s);
 }
 
 flash_status flash_clear(flash_index* h, void* stream) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
   cudaStream_t s = (cudaStream_t)stream;
+  if (h->dist) return dist_clear(h, s);
   TRY(enter(h, s));
   CUDA_TRY(cudaMemsetAsync(h->arrivals, 0, sizeof(uint32_t) * nbuckets(h), s));
   h->have_tables = false;
@@ -845,6 +833,7 @@ flash_status flash_get_table(const flash_index* hc, uint32_t t, const uint32_t**
   if (!hc) return fail(FLASH_EINVAL, "handle is NULL");
   flash_index* h = const_cast<flash_index*>(hc);
   if (t >= h->L) return fail(FLASH_EINVAL, "table %u >= L=%u", t, h->L);
+  if (h->dist) return dist_get_table(h, t, off, ids, arrivals, n_ids);
   if (h->shared) return fail(FLASH_ESTATE, "tables share reservoirs: use flash_table_arrays");
   if (!h->have_tables) return fail(FLASH_ESTATE, "nothing inserted yet");
   CUDA_TRY(cudaSetDevice(h->device));
@@ -868,6 +857,7 @@ flash_status flash_get_table(const flash_index* hc, uint32_t t, const uint32_t**
 
 flash_status flash_check(const flash_index* h, uint64_t* n_errors) {
   if (!h) return fail(FLASH_EINVAL, "handle is NULL");
+  if (h->dist) return dist_check(h, n_errors);
   CUDA_TRY(cudaSetDevice(h->device));
   if (h->have_last) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
   unsigned long long e = 0;

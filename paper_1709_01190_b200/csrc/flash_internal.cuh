@@ -21,6 +21,8 @@ struct HashKeys {
   uint32_t s_addr;              // K-tuple -> address key (R#5)
   uint32_t s_pool;              // shared-reservoir binding key (R#23)
   uint64_t s_prio;              // bottom-R priority key (R#9)
+  uint32_t tbase;               // global index of local table 0 (a multi-GPU table window; else 0):
+                                // priorities are keyed by the GLOBAL table index
 };
 
 __host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
@@ -49,6 +51,7 @@ inline HashKeys derive_keys(uint64_t seed) {
   s.s_addr = (uint32_t)w[2];
   s.s_pool = (uint32_t)(w[2] >> 32);
   s.s_prio = w[3];
+  s.tbase = 0;
   return s;
 }
 
@@ -63,9 +66,10 @@ __device__ __forceinline__ uint32_t shared_reservoir(const HashKeys& k, uint32_t
   return __umulhi(fmix32(fmix32(k.s_pool ^ t) ^ b), P);
 }
 
-// prio(t, b, id) = hi32(mix64(tb ^ id)) with tb = mix64(s_prio ^ (t<<32 | b)).
+// prio(t, b, id) = hi32(mix64(tb ^ id)) with tb = mix64(s_prio ^ (t<<32 | b)), t the global
+// table index (local table index + tbase).
 __device__ __forceinline__ uint64_t prio_bucket_key(const HashKeys& k, uint32_t t, uint32_t b) {
-  return mix64(k.s_prio ^ (((uint64_t)t << 32) | (uint64_t)b));
+  return mix64(k.s_prio ^ (((uint64_t)(t + k.tbase) << 32) | (uint64_t)b));
 }
 __device__ __forceinline__ uint32_t prio_of(uint64_t tb, uint32_t id) {
   return (uint32_t)(mix64(tb ^ (uint64_t)id) >> 32);
@@ -81,13 +85,24 @@ uint32_t device_sms();
 // Launchers (each returns the number of kernels it launched).
 // ---------------------------------------------------------------------------
 
-// H1-H3: DOPH bin minima, densification, addresses.  codes / addrs may be null.
-// world > 1: addrs is written owner-blocked for a floor-block partition of the L tables
-// over `world` ranks (table window of rank g: [floor(gL/world), floor((g+1)L/world))):
-// rank g's block [n_rows][L_g] starts at element n_rows * t0(g).  world == 1: [n_rows][L].
+// Where the hash writes the L addresses of each row.
+struct AddrOut {
+  uint32_t* addrs;         // world == 1: [n_rows][L]; world > 1 (peers null): owner-blocked for a
+                           // floor-block partition of the L tables over `world` ranks (table window
+                           // of rank g: [floor(gL/world), floor((g+1)L/world))), rank g's block
+                           // [n_rows][L_g] starting at element n_rows * t0(g)
+  uint32_t* const* peers;  // or (dist mode, device array [world]): rank g's window-address buffer
+                           // [N][L_g]; this call's row r is global row row0 + r
+  uint64_t row0;
+  uint32_t world;
+};
+inline AddrOut addr_out(uint32_t* addrs, uint32_t world = 1) { return AddrOut{addrs, nullptr, 0, world}; }
+
+// H1-H3: DOPH bin minima, densification, addresses.  codes may be null; addresses are
+// written when out.addrs or out.peers is set.
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
-                uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, uint32_t* addrs,
-                uint32_t world, cudaStream_t s);
+                uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
+                cudaStream_t s);
 
 // Reservoir sharing (R#23): addrs [n][L] -> reservoir indices [n][L]: entry (r, t) is
 // shared_reservoir(t, addrs[r][t]) unless the address is EMPTY/invalid or an earlier table of
@@ -159,24 +174,24 @@ struct QueryArgs {
   uint32_t* out_ids;
   uint32_t* out_counts;
   unsigned long long* err;
-  uint32_t table_log2;      // worst-case count-table slots = 2^table_log2 (from L*R)
-  int packed;               // every inserted id < 2^24-1 and L <= 255: u32 (id, count) entries
+  const uint32_t* seg_len;  // direct mode only (or null): segment i has seg_len[i] ids starting at
+                            // goff[i] (segments need not be contiguous); null: goff[i+1] - goff[i]
+  uint64_t mmax;            // a query has at most mmax = L*R candidates (more: error counter + pads)
   uint32_t max_id;          // largest id inserted (the sort kernel's digit range)
   int planned;              // launch_query_plan already ran for these queries (skip it)
 };
-// scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists)
-// huge_tab: query_huge_table_bytes() of global memory initialised once with
-// query_huge_table_init (kept clean by the kernels), needed only when L*R > 8192
-int launch_query(const QueryArgs& a, void* scratch, void* huge_tab, cudaStream_t s);
+// scratch: query_scratch_bytes(nq) bytes of device memory (size-class lists).  Returns the
+// number of kernels launched, or -1 if some size class could not be launched.
+int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s);
 // the size-class planning step of launch_query alone (needs only addrs and goff)
 int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s);
-size_t query_huge_table_bytes();
-void query_huge_table_init(void* gtab, cudaStream_t s);
 size_t query_scratch_bytes(uint64_t nq);
+// every size class of an index with L tables, R per bucket, top-k has a kernel that fits
+// (L*R <= FLASH_MAX_CANDIDATES and the CTA sort kernel's shared memory fits)
+bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k);
 // radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
                       cudaStream_t s);
-size_t query_smem_bytes(uint32_t table_log2, uint32_t L, uint32_t k);
 
 // Candidate exchange, sender side (exchange.cu).  addrs: [n][t1-t0] (a table window's
 // columns).  sizes[q] = sum of the window buckets' sizes; off = exclusive scan (n+1).
@@ -191,6 +206,5 @@ int launch_window_gather(const uint32_t* addrs, uint64_t n, uint32_t t0, uint32_
 // exclusive scan of n uint32 sizes into n+1 uint64 offsets
 int launch_scan_sizes(const uint32_t* sizes, uint64_t n, uint64_t* off, void* scan_tmp, size_t scan_tmp_bytes,
                       cudaStream_t s);
-uint32_t query_table_log2(uint32_t L, uint32_t R);
 
 }  // namespace flash

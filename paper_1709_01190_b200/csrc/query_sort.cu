@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(32 * NW) k_query_sort(QueryArgs a, const uint3
         if (ad < (a.shared ? a.shared : a.range)) {
           const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)t * a.range + ad;
           st = a.goff[i];
-          sz = (uint32_t)(a.goff[i + 1] - st);
+          sz = a.seg_len ? a.seg_len[i] : (uint32_t)(a.goff[i + 1] - st);
         }
       }
       uint32_t x = sz;
@@ -489,7 +489,7 @@ int launch_sort_nw(const QueryArgs& a, const uint32_t* list, const uint32_t* cou
   if (!ensure_smem_attr((const void*)k_query_sort<MCAP, BL, NW>, smem)) return 0;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sort<MCAP, BL, NW>, 32 * NW, smem);
-  if (per_sm < 1) per_sm = 1;
+  if (per_sm < 1) return 0;  // the caller runs the class on the CTA sort kernel instead
   uint64_t grid = (uint64_t)device_sms() * per_sm;
   const uint64_t need = (a.nq + NW - 1) / NW;
   if (grid > need) grid = need;
@@ -534,7 +534,7 @@ int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, c
   // when it is the top class — L*R <= 2048, saturated buckets put most queries there
   // (friendster graph query 1494 -> 1358 ms) — else 2048 bins (fewer inversions; webspam)
   if (mcap <= 2048)
-    return (1u << (a.table_log2 - 1)) <= 2048 ? launch_sort_t<2048, 10>(a, list, count, s)
+    return a.mmax <= 2048 ? launch_sort_t<2048, 10>(a, list, count, s)
                                               : launch_sort_t<2048, 11>(a, list, count, s);
   if (mcap <= 3072) return launch_sort_t<3072, 11>(a, list, count, s);
   return launch_sort_t<4096, 11>(a, list, count, s);

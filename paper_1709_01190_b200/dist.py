@@ -1,4 +1,18 @@
-"""Multi-GPU orchestration of the k-NN graph (one process per GPU; plumbing only).
+"""Multi-GPU plumbing (one process per GPU).
+
+The product path is the multi-GPU handle of libflash.so (include/flash.h
+flash_create_dist; csrc/dist.cu): the L tables partitioned over the GPUs, addresses and
+candidate lists exchanged as peer stores inside the library's kernels, stream-ordered NCCL
+barriers.  Python only bootstraps it: ``create_dist_index`` broadcasts the NCCL unique id
+(torch.distributed, any backend) and wraps the rank's handle.
+
+The schedules below are the same partitioning written against torch.distributed
+collectives and the single-GPU C ABI: ``knn_graph_replicated`` is the multi-GPU path of an
+index with reservoir sharing (F < 1: a shared pool does not partition by table), and
+``knn_graph_candidate_exchange`` / ``knn_graph_sharded_build`` are the torch-collective
+formulations of the table partition, kept as the CPU (gloo) model of the exchange in
+tests/test_dist_gloo.py.
+
 
 Replicated-table mode: rank g holds a contiguous, nnz-balanced row
 shard; it hashes its own rows (H1-H3), the L addresses of every row are all-gathered
@@ -16,6 +30,26 @@ from __future__ import annotations
 import numpy as np
 import torch
 import torch.distributed as dist
+
+
+def bootstrap_unique_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id (flash_get_unique_id); every rank receives it
+    (torch.distributed.broadcast_object_list: works over gloo and NCCL process groups)."""
+    from paper_1709_01190_b200 import flash
+
+    obj = [flash.flash_get_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def create_dist_index(K: int, L: int, R: int, range_: int, seed: int, group=None):
+    """This rank's FlashIndex of a multi-GPU handle (flash_create_dist, collective) on the
+    current CUDA device; world / rank from the torch.distributed group."""
+    from paper_1709_01190_b200 import flash
+
+    uid = bootstrap_unique_id(group)
+    h = flash.flash_create_dist(K, L, R, range_, seed, dist.get_rank(group), dist.get_world_size(group), uid)
+    return flash.FlashIndex(K, L, R, range_, seed, handle=h)
 
 
 def shard_bounds(row_lengths: np.ndarray, world: int) -> list[int]:
@@ -119,7 +153,7 @@ def knn_graph_sharded_build(index, row_ptr_local, col_idx_local, k: int, bounds:
     parts.append(torch.tensor([base], dtype=torch.int64, device=goff.device))
     full_goff = torch.cat(parts).contiguous()
     full_ids = torch.cat(idss).contiguous() if base else torch.zeros(0, dtype=ids.dtype, device=ids.device)
-    index.import_tables(full_goff, full_ids, arr.contiguous(), n_total - 1)
+    index.import_tables(full_goff, full_ids, arr.contiguous())
     excl = torch.arange(bounds[rank], bounds[rank] + n_local, dtype=torch.int64,
                         device=addrs_local.device).to(torch.int32)
     return index.query_addrs(addrs_local, k, excl)                             # Q1-Q3 (own rows)

@@ -34,8 +34,10 @@ EXPORTS = (
     "flash_table_arrays", "flash_import_tables", "flash_set_profiling", "flash_phase_ms",
     "flash_launch_count", "flash_reset_counters", "flash_last_error",
     "flash_hash_blocked", "flash_insert_addrs_cols", "flash_window_sizes", "flash_window_gather",
-    "flash_count_topk", "flash_create_pool",
+    "flash_count_topk", "flash_create_pool", "flash_get_unique_id", "flash_create_dist",
+    "flash_create_dist_local", "flash_dist_info",
 )
+UNIQUE_ID_BYTES = 128
 
 
 class FlashError(RuntimeError):
@@ -74,7 +76,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.flash_insert_addrs_window.argtypes = [vp, vp, u64, u32, u32, u32, vp]
     L.flash_table_arrays.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                                      ctypes.POINTER(u64)]
-    L.flash_import_tables.argtypes = [vp, vp, vp, u64, vp, u32, vp]
+    L.flash_import_tables.argtypes = [vp, vp, vp, u64, vp, vp]
     L.flash_set_profiling.argtypes = [vp, i32]
     L.flash_phase_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
     L.flash_launch_count.argtypes = [vp]
@@ -85,6 +87,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.flash_window_sizes.argtypes = [vp, vp, u64, u32, u32, vp, vp, vp]
     L.flash_window_gather.argtypes = [vp, vp, u64, u32, u32, vp, vp, vp]
     L.flash_count_topk.argtypes = [vp, vp, vp, u32, u64, u32, vp, u32, vp, vp, vp]
+    L.flash_get_unique_id.argtypes = [vp]
+    L.flash_create_dist.argtypes = [u32, u32, u32, u32, u64, i32, i32, vp, ctypes.POINTER(vp)]
+    L.flash_create_dist_local.argtypes = [u32, u32, u32, u32, u64, i32, vp, vp]
+    L.flash_dist_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(u32),
+                                  ctypes.POINTER(u32)]
     L.flash_last_error.argtypes = []
     L.flash_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -224,9 +231,49 @@ def flash_table_arrays(h):
     return g.value, i.value, a.value, n.value
 
 
-def flash_import_tables(h, goff, ids, n_ids, arrivals, max_id, stream=None):
-    _check(load_library().flash_import_tables(h, _ptr(goff), _ptr(ids), n_ids, _ptr(arrivals), max_id,
+def flash_import_tables(h, goff, ids, n_ids, arrivals, stream=None):
+    _check(load_library().flash_import_tables(h, _ptr(goff), _ptr(ids), n_ids, _ptr(arrivals),
                                               _stream(stream, goff)))
+
+
+def flash_get_unique_id() -> bytes:
+    """NCCL bootstrap id (FLASH_UNIQUE_ID_BYTES) for flash_create_dist; rank 0 makes it."""
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    _check(load_library().flash_get_unique_id(buf))
+    return buf.raw
+
+
+def flash_create_dist(K: int, L: int, R: int, range_: int, seed: int, rank: int, world: int,
+                      unique_id: bytes) -> int:
+    """Collective: rank `rank` of a multi-GPU handle on the current device (NCCL)."""
+    torch.cuda.current_device()
+    if len(unique_id) != UNIQUE_ID_BYTES:
+        raise ValueError(f"unique_id must be {UNIQUE_ID_BYTES} bytes")
+    buf = ctypes.create_string_buffer(bytes(unique_id), UNIQUE_ID_BYTES)
+    h = ctypes.c_void_p()
+    _check(load_library().flash_create_dist(K, L, R, range_, seed & 0xFFFFFFFFFFFFFFFF, rank, world, buf,
+                                            ctypes.byref(h)))
+    return h.value
+
+
+def flash_create_dist_local(K: int, L: int, R: int, range_: int, seed: int, world: int,
+                            devices=None) -> list[int]:
+    """`world` virtual ranks in this process (devices: list of device indices, or None = the
+    current device for every rank).  Each rank's collective calls come from its own thread."""
+    torch.cuda.current_device()
+    hs = (ctypes.c_void_p * world)()
+    dev = (ctypes.c_int * world)(*devices) if devices is not None else None
+    _check(load_library().flash_create_dist_local(K, L, R, range_, seed & 0xFFFFFFFFFFFFFFFF, world,
+                                                  dev, hs))
+    return [hs[g] for g in range(world)]
+
+
+def flash_dist_info(h):
+    """(rank, world, t_begin, t_end) of a handle."""
+    r, w = ctypes.c_int(), ctypes.c_int()
+    t0, t1 = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(load_library().flash_dist_info(h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(t0), ctypes.byref(t1)))
+    return r.value, w.value, t0.value, t1.value
 
 
 def flash_hash_blocked(h, row_ptr, col_idx, n_rows, world, addrs, stream=None):
@@ -309,14 +356,23 @@ def _copy_device(ptr: int, n: int, device, typestr: str = "<i4") -> torch.Tensor
 class FlashIndex:
     """Owns one flash_index handle (device = the current CUDA device)."""
 
-    def __init__(self, K: int, L: int, R: int, range_: int, seed: int, F: float = 1.0, pool: int | None = None):
+    def __init__(self, K: int, L: int, R: int, range_: int, seed: int, F: float = 1.0, pool: int | None = None,
+                 handle: int | None = None):
         """F < 1 (or an explicit pool < L*range): reservoir sharing over a pool of
-        ceil(F*L*range) reservoirs (R#23)."""
+        ceil(F*L*range) reservoirs (R#23).  handle: adopt an existing handle (e.g. a
+        multi-GPU rank from flash_create_dist / dist.create_dist_index)."""
         self.K, self.L, self.R, self.range, self.seed = K, L, R, range_, seed
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.pool = int(pool) if pool is not None else (pool_size(F, L, range_) if F < 1.0 else L * range_)
-        self.h = (flash_create_pool(K, L, R, range_, self.pool, seed) if self.pool < L * range_
-                  else flash_create(K, L, R, range_, seed))
+        if handle is not None:
+            self.h = handle
+        else:
+            self.h = (flash_create_pool(K, L, R, range_, self.pool, seed) if self.pool < L * range_
+                      else flash_create(K, L, R, range_, seed))
+
+    def dist_info(self):
+        """(rank, world, t_begin, t_end): this handle's rank and table window."""
+        return flash_dist_info(self.h)
 
     def close(self):
         if getattr(self, "h", None):
@@ -345,17 +401,17 @@ class FlashIndex:
     def hash_addrs(self, row_ptr, col_idx):
         return self.hash(row_ptr, col_idx, codes=False)[1]
 
-    def insert(self, row_ptr, col_idx, id_base=0):
-        flash_insert(self.h, row_ptr, col_idx, row_ptr.numel() - 1, id_base)
+    def insert(self, row_ptr, col_idx, id_base=0, stream=None):
+        flash_insert(self.h, row_ptr, col_idx, row_ptr.numel() - 1, id_base, stream)
 
     def insert_addrs(self, addrs, id_base=0):
         flash_insert_addrs(self.h, addrs, addrs.shape[0], id_base)
 
-    def query(self, row_ptr, col_idx, k, exclude=None):
+    def query(self, row_ptr, col_idx, k, exclude=None, stream=None):
         n = row_ptr.numel() - 1
-        ids = torch.empty((n, k), dtype=torch.int32, device=self.device)
-        cnt = torch.empty((n, k), dtype=torch.int32, device=self.device)
-        flash_query_topk(self.h, row_ptr, col_idx, n, k, exclude, ids, cnt)
+        ids = torch.empty((max(n, 1), k), dtype=torch.int32, device=self.device)[:n]
+        cnt = torch.empty((max(n, 1), k), dtype=torch.int32, device=self.device)[:n]
+        flash_query_topk(self.h, row_ptr, col_idx, n, k, exclude, ids, cnt, stream)
         return ids, cnt
 
     def query_addrs(self, addrs, k, exclude=None):
@@ -365,11 +421,11 @@ class FlashIndex:
         flash_query_addrs(self.h, addrs, n, k, exclude, ids, cnt)
         return ids, cnt
 
-    def knn_graph(self, row_ptr, col_idx, k):
+    def knn_graph(self, row_ptr, col_idx, k, stream=None):
         n = row_ptr.numel() - 1
-        ids = torch.empty((n, k), dtype=torch.int32, device=self.device)
-        cnt = torch.empty((n, k), dtype=torch.int32, device=self.device)
-        flash_knn_graph(self.h, row_ptr, col_idx, n, k, ids, cnt)
+        ids = torch.empty((max(n, 1), k), dtype=torch.int32, device=self.device)[:n]
+        cnt = torch.empty((max(n, 1), k), dtype=torch.int32, device=self.device)[:n]
+        flash_knn_graph(self.h, row_ptr, col_idx, n, k, ids, cnt, stream)
         return ids, cnt
 
     def table(self, t: int):
@@ -394,8 +450,8 @@ class FlashIndex:
         return (_copy_device(g, nb + 1, self.device, "<i8"), _copy_device(i, n, self.device) if ids else None,
                 _copy_device(a, nb, self.device))
 
-    def import_tables(self, goff, ids, arrivals, max_id):
-        flash_import_tables(self.h, goff, ids if ids.numel() else None, ids.numel(), arrivals, max_id)
+    def import_tables(self, goff, ids, arrivals):
+        flash_import_tables(self.h, goff, ids if ids.numel() else None, ids.numel(), arrivals)
 
     def errors(self) -> int:
         return flash_check(self.h)
@@ -403,12 +459,11 @@ class FlashIndex:
     # ---- serialization ----
     FORMAT = "flash-b200-index-v1"
 
-    def save(self, path: str, max_id: int):
-        """Write the index (config + bucket offsets + kept ids + arrivals) to an .npz file.
-        max_id: the largest id inserted (the query kernels' digit range)."""
+    def save(self, path: str):
+        """Write the index (config + bucket offsets + kept ids + arrivals) to an .npz file."""
         goff, ids, arr = self.table_arrays()
         np.savez(path, format=self.FORMAT, K=self.K, L=self.L, R=self.R, range=self.range, seed=self.seed,
-                 pool=self.pool, max_id=max_id, goff=goff.cpu().numpy(), ids=as_u32(ids), arrivals=as_u32(arr))
+                 pool=self.pool, goff=goff.cpu().numpy(), ids=as_u32(ids), arrivals=as_u32(arr))
 
     @classmethod
     def load(cls, path: str) -> "FlashIndex":
@@ -423,7 +478,7 @@ class FlashIndex:
         goff = torch.from_numpy(z["goff"].astype(np.int64)).to(dev)
         ids = torch.from_numpy(np.ascontiguousarray(z["ids"]).view(np.int32)).to(dev)
         arr = torch.from_numpy(np.ascontiguousarray(z["arrivals"]).view(np.int32)).to(dev)
-        idx.import_tables(goff, ids, arr, int(z["max_id"]))
+        idx.import_tables(goff, ids, arr)
         return idx
 
     # ---- candidate exchange (dist.knn_graph_candidate_exchange) ----

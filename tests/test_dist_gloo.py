@@ -55,7 +55,7 @@ class OracleIndex:
         return (torch.from_numpy(np.concatenate(goff)), torch.from_numpy(np.concatenate(ids).view(np.int32)),
                 torch.from_numpy(self.T.arrivals.reshape(-1).view(np.int32).copy()))
 
-    def import_tables(self, goff, ids, arrivals, max_id):
+    def import_tables(self, goff, ids, arrivals):
         g = goff.numpy()
         i = ids.numpy().view(np.uint32)
         off = np.stack([g[t * self.range: (t + 1) * self.range + 1] - g[t * self.range]
@@ -243,5 +243,26 @@ def _gather_worker(rank, port, out_dir):
         out = fdist.all_gather_rows(local, counts)
         if rank == 0:
             np.save(os.path.join(out_dir, "g0.npy"), out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_unique_id_bootstrap_reaches_every_rank(tmp_path):
+    """dist.bootstrap_unique_id (the multi-GPU handle's bootstrap): rank 0's NCCL unique id
+    (flash_get_unique_id, no GPU needed) arrives byte-identical on every rank (gloo, world 3)."""
+    mp.spawn(_uid_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    ids = [open(tmp_path / f"uid_{r}.bin", "rb").read() for r in range(3)]
+    assert len(ids[0]) == 128 and ids[0] == ids[1] == ids[2]
+    assert ids[0] != bytes(128)
+
+
+def _uid_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = fdist.bootstrap_unique_id()
+        with open(os.path.join(out_dir, f"uid_{rank}.bin"), "wb") as f:
+            f.write(uid)
     finally:
         dist.destroy_process_group()

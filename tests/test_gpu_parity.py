@@ -221,10 +221,13 @@ QUERY_CASES = [
     ("webspam_dense_buckets_k128", lambda: shape_slice("webspam", 2500), 4, 50, 128, 1 << 7, 128),
     ("url_k128", lambda: shape_slice("url", 6000), 4, 128, 32, 1 << 15, 128),
     ("edge_k5", edge_csr, 4, 16, 4, 1000, 5),
-    # L*R = 10240 > 8192 with full buckets: M = 10240 candidates per query, the class whose
-    # count table lives in global memory
+    # L*R = 10240 > 8192 with full buckets: M = 10240 candidates per query, the CTA sort class
     ("full_buckets_LR10240_k100", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=8000, seed=3)), 1, 40, 256, 16, 100),
     ("LR32768_k64", lambda: shape_slice("webspam", 1500), 4, 128, 256, 1 << 12, 64),
+    ("LR16384_k1024", lambda: shape_slice("webspam", 1500), 4, 64, 256, 1 << 10, 1024),
+    # L = 4096: the warp sort classes' per-warp slices (L*8 B of segment bases) do not fit, so
+    # every class runs on the CTA sort kernel (classes that cannot launch)
+    ("L4096_R8_k32", lambda: synth.generate(synth.SHAPES["tiny"].with_(N=500, seed=4)), 2, 4096, 8, 64, 32),
 ]
 
 
@@ -251,6 +254,14 @@ def test_query_topk_bit_exact(name, make, K, L, R, rng, k):
         g_ids, g_cnt = idx.query(d_rp, d_col, k)  # CSR query path, no exclusion
         assert np.array_equal(flash.as_u32(g_ids), o_ids2)
         assert np.array_equal(flash.as_u32(g_cnt), o_cnt2)
+
+
+@pytest.mark.parametrize("name,make,K,L,R,rng,k", QUERY_CASES[:8], ids=[c[0] for c in QUERY_CASES[:8]])
+def test_query_csort_kernel_every_class(monkeypatch, name, make, K, L, R, rng, k):
+    """FLASH_QUERY_CSORT=1 routes every size class through the CTA sort kernel (the class of
+    L*R > 8192 and the fallback of classes that do not fit): bit-exact on the same cases."""
+    monkeypatch.setenv("FLASH_QUERY_CSORT", "1")
+    test_query_topk_bit_exact(name, make, K, L, R, rng, k)
 
 
 @pytest.mark.parametrize("few", ["0", "1000000000"])
@@ -414,7 +425,7 @@ def test_table_windows_assemble_to_the_full_index():
         parts.append(torch.tensor([base], dtype=torch.int64, device="cuda"))
         with flash.FlashIndex(K, L, R, rng, seed) as imp:
             imp.import_tables(torch.cat(parts).contiguous(), torch.cat(ids_parts).contiguous(),
-                              arr_sum.contiguous(), n - 1)
+                              arr_sum.contiguous())
             excl = torch.arange(n, dtype=torch.int32, device="cuda")
             g_ids, g_cnt = imp.query_addrs(addrs, k, excl)
             assert np.array_equal(flash.as_u32(g_ids), o_ids)

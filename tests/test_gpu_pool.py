@@ -122,7 +122,7 @@ def test_save_load_round_trip_then_further_inserts(tmp_path, F):
     h = 1800
     with flash.FlashIndex(K, L, R, rng, seed, F=F) as a:
         flash.flash_insert(a.h, d_rp[: h + 1].contiguous(), d_col, h, 0)
-        a.save(str(tmp_path / "idx.npz"), max_id=h - 1)
+        a.save(str(tmp_path / "idx.npz"))
         want = a.query(d_rp, d_col, k)
         g0, i0, r0 = a.table_arrays()
     with flash.FlashIndex.load(str(tmp_path / "idx.npz")) as b:
