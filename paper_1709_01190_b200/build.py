@@ -16,7 +16,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 SO = os.path.join(PKG, "libflash.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["doph.cu", "build.cu", "query.cu", "query_sort.cu", "exchange.cu", "util.cu", "flash_api.cu", "dist.cu"]
+SOURCES = ["doph.cu", "build.cu", "query.cu", "query_sort.cu", "exchange.cu", "query_mark.cu", "util.cu", "flash_api.cu", "dist.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -189,6 +189,13 @@ size_t query_scratch_bytes(uint64_t nq);
 // every size class of an index with L tables, R per bucket, top-k has a kernel that fits
 // (L*R <= FLASH_MAX_CANDIDATES and the CTA sort kernel's shared memory fits)
 bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k);
+// occupancy-bitmap CTA-per-query kernel (query_mark.cu) for ids that fit a shared-memory
+// bitmap; queries it cannot finish go to the CTA sort kernel.  scratch >= query_mark_scratch_bytes
+bool query_mark_eligible(const QueryArgs& a);
+size_t query_mark_scratch_bytes(uint64_t nq);
+int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s);
+// CTA sort kernel over a device-side query list (list[0..*count)), M <= cap
+int launch_csort(const QueryArgs& a, uint32_t cap, const uint32_t* list, const uint32_t* count, cudaStream_t s);
 // radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
                       cudaStream_t s);

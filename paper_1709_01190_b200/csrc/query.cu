@@ -927,6 +927,8 @@ int launch_class(const QueryArgs& a, const uint32_t* list, const uint32_t* count
   return 1;
 }
 
+}  // namespace
+
 // the CTA sort kernel for queries of at most `cap` candidates (cap <= FLASH_MAX_CANDIDATES)
 int launch_csort(const QueryArgs& a, uint32_t cap, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
   cap = (cap + 127) & ~127u;
@@ -944,8 +946,6 @@ int launch_csort(const QueryArgs& a, uint32_t cap, const uint32_t* list, const u
   return 1;
 }
 
-}  // namespace
-
 bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k) {
   const uint64_t mmax = (uint64_t)L * R;
   if (mmax > FLASH_MAX_CANDIDATES) return false;
@@ -957,7 +957,7 @@ bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k) {
 size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * kClasses + kClasses); }
 
 int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s) {
-  if (a.nq == 0) return 0;
+  if (a.nq == 0 || query_mark_eligible(a)) return 0;  // the bitmap kernel needs no plan
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* counts = lists + a.nq * kClasses;
   cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kClasses, s);
@@ -971,6 +971,7 @@ int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s) {
 
 int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (a.nq == 0) return 0;
+  if (query_mark_eligible(a)) return launch_query_mark(a, scratch, s);  // query_mark.cu
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* counts = lists + a.nq * kClasses;
   const uint64_t max_m = a.mmax;

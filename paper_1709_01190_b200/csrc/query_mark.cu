@@ -1,0 +1,458 @@
+// query_mark.cu — Q1-Q3 by an occupancy bitmap over the id range (sm_100a), for indexes
+// whose ids fit a shared-memory bitmap (max_id < 8 * kMarkMaxBitmapBytes).
+//
+// What the top-k needs (Alg. 3; R#11-R#13): every id seen at least twice, with
+// its full multiplicity, and — when fewer than k ids repeat — the smallest `need` ids seen
+// exactly once (ties at count 1 go by ascending id).  On the webspam graph a query has
+// ~1,060 candidates of which ~80 are repeats of ~4 ids (a near-duplicate family seen in
+// most of the L tables), and the 124-odd surviving singletons are the smallest ids, so a
+// full sort of the candidates (query_sort.cu) does mostly unneeded work.  Instead, one
+// CTA owns one query at a time (persistent over the queries):
+//   Q1 gather   thread t < L holds bucket t's extent (loaded during the previous query); a
+//               scan gives each non-empty bucket's first flattened position: a start bitmap
+//               over the positions, the number of starts below each of its words, and one
+//               base pointer per bucket, so position p's bucket is a popc away; 32-position
+//               blocks go round-robin to the warps, 4 loads in flight per lane.
+//   Q2 count    each candidate sets its bit in the id bitmap with one shared-memory
+//               atomicOr; a bit already set means a repeat, and only repeats go to a small
+//               open-addressing table (id -> extra occurrences; new slots are listed).
+//               Full multiplicity = 1 + extra (R#11).  The excluded id (self, R#14) is
+//               dropped at the gather.
+//   Q3 top-k    warp 0 compacts the listed repeated ids into (count desc, id asc) keys and
+//               clears their bits, so the bitmap holds exactly the singletons, and ranks
+//               them by counting; the CTA then scans the bitmap from id 0 (2,048 words per
+//               round, a block scan of the per-thread bit counts) writing the first `need`
+//               set bits in ascending order (R#12); pads (EMPTY, 0) fill the rest (R#13).
+//   reset       the bitmap words of the staged candidates (their u16 word indices, M <=
+//               kStage; else the whole bitmap) and the listed table slots.
+// A query with more than kRepMax distinct repeated ids (or a probe sequence longer than
+// kRepProbes) is appended to a fallback list and answered by the CTA sort kernel
+// (k_query_csort) afterwards; the results do not depend on which kernel answers a query
+// (both compute the same (count desc, id asc) top-k).
+#include <cstdlib>
+
+#include "flash_internal.cuh"
+
+namespace flash {
+namespace {
+
+constexpr int kMarkThreads = 256;
+constexpr uint32_t kMarkWarps = kMarkThreads / 32;
+constexpr uint32_t kRepLog2 = 8;
+constexpr uint32_t kRepSlots = 1u << kRepLog2;  // open-addressing table of repeated ids
+constexpr uint32_t kRepMax = 112;               // distinct repeated ids ranked here (more: fallback)
+constexpr uint32_t kRepProbes = 32;             // a longer probe sequence also falls back
+constexpr uint32_t kMarkMaxL = 128;             // Q1: one thread per bucket, 8-bit bucket ranks
+constexpr uint32_t kStage = 2048;               // candidates staged for the bitmap reset
+constexpr uint32_t kScanWpt = 8;                // bitmap words per thread per scan round
+constexpr size_t kMarkMaxBitmapBytes = 96 * 1024;  // >= 2 CTAs per SM (and u16 word indices)
+
+struct MarkHdr {
+  uint32_t nsingle, nrep, overflow, excl, nhi;
+  uint32_t wsum[kMarkWarps];
+  uint32_t rsum[2][kMarkWarps];
+};
+
+__host__ __device__ inline uint32_t mark_words(uint32_t max_id) {  // bitmap words, multiple of 128
+  const uint64_t bits = (uint64_t)max_id + 1;
+  return (uint32_t)(((bits + 32 * 128 - 1) / (32 * 128)) * 128);
+}
+__host__ __device__ inline uint32_t mark_bmap_words(uint64_t mmax) { return (uint32_t)((mmax / 32 + 2 + 7) & ~7ull); }
+__host__ __device__ inline uint32_t mark_stage(uint64_t mmax) {
+  return mmax < kStage ? (uint32_t)((mmax + 7) & ~7ull) : kStage;
+}
+
+__host__ __device__ inline size_t mark_smem_bytes(uint32_t nwords, uint32_t L, uint64_t mmax) {
+  size_t b = (size_t)nwords * 4                  // id bitmap
+             + (size_t)kRepSlots * 10            // repeated ids, their extra occurrences, slot list
+             + (size_t)kRepMax * 8               // ranked repeated ids (u64 keys)
+             + (size_t)((L + 1) & ~1u) * 8       // base of each non-empty bucket (16-B multiple)
+             + (size_t)mark_bmap_words(mmax) * 8  // bucket-start bitmap over positions + prefix
+             + (size_t)mark_stage(mmax) * 2;     // staged bitmap word indices (reset)
+  return (b + 15) & ~(size_t)15;
+}
+
+// shared-memory atomics on 32-bit shared-window addresses (no generic-address conversion
+// per access)
+__device__ __forceinline__ uint32_t smem_or(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t smem_cas(uint32_t addr, uint32_t cmp, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(addr), "r"(cmp), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void smem_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// word j (< 8) of a thread's scan words, without indexing registers dynamically
+__device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], uint32_t j) {
+  const uint32_t a = (j & 1) ? w[1] : w[0], b = (j & 1) ? w[3] : w[2];
+  const uint32_t c = (j & 1) ? w[5] : w[4], d = (j & 1) ? w[7] : w[6];
+  const uint32_t ab = (j & 2) ? b : a, cd = (j & 2) ? d : c;
+  return (j & 4) ? cd : ab;
+}
+
+__global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32_t nwords, uint32_t rep_max,
+                                                            uint32_t* __restrict__ fb_list,
+                                                            uint32_t* __restrict__ fb_count) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ MarkHdr hdr;
+  const uint32_t L = a.L, k = a.k;
+  const uint32_t nbw = mark_bmap_words(a.mmax);
+  const uint32_t stage_cap = mark_stage(a.mmax);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(sm);                     // [nwords]
+  uint32_t* rkey = bits + nwords;                                       // [kRepSlots]
+  uint32_t* rcnt = rkey + kRepSlots;                                    // [kRepSlots]
+  uint64_t* rlist = reinterpret_cast<uint64_t*>(rcnt + kRepSlots);      // [kRepMax]
+  const uint32_t** nbase = reinterpret_cast<const uint32_t**>(rlist + kRepMax);  // [L]
+  // word w of the bucket-start bitmap over positions: .x = the starts in [32w, 32w + 32),
+  // .y = the number of starts below 32w
+  uint2* bmap = reinterpret_cast<uint2*>(nbase + ((L + 1) & ~1u));     // [nbw]
+  uint16_t* stage = reinterpret_cast<uint16_t*>(bmap + nbw);            // [stage_cap], 16-B aligned
+  uint16_t* rslot = stage + stage_cap;                                  // [kRepSlots] slots in use
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const uint32_t nwq = (L + 31) >> 5;  // warps holding a bucket
+  const uint32_t* __restrict__ gids = a.ids;
+  const uint32_t lim = a.shared ? a.shared : a.range;
+  const uint32_t nbits = nwords * 32u;
+  const uint32_t s_bits = (uint32_t)__cvta_generic_to_shared(bits);
+  const uint32_t s_rkey = (uint32_t)__cvta_generic_to_shared(rkey);
+  const uint32_t s_rcnt = (uint32_t)__cvta_generic_to_shared(rcnt);
+  uint32_t lanele;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(lanele));
+
+  // thread tid < L: table tid's bucket of query q (issued a phase before it is consumed)
+  auto bucket_addr = [&](uint64_t q) -> uint32_t {
+    return q < a.nq ? (a.direct ? (uint32_t)q : a.addrs[q * L + tid]) : kEmpty;
+  };
+  auto bucket_extent = [&](uint32_t ad, uint64_t& st, uint32_t& sz) {
+    st = 0;
+    sz = 0;
+    if (ad < lim) {
+      const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)tid * a.range + ad;
+      st = a.goff[i];
+      sz = a.seg_len ? a.seg_len[i] : (uint32_t)(a.goff[i + 1] - st);
+    }
+  };
+  auto exclude_of = [&](uint64_t q) -> uint32_t {
+    return a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
+  };
+
+  {  // one-time reset (later queries reset what they touched)
+    uint4* b4 = reinterpret_cast<uint4*>(bits);
+    for (uint32_t j = tid; j < nwords / 4; j += kMarkThreads) b4[j] = make_uint4(0, 0, 0, 0);
+    for (uint32_t j = tid; j < kRepSlots; j += kMarkThreads) {
+      rkey[j] = kEmpty;
+      rcnt[j] = 0;
+    }
+    for (uint32_t j = tid; j < nbw; j += kMarkThreads) bmap[j] = make_uint2(0, 0);
+    for (uint32_t j = tid; j < stage_cap; j += kMarkThreads) stage[j] = 0;
+    if (tid == 0) {
+      hdr.nrep = hdr.overflow = 0;
+      hdr.excl = blockIdx.x < a.nq ? exclude_of(blockIdx.x) : kEmpty;
+    }
+  }
+  uint32_t cur_ad = kEmpty, cur_sz = 0;
+  uint64_t cur_st = 0;
+  if (tid < L) {
+    cur_ad = bucket_addr(blockIdx.x);
+    bucket_extent(cur_ad, cur_st, cur_sz);
+  }
+  __syncthreads();
+
+  for (uint64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const uint64_t qn = q + gridDim.x;  // this CTA's next query (prefetched)
+
+    // ---- Q1: scan of (size, non-empty) over the L buckets (sizes clamped above L*R: the
+    //      sum then stays below 2^24; ranks < 2^8) ----
+    const uint32_t sz = cur_sz <= a.mmax ? cur_sz : (uint32_t)a.mmax + 1;
+    const uint32_t v = sz | ((uint32_t)(sz > 0) << 24);
+    uint32_t x = v, nx_ad = kEmpty;
+    if (wib < nwq) {
+      if (cur_ad != kEmpty && cur_ad >= lim) atomicAdd(a.err, 1ull);  // an address outside the table
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) hdr.wsum[wib] = x;
+      if (tid < L) nx_ad = bucket_addr(qn);  // prefetch: the next query's addresses
+    }
+    __syncthreads();
+    const uint32_t excl = hdr.excl;
+    const uint32_t wsl = lane < nwq ? hdr.wsum[lane] : 0u;
+    const uint32_t before_w = __reduce_add_sync(0xFFFFFFFFu, lane < wib ? wsl : 0u);
+    const uint32_t M = __reduce_add_sync(0xFFFFFFFFu, wsl) & 0xFFFFFFu;
+    if (sz > 0 && M <= a.mmax) {
+      const uint32_t ex = before_w + x - v;  // exclusive prefix: position | rank << 24
+      const uint32_t pos = ex & 0xFFFFFFu, r = ex >> 24;
+      nbase[r] = gids + (int64_t)(cur_st - (uint64_t)pos);
+      atomicOr(&bmap[pos >> 5].x, 1u << (pos & 31));
+      // words whose position just below them lies in this bucket: r + 1 starts below them
+      for (uint32_t w = (pos + 32) >> 5; w <= (pos + sz) >> 5; ++w) bmap[w].y = r + 1;
+    }
+    uint32_t* oid = a.out_ids + q * k;
+    uint32_t* ocnt = a.out_counts + q * k;
+    if (M > a.mmax || M == 0) {  // more than L*R candidates (bad direct segments): error + pads
+      if (M && tid == 0) atomicAdd(a.err, 1ull);
+      for (uint32_t j = tid; j < k; j += kMarkThreads) {
+        oid[j] = kEmpty;
+        ocnt[j] = 0;
+      }
+      if (tid < L) {
+        cur_ad = nx_ad;
+        bucket_extent(cur_ad, cur_st, cur_sz);
+      }
+      __syncthreads();  // hdr is rewritten for the next query
+      if (tid == 0 && qn < a.nq) hdr.excl = exclude_of(qn);
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+
+    // ---- Q2: gather 32-position blocks (block b -> warp b mod 8, 4 in flight), mark the
+    //      bitmap, table the repeats.  Position p lies in bucket (#starts <= p) - 1.  The
+    //      excluded id is marked like any other and taken out at Q3a. ----
+    const bool staged = M <= stage_cap;
+    {
+      const uint32_t nblk = (M + 31) >> 5;
+      for (uint32_t b0 = wib; b0 < nblk; b0 += 4 * kMarkWarps) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t b = b0 + u * kMarkWarps, p = b * 32 + lane;
+          idv[u] = kEmpty;
+          if (p < M) {
+            const uint2 e = bmap[b];
+            idv[u] = __ldg(nbase[e.y + __popc(e.x & lanele) - 1] + p);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          const uint32_t p = (b0 + u * kMarkWarps) * 32 + lane;
+          if (id < nbits) {
+            if (staged) stage[p] = (uint16_t)(id >> 5);
+            const uint32_t bit = 1u << (id & 31);
+            const uint32_t old = smem_or(s_bits + ((id >> 5) << 2), bit);
+            if (old & bit) {  // a repeat: one more occurrence of id in the table
+              uint32_t s = (id * 0x9E3779B1u) >> (32 - kRepLog2);
+#pragma unroll 1
+              for (uint32_t probe = 0;; ++probe) {
+                const uint32_t c = smem_cas(s_rkey + (s << 2), kEmpty, id);
+                if (c == kEmpty || c == id) {
+                  smem_add(s_rcnt + (s << 2), 1u);
+                  if (c == kEmpty) rslot[atomicAdd(&hdr.nrep, 1u)] = (uint16_t)s;
+                  break;
+                }
+                if (probe == kRepProbes) {  // (a crowded table) -> the fallback kernel
+                  atomicExch(&hdr.overflow, 1u);
+                  break;
+                }
+                s = (s + 1) & (kRepSlots - 1);
+              }
+            }
+          } else if (id != kEmpty) {
+            atomicAdd(a.err, 1ull);  // an id above max_id: contract violation
+            if (staged) stage[p] = 0;
+          }
+        }
+      }
+    }
+    if (tid < L) {
+      cur_ad = nx_ad;
+      bucket_extent(cur_ad, cur_st, cur_sz);  // prefetch: the next query's bucket extents
+    }
+    __syncthreads();
+
+    // ---- Q3a (warp 0): compact the listed repeated ids into (count desc, id asc) keys,
+    //      clear their bits and the excluded id's (the bitmap then holds exactly the ids
+    //      seen once, excluded id aside) and the slots; the other warps reset the start
+    //      bitmap.  distinct ids = M - extra occurrences (ids above max_id aside). ----
+    if (wib == 0) {
+      const uint32_t nrep = hdr.nrep;
+      const bool ovf = hdr.overflow != 0 || nrep > rep_max;
+      uint32_t extra = 0;
+      bool xrep = false;
+      for (uint32_t j = lane; j < nrep; j += 32) {
+        const uint32_t s = rslot[j], key = rkey[s], c = rcnt[s];
+        extra += c;
+        xrep |= key == excl;
+        if (!ovf) {
+          rlist[j] = key == excl ? ~0ull : ((uint64_t)(0xFFFFFFFEu - (c + 1)) << 32) | key;
+          atomicAnd(&bits[key >> 5], ~(1u << (key & 31)));
+        }
+        rkey[s] = kEmpty;
+        rcnt[s] = 0;
+      }
+      extra = __reduce_add_sync(0xFFFFFFFFu, extra);
+      xrep = __any_sync(0xFFFFFFFFu, xrep);
+      if (lane == 0) {
+        if (ovf) {
+          fb_list[atomicAdd(fb_count, 1u)] = (uint32_t)q;
+          hdr.overflow = 1;
+        } else {
+          bool xonce = false;  // the excluded id seen exactly once: its bit goes too
+          if (!xrep && excl < nbits) {
+            const uint32_t w = bits[excl >> 5], bit = 1u << (excl & 31);
+            xonce = (w & bit) != 0;
+            if (xonce) bits[excl >> 5] = w & ~bit;
+          }
+          hdr.nhi = nrep;  // listed entries (the excluded id's included)
+          hdr.nrep = nrep - (xrep ? 1u : 0u);
+          hdr.nsingle = M - extra - nrep - (xonce ? 1u : 0u);
+        }
+      }
+    } else {
+      for (uint32_t j = tid - 32; j <= (M >> 5) + 1 && j < nbw; j += kMarkThreads - 32) bmap[j].x = 0;
+    }
+    __syncthreads();
+    const bool overflow = hdr.overflow != 0;
+    const uint32_t nrep = hdr.nrep, nlist = hdr.nhi;
+    if (!overflow) {
+      // ---- Q3b (warp 0): rank the repeated ids (count desc, id asc) ----
+      const uint32_t nhi = nrep < k ? nrep : k;
+      if (wib == 0) {
+        // (the listed entries: nrep, plus the excluded id's key ~0 when it repeated, which
+        //  ranks last and is not written)
+        const uint32_t nl = nlist;
+        for (uint32_t e0 = 0; e0 < nl; e0 += 32) {
+          const uint32_t e = e0 + lane;
+          const uint64_t me = e < nl ? rlist[e] : ~0ull;
+          uint32_t rank = 0;
+          if (nl <= 32) {
+            for (uint32_t j = 0; j < nl; ++j) rank += __shfl_sync(0xFFFFFFFFu, me, j) < me;
+          } else {
+            for (uint32_t j = 0; j < nl; ++j) rank += rlist[j] < me;
+          }
+          if (e < nl && rank < nhi) {
+            oid[rank] = (uint32_t)me;
+            ocnt[rank] = 0xFFFFFFFEu - (uint32_t)(me >> 32);
+          }
+        }
+      }
+      // ---- Q3c: the smallest `target` singletons, in ascending id order ----
+      const uint32_t need = k - nhi;
+      const uint32_t nsingle = hdr.nsingle;
+      const uint32_t target = need < nsingle ? need : nsingle;
+      uint32_t* osg = oid + nhi;
+      uint32_t found = 0, buf = 0;
+      for (uint32_t w0 = 0; found < target && w0 < nwords; w0 += kMarkThreads * kScanWpt) {
+        const uint32_t wt = w0 + tid * kScanWpt;
+        uint32_t wv[kScanWpt];
+        const bool in = wt < nwords;  // (nwords is a multiple of kScanWpt)
+#pragma unroll
+        for (uint32_t j = 0; j < kScanWpt; j += 4) {
+          const uint4 b4 = in ? *reinterpret_cast<const uint4*>(bits + wt + j) : make_uint4(0, 0, 0, 0);
+          wv[j] = b4.x;
+          wv[j + 1] = b4.y;
+          wv[j + 2] = b4.z;
+          wv[j + 3] = b4.w;
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kScanWpt; ++j) c += __popc(wv[j]);
+        uint32_t incl = c;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) hdr.rsum[buf][wib] = incl;
+        __syncthreads();
+        const uint32_t rs = lane < kMarkWarps ? hdr.rsum[buf][lane] : 0u;
+        const uint32_t wpre = __reduce_add_sync(0xFFFFFFFFu, lane < wib ? rs : 0u);
+        const uint32_t rtot = __reduce_add_sync(0xFFFFFFFFu, rs);
+        uint32_t pos = found + wpre + incl - c;
+        uint32_t nz = 0;
+        if (c && pos < target) {
+#pragma unroll
+          for (uint32_t j = 0; j < kScanWpt; ++j) nz |= (wv[j] != 0 ? 1u : 0u) << j;
+        }
+        while (nz && pos < target) {  // this thread's non-empty words, in order
+          const uint32_t j = __ffs(nz) - 1;
+          nz &= nz - 1;
+          uint32_t xw = pick8(wv, j);
+          const uint32_t idb = (wt + j) * 32 - 1;
+          do {
+            osg[pos++] = idb + __ffs(xw);
+            xw &= xw - 1;
+          } while (xw && pos < target);
+        }
+        found += rtot;
+        buf ^= 1;
+      }
+      // counts of the singletons, then pads (EMPTY, 0)
+      for (uint32_t j = nhi + tid; j < k; j += kMarkThreads) {
+        const bool pad = j >= nhi + target;
+        if (pad) oid[j] = kEmpty;
+        ocnt[j] = pad ? 0u : 1u;
+      }
+    }
+    __syncthreads();
+
+    // ---- reset for the next query (its Q1 barrier orders this before its gather) ----
+    if (staged) {  // 8 staged word indices per thread
+      for (uint32_t j = tid * 8; j < M; j += kMarkThreads * 8) {
+        const uint4 s4 = *reinterpret_cast<const uint4*>(stage + j);
+        bits[s4.x & 0xFFFFu] = 0;
+        bits[s4.x >> 16] = 0;
+        bits[s4.y & 0xFFFFu] = 0;
+        bits[s4.y >> 16] = 0;
+        bits[s4.z & 0xFFFFu] = 0;
+        bits[s4.z >> 16] = 0;
+        bits[s4.w & 0xFFFFu] = 0;
+        bits[s4.w >> 16] = 0;
+      }
+    } else {
+      uint4* b4 = reinterpret_cast<uint4*>(bits);
+      for (uint32_t j = tid; j < nwords / 4; j += kMarkThreads) b4[j] = make_uint4(0, 0, 0, 0);
+    }
+    if (tid == 0) {
+      hdr.nrep = hdr.overflow = 0;
+      if (qn < a.nq) hdr.excl = exclude_of(qn);
+    }
+  }
+}
+
+}  // namespace
+
+bool query_mark_eligible(const QueryArgs& a) {
+  const char* e = getenv("FLASH_QUERY_MARK");  // tests: 0 = the sort kernels
+  if ((e && e[0] == '0') || a.L > kMarkMaxL || a.mmax > FLASH_MAX_CANDIDATES) return false;
+  if ((size_t)mark_words(a.max_id) * 4 > kMarkMaxBitmapBytes) return false;
+  return mark_smem_bytes(mark_words(a.max_id), a.L, a.mmax) <= 227 * 1024;
+}
+
+size_t query_mark_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq + 4); }
+
+int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s) {
+  if (a.nq == 0) return 0;
+  const uint32_t nwords = mark_words(a.max_id);
+  const size_t smem = mark_smem_bytes(nwords, a.L, a.mmax);
+  if (!ensure_smem_attr((const void*)k_query_mark, smem)) return -1;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_mark, kMarkThreads, smem);
+  if (per_sm < 1) return -1;
+  uint32_t* fb_list = reinterpret_cast<uint32_t*>(scratch);
+  uint32_t* fb_count = fb_list + a.nq;
+  cudaMemsetAsync(fb_count, 0, sizeof(uint32_t), s);
+  uint64_t grid = (uint64_t)device_sms() * per_sm;
+  if (grid > a.nq) grid = a.nq;
+  // FLASH_QUERY_MARK_REPMAX (tests): a lower cap on distinct repeated ids, so that queries
+  // take the fallback path
+  const char* e = getenv("FLASH_QUERY_MARK_REPMAX");
+  uint32_t rep_max = e ? (uint32_t)strtoul(e, nullptr, 10) : kRepMax;
+  if (rep_max > kRepMax) rep_max = kRepMax;
+  k_query_mark<<<(unsigned)grid, kMarkThreads, smem, s>>>(a, nwords, rep_max, fb_list, fb_count);
+  // the queries with more than rep_max distinct repeated ids: the CTA sort kernel
+  const int r = launch_csort(a, (uint32_t)a.mmax, fb_list, fb_count, s);
+  if (r < 0) return -1;
+  return 2 + r;
+}
+
+}  // namespace flash

@@ -231,8 +231,23 @@ QUERY_CASES = [
 ]
 
 
+# query kernels: "mark" = the default (the occupancy-bitmap kernel when the ids fit its
+# bitmap), "sort" = FLASH_QUERY_MARK=0 (the size-class sort kernels), "fallback0" /
+# "fallback3" = the bitmap kernel with at most 0 / 3 distinct repeated ids per query, so
+# every / some queries go to its CTA-sort fallback list
+QUERY_KERNELS = {"mark": {}, "sort": {"FLASH_QUERY_MARK": "0"},
+                 "fallback0": {"FLASH_QUERY_MARK_REPMAX": "0"}, "fallback3": {"FLASH_QUERY_MARK_REPMAX": "3"}}
+
+
+def _set_kernel(monkeypatch, kern):
+    for key, val in QUERY_KERNELS[kern].items():
+        monkeypatch.setenv(key, val)
+
+
+@pytest.mark.parametrize("kern", list(QUERY_KERNELS))
 @pytest.mark.parametrize("name,make,K,L,R,rng,k", QUERY_CASES, ids=[c[0] for c in QUERY_CASES])
-def test_query_topk_bit_exact(name, make, K, L, R, rng, k):
+def test_query_topk_bit_exact(monkeypatch, name, make, K, L, R, rng, k, kern):
+    _set_kernel(monkeypatch, kern)
     rp, col = make()
     n = rp.size - 1
     seed = 0xC0DE + k
@@ -261,7 +276,7 @@ def test_query_csort_kernel_every_class(monkeypatch, name, make, K, L, R, rng, k
     """FLASH_QUERY_CSORT=1 routes every size class through the CTA sort kernel (the class of
     L*R > 8192 and the fallback of classes that do not fit): bit-exact on the same cases."""
     monkeypatch.setenv("FLASH_QUERY_CSORT", "1")
-    test_query_topk_bit_exact(name, make, K, L, R, rng, k)
+    test_query_topk_bit_exact(monkeypatch, name, make, K, L, R, rng, k, "sort")
 
 
 @pytest.mark.parametrize("few", ["0", "1000000000"])
@@ -270,6 +285,7 @@ def test_query_4096_class_both_kernels(monkeypatch, few):
     are many queries and the CTA-per-query kernel when there are few (FLASH_QUERY_FEW sets
     the cut; 0 forces the sort class, a huge value the CTA kernel): both bit-exact."""
     monkeypatch.setenv("FLASH_QUERY_FEW", few)
+    monkeypatch.setenv("FLASH_QUERY_MARK", "0")
     rp, col = shape_slice("url", 6000)
     K, L, R, rng, k = 4, 128, 32, 1 << 6, 128  # 64 buckets: all saturate, M = L*R = 4096
     n = rp.size - 1
@@ -294,8 +310,10 @@ GRAPH_CASES = [
 ]
 
 
+@pytest.mark.parametrize("kern", list(QUERY_KERNELS))
 @pytest.mark.parametrize("name,make,K,L,R,rng,k", GRAPH_CASES, ids=[c[0] for c in GRAPH_CASES])
-def test_knn_graph_bit_exact(name, make, K, L, R, rng, k):
+def test_knn_graph_bit_exact(monkeypatch, name, make, K, L, R, rng, k, kern):
+    _set_kernel(monkeypatch, kern)
     rp, col = make()
     seed = 0x5EED0002
     o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
@@ -382,7 +400,7 @@ def test_full_webspam_graph_sampled_parity():
     assert np.array_equal(flash.as_u32(g_cnt)[sample], o_cnt)
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):
     """compute-sanitizer finds no memory errors / shared-memory races / barrier misuse on
     small runs of every kernel family (tools/sanitize_run.py: tiny, webspam, url, kdd12

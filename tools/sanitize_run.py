@@ -1,4 +1,4 @@
-"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck / synccheck): every
+"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every
 kernel family — dense and sparse DOPH, row-major and table-major builds, the small /
 register / warp / CTA selects, the size-classed query kernels, and the multi-GPU
 exchange steps (window gather, direct-segment count/top-k) on one GPU."""
@@ -19,8 +19,12 @@ CASES = [("tiny", 1000, (4, 16, 32, 1 << 15, 10), "0"),
          ("tiny", 4000, (2, 4, 16, 64, 20), "0"),          # register-path select, m > R
          ("tiny", 3000, (4, 8, 64, 4, 10), "0")]           # > 512 members: early list, side stream
 
-for name, n, (K, L, R, rng, k), tm in CASES:
+for ci, (name, n, (K, L, R, rng, k), tm) in enumerate(CASES):
     os.environ["FLASH_BUILD_TM"] = tm
+    # query kernels: alternate the occupancy-bitmap kernel (with a forced fallback list on
+    # every third case) and the size-class sort kernels
+    os.environ["FLASH_QUERY_MARK"] = "1" if ci % 2 == 0 else "0"
+    os.environ["FLASH_QUERY_MARK_REPMAX"] = "2" if ci % 3 == 0 else "224"
     rp, col = synth.generate(synth.SHAPES[name].with_(N=n))
     rows = [col[rp[i]:rp[i + 1]] for i in range(n)] + synth.edge_case_rows()
     rp, col = synth.csr_from_rows(rows)
@@ -29,7 +33,7 @@ for name, n, (K, L, R, rng, k), tm in CASES:
         ids, cnt = idx.knn_graph(d_rp, d_col, k)
         idx.table(0)
         torch.cuda.synchronize()
-    print(name, n, "ok", int(flash.as_u32(cnt).max()), flush=True)
+    print(name, n, "mark" if ci % 2 == 0 else "sort", "ok", int(flash.as_u32(cnt).max()), flush=True)
 
 # the exchange steps: 2 virtual ranks, each owning half of the tables
 os.environ["FLASH_BUILD_TM"] = "0"
