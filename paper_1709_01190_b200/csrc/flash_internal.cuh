@@ -189,11 +189,12 @@ size_t query_scratch_bytes(uint64_t nq);
 // every size class of an index with L tables, R per bucket, top-k has a kernel that fits
 // (L*R <= FLASH_MAX_CANDIDATES and the CTA sort kernel's shared memory fits)
 bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k);
-// occupancy-bitmap CTA-per-query kernel (query_mark.cu) for ids that fit a shared-memory
-// bitmap; queries it cannot finish go to the CTA sort kernel.  scratch >= query_mark_scratch_bytes
-bool query_mark_eligible(const QueryArgs& a);
-size_t query_mark_scratch_bytes(uint64_t nq);
-int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s);
+// occupancy-bitmap CTA-per-query kernel (query_mark.cu) for indexes whose ids fit a
+// shared-memory bitmap: launch_query routes the queries with more than query_mark_min(a)
+// candidates to it (0xFFFFFFFF: never); the queries it cannot finish go to the CTA sort
+// kernel.  list/count: device-side query list; fb: scratch for nq + 1 u32 (fallback list)
+uint32_t query_mark_min(const QueryArgs& a);
+int launch_query_mark(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t* fb, cudaStream_t s);
 // CTA sort kernel over a device-side query list (list[0..*count)), M <= cap
 int launch_csort(const QueryArgs& a, uint32_t cap, const uint32_t* list, const uint32_t* count, cudaStream_t s);
 // radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)

@@ -50,11 +50,15 @@ __host__ __device__ constexpr uint32_t class_max(int c) {
 // the last class (8192 < M <= 32768, indexes with L*R > 8192): one 1024-thread CTA per query
 // sorts its candidates in shared memory (k_query_csort; 128 KB of ids)
 constexpr int kClasses = kSortClasses + 2;
+// one more list: queries with more than mark_min candidates, for the occupancy-bitmap kernel
+// (query_mark.cu) when the index's ids fit its bitmap
+constexpr int kLists = kClasses + 1;
 constexpr uint64_t kFewQueries = 65536;  // below: the 3072 < M <= 4096 class runs CTA-per-query
 
 __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, const uint64_t* __restrict__ goff,
                              const uint32_t* __restrict__ seg_len,
-                             uint32_t L, uint32_t range, int direct, uint32_t shared, uint64_t mmax, uint32_t k,
+                             uint32_t L, uint32_t range, int direct, uint32_t shared, uint64_t mmax,
+                             uint32_t mark_min, uint32_t k,
                              uint32_t* __restrict__ out_ids, uint32_t* __restrict__ out_counts,
                              uint32_t* __restrict__ lists, uint32_t* __restrict__ counts, unsigned long long* err) {
   const uint32_t lane = threadIdx.x & 31;
@@ -89,6 +93,7 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
     }
     int cls = 0;
     while (cls < kClasses - 1 && M > class_max(cls)) ++cls;
+    if (M > mark_min || mark_min == 0) cls = kClasses;  // the bitmap kernel's list (it pads M = 0)
     if (q < nq && M > mmax) {  // more candidates than L*R: only possible for bad direct segments
       // (flash.h flash_count_topk: counted in the error counter, k pads)
       atomicAdd(err, 1ull);
@@ -96,10 +101,10 @@ __global__ void k_query_plan(const uint32_t* __restrict__ addrs, uint64_t nq, co
         out_ids[q * k + j] = kEmpty;
         out_counts[q * k + j] = 0;
       }
-      cls = kClasses;  // in no list
+      cls = kLists;  // in no list
     }
 #pragma unroll
-    for (int c = 0; c < kClasses; ++c) {
+    for (int c = 0; c < kLists; ++c) {
       const uint32_t m = __ballot_sync(kFullMask, q < nq && cls == c);
       if (!m) continue;
       uint32_t b = 0;
@@ -954,27 +959,29 @@ bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k) {
   return csort_smem_bytes(cap, L, L, k) <= 227 * 1024;
 }
 
-size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * kClasses + kClasses); }
+// lists [kLists][nq], counts [kLists], then the bitmap kernel's fallback list [nq] + count
+size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * (kLists + 1) + kLists + 4); }
 
 int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s) {
-  if (a.nq == 0 || query_mark_eligible(a)) return 0;  // the bitmap kernel needs no plan
+  if (a.nq == 0) return 0;
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
-  uint32_t* counts = lists + a.nq * kClasses;
-  cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kClasses, s);
+  uint32_t* counts = lists + a.nq * kLists;
+  cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kLists, s);
   const uint64_t warps = (a.nq + 31) / 32;
   uint64_t blocks = (warps + 7) / 8;
   if (blocks > (uint64_t)device_sms() * 16) blocks = (uint64_t)device_sms() * 16;
-  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.seg_len, a.L, a.range, a.direct, a.shared, a.mmax, a.k,
-                                                 a.out_ids, a.out_counts, lists, counts, a.err);
+  k_query_plan<<<(unsigned)blocks, 256, 0, s>>>(a.addrs, a.nq, a.goff, a.seg_len, a.L, a.range, a.direct, a.shared, a.mmax,
+                                                 query_mark_min(a), a.k, a.out_ids, a.out_counts, lists, counts, a.err);
   return 1;
 }
 
 int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   if (a.nq == 0) return 0;
-  if (query_mark_eligible(a)) return launch_query_mark(a, scratch, s);  // query_mark.cu
   uint32_t* lists = reinterpret_cast<uint32_t*>(scratch);
-  uint32_t* counts = lists + a.nq * kClasses;
-  const uint64_t max_m = a.mmax;
+  uint32_t* counts = lists + a.nq * kLists;
+  const uint32_t mark_min = query_mark_min(a);
+  // the size classes hold the queries with at most min(L*R, mark_min) candidates
+  const uint64_t max_m = a.mmax < mark_min ? a.mmax : mark_min;
   const int planned = a.planned ? 0 : launch_query_plan(a, scratch, s);
   const uint32_t hist_len = (a.cmax + 1) > 1024 ? a.cmax + 1 : 1024;
   // The class kernels are persistent over their device-side query lists and run back to
@@ -986,7 +993,7 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   const char* cs_env = getenv("FLASH_QUERY_CSORT");
   const bool all_csort = cs_env && cs_env[0] == '1';
   int n = planned;
-  for (int c = 0; c < kClasses; ++c) {
+  for (int c = 0; c < kClasses && max_m; ++c) {
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
     const uint32_t* lc = lists + (uint64_t)c * a.nq;
     const uint32_t cap = class_max(c) < max_m ? class_max(c) : (uint32_t)max_m;
@@ -998,6 +1005,12 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
     else if (c < kSortClasses) r = launch_query_sort(a, class_max(c), lc, counts + c, s);
     else r = launch_class<14, 256>(a, lc, counts + c, hist_len, s);
     if (r == 0) r = launch_csort(a, cap, lc, counts + c, s);  // a warp class that does not fit
+    if (r < 0) return -1;
+    n += r;
+  }
+  if (mark_min < a.mmax) {  // the queries with more than mark_min candidates (query_mark.cu)
+    const int r = launch_query_mark(a, lists + (uint64_t)kClasses * a.nq, counts + kClasses,
+                                    lists + (uint64_t)kLists * a.nq + kLists, s);
     if (r < 0) return -1;
     n += r;
   }

@@ -46,6 +46,7 @@ constexpr uint32_t kMarkMaxL = 128;             // Q1: one thread per bucket, 8-
 constexpr uint32_t kStage = 2048;               // candidates staged for the bitmap reset
 constexpr uint32_t kScanWpt = 8;                // bitmap words per thread per scan round
 constexpr size_t kMarkMaxBitmapBytes = 96 * 1024;  // >= 2 CTAs per SM (and u16 word indices)
+constexpr uint32_t kMarkMinCandidates = 768;     // fewer: the size-class sort kernels
 
 struct MarkHdr {
   uint32_t nsingle, nrep, overflow, excl, nhi;
@@ -96,8 +97,9 @@ __device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], uint32_t j) {
   return (j & 4) ? cd : ab;
 }
 
-__global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32_t nwords, uint32_t rep_max,
-                                                            uint32_t* __restrict__ fb_list,
+__global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const uint32_t* __restrict__ qlist,
+                                                            const uint32_t* __restrict__ qcount, uint32_t nwords,
+                                                            uint32_t rep_max, uint32_t* __restrict__ fb_list,
                                                             uint32_t* __restrict__ fb_count) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ MarkHdr hdr;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
 
   // thread tid < L: table tid's bucket of query q (issued a phase before it is consumed)
   auto bucket_addr = [&](uint64_t q) -> uint32_t {
-    return q < a.nq ? (a.direct ? (uint32_t)q : a.addrs[q * L + tid]) : kEmpty;
+    return a.direct ? (uint32_t)q : a.addrs[q * L + tid];
   };
   auto bucket_extent = [&](uint32_t ad, uint64_t& st, uint32_t& sz) {
     st = 0;
@@ -141,6 +143,8 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
   auto exclude_of = [&](uint64_t q) -> uint32_t {
     return a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
   };
+  const uint64_t nq = qlist ? (uint64_t)*qcount : a.nq;  // this launch's queries
+  auto query_at = [&](uint64_t it) -> uint64_t { return qlist ? (uint64_t)qlist[it] : it; };
 
   {  // one-time reset (later queries reset what they touched)
     uint4* b4 = reinterpret_cast<uint4*>(bits);
@@ -153,19 +157,21 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
     for (uint32_t j = tid; j < stage_cap; j += kMarkThreads) stage[j] = 0;
     if (tid == 0) {
       hdr.nrep = hdr.overflow = 0;
-      hdr.excl = blockIdx.x < a.nq ? exclude_of(blockIdx.x) : kEmpty;
+      hdr.excl = blockIdx.x < nq ? exclude_of(query_at(blockIdx.x)) : kEmpty;
     }
   }
   uint32_t cur_ad = kEmpty, cur_sz = 0;
   uint64_t cur_st = 0;
-  if (tid < L) {
-    cur_ad = bucket_addr(blockIdx.x);
+  if (tid < L && blockIdx.x < nq) {
+    cur_ad = bucket_addr(query_at(blockIdx.x));
     bucket_extent(cur_ad, cur_st, cur_sz);
   }
   __syncthreads();
 
-  for (uint64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
-    const uint64_t qn = q + gridDim.x;  // this CTA's next query (prefetched)
+  for (uint64_t it = blockIdx.x; it < nq; it += gridDim.x) {
+    const uint64_t q = query_at(it);
+    const bool more = it + gridDim.x < nq;
+    const uint64_t qn = more ? query_at(it + gridDim.x) : 0;  // this CTA's next query (prefetched)
 
     // ---- Q1: scan of (size, non-empty) over the L buckets (sizes clamped above L*R: the
     //      sum then stays below 2^24; ranks < 2^8) ----
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
         if (lane >= o) x += y;
       }
       if (lane == 31) hdr.wsum[wib] = x;
-      if (tid < L) nx_ad = bucket_addr(qn);  // prefetch: the next query's addresses
+      if (tid < L && more) nx_ad = bucket_addr(qn);  // prefetch: the next query's addresses
     }
     __syncthreads();
     const uint32_t excl = hdr.excl;
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
         bucket_extent(cur_ad, cur_st, cur_sz);
       }
       __syncthreads();  // hdr is rewritten for the next query
-      if (tid == 0 && qn < a.nq) hdr.excl = exclude_of(qn);
+      if (tid == 0 && more) hdr.excl = exclude_of(qn);
       __syncthreads();
       continue;
     }
@@ -414,23 +420,33 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, uint32
     }
     if (tid == 0) {
       hdr.nrep = hdr.overflow = 0;
-      if (qn < a.nq) hdr.excl = exclude_of(qn);
+      if (more) hdr.excl = exclude_of(qn);
     }
   }
 }
 
 }  // namespace
 
-bool query_mark_eligible(const QueryArgs& a) {
+static bool query_mark_eligible(const QueryArgs& a) {
   const char* e = getenv("FLASH_QUERY_MARK");  // tests: 0 = the sort kernels
   if ((e && e[0] == '0') || a.L > kMarkMaxL || a.mmax > FLASH_MAX_CANDIDATES) return false;
   if ((size_t)mark_words(a.max_id) * 4 > kMarkMaxBitmapBytes) return false;
   return mark_smem_bytes(mark_words(a.max_id), a.L, a.mmax) <= 227 * 1024;
 }
 
-size_t query_mark_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq + 4); }
+// Queries with more candidates than this go to the bitmap kernel, the rest to the size-class
+// sort kernels: the bitmap kernel's cost per query is nearly flat in M (its bitmap scan ends
+// further out when fewer ids were seen), the sort kernels' grows with M; measured crossover
+// on the webspam sweep ~850 candidates (profiles/r02_sweep.txt).  FLASH_QUERY_MARK_MIN
+// (tests, tuning) overrides.
+uint32_t query_mark_min(const QueryArgs& a) {
+  if (!query_mark_eligible(a)) return 0xFFFFFFFFu;
+  const char* e = getenv("FLASH_QUERY_MARK_MIN");
+  return e ? (uint32_t)strtoul(e, nullptr, 10) : kMarkMinCandidates;
+}
 
-int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s) {
+int launch_query_mark(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t* fb,
+                      cudaStream_t s) {
   if (a.nq == 0) return 0;
   const uint32_t nwords = mark_words(a.max_id);
   const size_t smem = mark_smem_bytes(nwords, a.L, a.mmax);
@@ -438,8 +454,8 @@ int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_mark, kMarkThreads, smem);
   if (per_sm < 1) return -1;
-  uint32_t* fb_list = reinterpret_cast<uint32_t*>(scratch);
-  uint32_t* fb_count = fb_list + a.nq;
+  uint32_t* fb_list = fb;
+  uint32_t* fb_count = fb + a.nq;
   cudaMemsetAsync(fb_count, 0, sizeof(uint32_t), s);
   uint64_t grid = (uint64_t)device_sms() * per_sm;
   if (grid > a.nq) grid = a.nq;
@@ -448,7 +464,7 @@ int launch_query_mark(const QueryArgs& a, void* scratch, cudaStream_t s) {
   const char* e = getenv("FLASH_QUERY_MARK_REPMAX");
   uint32_t rep_max = e ? (uint32_t)strtoul(e, nullptr, 10) : kRepMax;
   if (rep_max > kRepMax) rep_max = kRepMax;
-  k_query_mark<<<(unsigned)grid, kMarkThreads, smem, s>>>(a, nwords, rep_max, fb_list, fb_count);
+  k_query_mark<<<(unsigned)grid, kMarkThreads, smem, s>>>(a, list, count, nwords, rep_max, fb_list, fb_count);
   // the queries with more than rep_max distinct repeated ids: the CTA sort kernel
   const int r = launch_csort(a, (uint32_t)a.mmax, fb_list, fb_count, s);
   if (r < 0) return -1;

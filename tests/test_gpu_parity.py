@@ -231,12 +231,16 @@ QUERY_CASES = [
 ]
 
 
-# query kernels: "mark" = the default (the occupancy-bitmap kernel when the ids fit its
-# bitmap), "sort" = FLASH_QUERY_MARK=0 (the size-class sort kernels), "fallback0" /
-# "fallback3" = the bitmap kernel with at most 0 / 3 distinct repeated ids per query, so
-# every / some queries go to its CTA-sort fallback list
-QUERY_KERNELS = {"mark": {}, "sort": {"FLASH_QUERY_MARK": "0"},
-                 "fallback0": {"FLASH_QUERY_MARK_REPMAX": "0"}, "fallback3": {"FLASH_QUERY_MARK_REPMAX": "3"}}
+# query kernels: "default" (queries with more than 768 candidates on the occupancy-bitmap
+# kernel when the ids fit its bitmap, the rest on the size-class sort kernels), "mark" /
+# "split" = every query / those above 100 candidates on the bitmap kernel, "sort" =
+# FLASH_QUERY_MARK=0 (sort kernels only), "fallback0" / "fallback3" = the bitmap kernel with
+# at most 0 / 3 distinct repeated ids per query, so every / some queries go to its CTA-sort
+# fallback list
+QUERY_KERNELS = {"default": {}, "mark": {"FLASH_QUERY_MARK_MIN": "0"}, "split": {"FLASH_QUERY_MARK_MIN": "100"},
+                 "sort": {"FLASH_QUERY_MARK": "0"},
+                 "fallback0": {"FLASH_QUERY_MARK_MIN": "0", "FLASH_QUERY_MARK_REPMAX": "0"},
+                 "fallback3": {"FLASH_QUERY_MARK_MIN": "0", "FLASH_QUERY_MARK_REPMAX": "3"}}
 
 
 def _set_kernel(monkeypatch, kern):

@@ -24,6 +24,7 @@ for ci, (name, n, (K, L, R, rng, k), tm) in enumerate(CASES):
     # query kernels: alternate the occupancy-bitmap kernel (with a forced fallback list on
     # every third case) and the size-class sort kernels
     os.environ["FLASH_QUERY_MARK"] = "1" if ci % 2 == 0 else "0"
+    os.environ["FLASH_QUERY_MARK_MIN"] = "0" if ci % 4 == 0 else "64"
     os.environ["FLASH_QUERY_MARK_REPMAX"] = "2" if ci % 3 == 0 else "224"
     rp, col = synth.generate(synth.SHAPES[name].with_(N=n))
     rows = [col[rp[i]:rp[i + 1]] for i in range(n)] + synth.edge_case_rows()

@@ -38,6 +38,7 @@ ap.add_argument("--queries", type=int, default=1000)
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
+HBM_PEAK = bench.peaks()[0]
 shape = synth.SHAPES["webspam"]
 t0 = time.time()
 h_rp, h_col, nnz = bench.gen_local(shape, [0, shape.N], 0)
@@ -77,12 +78,28 @@ for K in args.K:
                     if rep > 0:
                         times.append(e0.elapsed_time(e1))
                 ms, calls = flash.flash_phase_ms(idx.h)
+                # candidates per query (outside the timing): the sizes of its L buckets
+                addrs = idx.hash_addrs(d_rp, d_col).long() & 0xFFFFFFFF
+                goff = idx.table_arrays(ids=False)[0]
+                bidx = addrs + torch.arange(L, device=addrs.device)[None, :] * (1 << 15)
+                M = (goff[bidx + 1] - goff[bidx]).sum(1).double()
+                del addrs, bidx, goff
                 idx.close()
                 g = statistics.median(times)
+                qms = ms[2] / args.reps
                 r_at, s_at = bench.recall_at_k(cos, best, out_ids[qsel], k)
+                # query-phase roofline: SURVEY 8(d) bytes, (4L + 8L + 8k) B/query + 4 B/candidate
+                qbytes = (12 * L + 8 * k) * N + 4 * float(M.sum().item())
                 rec.update({"graph_ms": g, "queries_per_s": N / (g * 1e-3),
                             "hash_ms": ms[0] / args.reps, "build_ms": ms[1] / args.reps,
-                            "query_ms": ms[2] / args.reps, "R@k": r_at, "S@k": s_at})
+                            "query_ms": qms, "R@k": r_at, "S@k": s_at,
+                            "candidates_per_query": {"mean": float(M.mean().item()),
+                                                     "p99": float(torch.quantile(M[:100000], 0.99).item()),
+                                                     "max": float(M.max().item()), "of_LR": float(M.mean().item()) / (L * R)},
+                            "query_roofline": {"bound": "hbm", "bytes": qbytes,
+                                               "achieved_GBps": qbytes / (qms * 1e-3) / 1e9,
+                                               "peak_GBps": HBM_PEAK, "frac": qbytes / (qms * 1e-3) / 1e9 / HBM_PEAK,
+                                               "candidates_per_s": float(M.sum().item()) / (qms * 1e-3)}})
             except flash.FlashError as e:
                 rec["error"] = str(e)
             rows.append(rec)
