@@ -84,12 +84,7 @@ __device__ __forceinline__ void write_addrs(const uint32_t* code, bool nonempty,
   }
 }
 
-// kTable (256 < B <= kTableMaxB, the url shape: most bins empty): the probe chains are
-// tabulated once per CTA, ptab[(a-1)*B + i] = probe a of bin i (u16), so a probe is two
-// shared-memory loads instead of an fmix32 and a load (HASHSPEC H2 unchanged).
-constexpr uint32_t kTableMaxB = 768;
-
-template <bool kCodes, bool kAddrs, bool kTable>
+template <bool kCodes, bool kAddrs>
 __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict__ row_ptr,
                                                    const uint32_t* __restrict__ col_idx,
                                                    uint64_t n_rows, uint32_t K, uint32_t L,
@@ -101,16 +96,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t wpb = blockDim.x >> 5;
-  uint16_t* ptab = reinterpret_cast<uint16_t*>(smem);  // [kProbes][B] (kTable)
-  const uint32_t tab_words = kTable ? (kProbes * B + 1) / 2 : 0u;
-  if (kTable) {
-    for (uint32_t x = threadIdx.x; x < kProbes * B; x += blockDim.x) {
-      const uint32_t a = x / B + 1, i = x - (a - 1) * B;
-      ptab[x] = (uint16_t)__umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B);
-    }
-    __syncthreads();
-  }
-  uint32_t* v = smem + tab_words + (size_t)warp * warp_words(B);  // bin minima (pre-densification)
+  uint32_t* v = smem + (size_t)warp * warp_words(B);  // bin minima (pre-densification)
   uint32_t* code = v + B;                              // densified codes of the current row
   uint16_t* elist = reinterpret_cast<uint16_t*>(code + B);  // empty bins of the current row
 
@@ -194,8 +180,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
           uint32_t jl = 0;
 #pragma unroll
           for (uint32_t u = 0; u < kBatch; ++u) {
-            const uint32_t j = kTable ? (uint32_t)ptab[(a + u - 1) * B + i]
-                                      : __umulhi(fmix32(keys.s_dens ^ ((i << 8) | (a + u))), B);
+            const uint32_t j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | (a + u))), B);
             const uint32_t y = v[j];
             if (x == kEmpty) x = y;  // the first hit in chain order wins
             jl = j;
@@ -370,37 +355,20 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     skip_le = kSparseNnz;
   }
   const size_t per_warp = (size_t)warp_words(B) * sizeof(uint32_t);
-  if (B > kSparseMaxB && B <= kTableMaxB) {  // tabulated probe chains, persistent CTAs
-    const size_t tab = (size_t)((kProbes * B + 1) / 2) * 4;
-    const size_t smem = tab + per_warp * (kThreads / 32);
-    int per_sm = 0;
-    if (ensure_smem_attr((const void*)k_doph<C, A, true>, smem, true))
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph<C, A, true>, kThreads, smem);
-    if (per_sm >= 1) {  // (else the untabulated kernel below)
-      uint64_t blocks = (uint64_t)device_sms() * per_sm;
-      const uint64_t need = (n_rows + kThreads / 32 - 1) / (kThreads / 32);
-      if (blocks > need) blocks = need;
-      if (blocks == 0) return launched;
-      k_doph<C, A, true><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                                  codes, out, skip_le);
-      return launched + 1;
-    }
-    cudaGetLastError();
-  }
   int wpb = (int)((96 * 1024) / per_warp);
   wpb = wpb < 1 ? 1 : (wpb > kThreads / 32 ? kThreads / 32 : wpb);
   const size_t smem = per_warp * wpb;
   // the column stream bypasses L1 (no_allocate): give the whole carveout to shared memory,
   // so the per-warp bin arrays never cap the resident warps below the thread limit
-  ensure_smem_attr((const void*)k_doph<C, A, false>, smem, true);
+  ensure_smem_attr((const void*)k_doph<C, A>, smem, true);
   uint64_t blocks = (n_rows + wpb - 1) / wpb;  // one warp per row: the block scheduler balances
   // the skewed row lengths; with the sparse kernel in use, a grid-stride cap keeps the launch
   // from scheduling millions of CTAs that would only skip sparse rows
   const uint64_t cap = skip_le >= 0 ? 65536ull : 0x7FFFFFFFull;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return launched;
-  k_doph<C, A, false><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                                codes, out, skip_le);
+  k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
+                                                         codes, out, skip_le);
   return launched + 1;
 }
 

@@ -596,6 +596,9 @@ flash_status flash_knn_graph(flash_index* h, const int64_t* row_ptr, const uint3
     void* scratch;
     uint64_t launches;
   } ctx{h, query_args(h, addrs, n_rows, k, nullptr, 1, 0, out_ids, out_counts, h->cur), h->qscratch.p, 0};
+  // the ids about to be inserted are 0..n_rows-1 (a fresh handle): the plan's routing between
+  // the bitmap and sort kernels must see the same max_id as the query launch after the build
+  ctx.a.max_id = (uint32_t)(n_rows - 1);
   auto plan = [](void* c, cudaStream_t side) {
     PlanCtx* p = static_cast<PlanCtx*>(c);
     // a fresh handle builds into goff[cur]; allocated by now

@@ -341,6 +341,20 @@ def test_knn_graph_bit_exact(monkeypatch, name, make, K, L, R, rng, k, kern):
         assert np.array_equal(out_c.numpy().view(np.uint32), o_cnt)
 
 
+def test_knn_graph_ids_beyond_the_bitmap_kernel():
+    """800,000 rows: the ids no longer fit the bitmap kernel's shared-memory bitmap, so every
+    query goes to the sort kernels — also in flash_knn_graph, whose size-class plan runs
+    during the build (before the handle has counted the inserted ids)."""
+    rp, col = shape_slice("kdd12", 800_000)
+    K, L, R, rng, k, seed = 4, 32, 64, 1 << 18, 16, 0x5EED0004
+    o_ids, o_cnt = oracle.knn_graph(K, L, R, rng, seed, rp, col, k)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        g_ids, g_cnt = idx.knn_graph(d_rp, d_col, k)
+        assert np.array_equal(flash.as_u32(g_ids), o_ids)
+        assert np.array_equal(flash.as_u32(g_cnt), o_cnt)
+
+
 def test_graph_is_deterministic_across_runs_and_streams():
     rp, col = shape_slice("webspam", 3000)
     d_rp, d_col = flash.to_device_csr(rp, col)
