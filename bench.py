@@ -42,7 +42,9 @@ import synth  # noqa: E402
 K, L, R, RANGE, SEED, TOPK = 4, 50, 128, 1 << 15, 0x5EED0002, 128
 METRIC = "webspam-shaped k-NN graph time (s), queries/s, hash nnz/s at 1/2/4/8 B200"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+# the newest committed ncu --set full summary of one webspam graph (tools/refresh_profiles.sh)
+TRAFFIC_PATH = next((p for p in (os.path.join(ROOT, "profiles", f"r0{i}_ncu_full_summary.json") for i in (2, 1))
+                     if os.path.exists(p)), os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json"))
 # Shared-memory RMW throughput measured on this pool's B200 (profiles/r01_microbench_smem.txt:
 # RED.S.ADD on random addresses, 8.76 lane-ops/clk/SM at 1.9 GHz x 148 SMs): the ceiling
 # for the count step, which needs at least one shared-memory RMW per candidate.
@@ -236,6 +238,65 @@ def exact_cosine(crow, col, cnt, qs, B=64):
         cos[qb, torch.arange(nb, device=dev)] = -1.0                      # exclude self
         out[:, b0:b0 + nb] = cos
     return out, out.max(0).values
+
+
+def heavy_recall(h_rp, d_col, top_ids, qs, thr, batch=32):
+    """Recall of the neighbours whose exact binary cosine exceeds thr in the reported top-k
+    (the friendster metric of P:507: "recall of neighbors with similarity > 0.65 ... in the
+    top 20"), for the query rows qs.  Exact cosines through a column index of the
+    deduplicated rows (every row sharing a column with the query), on the device.
+    Evaluation only."""
+    import torch
+
+    crow, col, cnt, key = dedup_csr(h_rp, d_col)
+    dev = col.device
+    ckey = torch.sort(((key & 0xFFFFFFFF) << 32) | (key >> 32)).values  # (col, row), sorted
+    del key
+    ccol = ckey >> 32
+    D = int(ccol[-1].item()) + 1 if ccol.numel() else 1
+    cptr = torch.zeros(D + 1, dtype=torch.int64, device=dev)
+    cptr[1:] = torch.cumsum(torch.bincount(ccol, minlength=D), 0)
+    crows = ckey & 0xFFFFFFFF
+    del ccol, ckey
+    top = top_ids.to(dev).long()
+    hit = tot = 0
+
+    def expand(starts, lens):  # starts[i] + [0, lens[i]) for every i, and the owner index
+        own = torch.repeat_interleave(torch.arange(lens.numel(), device=dev), lens)
+        first = torch.cumsum(lens, 0) - lens
+        return starts[own] + torch.arange(own.numel(), device=dev) - first[own], own
+
+    for b0 in range(0, len(qs), batch):
+        qb = torch.as_tensor(np.asarray(qs[b0:b0 + batch]), device=dev, dtype=torch.int64)
+        pos, qi = expand(crow[qb], cnt[qb])
+        qc = col[pos].long()                                  # the queries' columns
+        ppos, pi = expand(cptr[qc], cptr[qc + 1] - cptr[qc])  # their posting lists
+        u, inter = torch.unique((qi[pi] << 32) | crows[ppos], return_counts=True)
+        uq, ur = u >> 32, u & 0xFFFFFFFF
+        cosv = inter.double() / torch.sqrt(cnt[qb][uq].double() * cnt[ur].double())
+        heavy = (cosv > thr) & (ur != qb[uq])
+        hq, hr = uq[heavy], ur[heavy]
+        tot += int(heavy.sum().item())
+        hit += int((top[qb[hq]] == hr[:, None]).any(1).sum().item())
+    return {"queries": int(len(qs)), "threshold": thr, "heavy_neighbours": tot, "recall": hit / max(tot, 1)}
+
+
+def graph_candidates(idx, d_rp, d_col, n, L, range_, chunk=1 << 22):
+    """Candidates per query of a k-NN graph (the sum of its L bucket sizes), from the
+    rows' addresses and the built index's offsets (evaluation only): int64 [n] on the device."""
+    import torch
+
+    goff = idx.table_arrays(ids=False)[0]
+    tb = torch.arange(L, device=goff.device, dtype=torch.int64)[None, :] * range_
+    out = torch.empty(n, dtype=torch.int64, device=goff.device)
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        rp = d_rp[r0:r1 + 1]
+        a = idx.hash_addrs(rp, d_col).long() & 0xFFFFFFFF
+        valid = a != 0xFFFFFFFF
+        b = torch.where(valid, a + tb, torch.zeros_like(a))
+        out[r0:r1] = torch.where(valid, goff[b + 1] - goff[b], torch.zeros_like(a)).sum(1)
+    return out
 
 
 def recall_at_k(cos, best, top_ids, kmax):
@@ -472,10 +533,12 @@ def run_ours(args):
             pass
         peak_all = hbm_peak * world  # GB/s over the job's GPUs
         if dominant == "query":
-            q_traffic = (sum(traffic.get(nm, 0.0) for nm in ("k_query_sort", "k_query", "k_query_csort", "k_query_plan"))
-                         if "k_query_sort" in traffic and world == 1 else None)
-            roof = {"kernel": "query phase: k_query_plan + k_query_sort<MCAP,BL> size classes (+ k_query / "
-                              "k_query_csort for M > 4096)" + ("; + k_dist_gather peer stores" if world > 1 else ""),
+            qk = ("k_query_mark", "k_query_sort", "k_query", "k_query_csort", "k_query_plan")
+            q_traffic = (sum(traffic.get(nm, 0.0) for nm in qk)
+                         if any(nm in traffic for nm in qk[:2]) and world == 1 else None)
+            roof = {"kernel": "query phase: k_query_plan, then k_query_mark (occupancy bitmap, queries with > 768 "
+                              "candidates) and the k_query_sort<MCAP,BL> size classes (the rest)"
+                              + ("; + k_dist_gather peer stores" if world > 1 else ""),
                     "bound": "hbm", "achieved": query_bytes / (query_ms * 1e-3) / 1e9, "peak": peak_all,
                     "unit": "GB/s", "peak_kind": peak_kind, "traffic": q_traffic, "algorithmic_bytes": query_bytes,
                     "bytes_formula": "(4L + 8L + 8k) B/query + 4 B/candidate (SURVEY 8(d))", "candidates": n_cand,
@@ -483,12 +546,13 @@ def run_ours(args):
                     "smem_view": {"achieved_candidates_per_s": n_cand / (query_ms * 1e-3), "peak": SMEM_RMW_PEAK * world,
                                   "frac": n_cand / (query_ms * 1e-3) / (SMEM_RMW_PEAK * world),
                                   "peak_kind": "measured smem RMW microbench (profiles/r01_microbench_smem.txt)"}}
-            if "k_query_sort" in issue and world == 1:
+            if any(nm in issue for nm in ("k_query_mark", "k_query_sort")) and world == 1:
                 # instruction-issue view from the committed ncu capture: warp instructions
-                # issued per second by the sort kernels vs 4 schedulers x 148 SMs x clock
-                w, t = issue["k_query_sort"]
+                # issued per second by the query kernels vs 4 schedulers x 148 SMs x clock
+                w = sum(issue.get(nm, (0.0, 0.0))[0] for nm in ("k_query_mark", "k_query_sort"))
+                t = sum(issue.get(nm, (0.0, 0.0))[1] for nm in ("k_query_mark", "k_query_sort"))
                 peak_issue = 4 * 148 * clk_mhz_for_peak() * 1e6
-                roof["issue_view"] = {"kernel": "k_query_sort (all classes, ncu)", "warp_inst": w,
+                roof["issue_view"] = {"kernel": "k_query_mark + k_query_sort (ncu)", "warp_inst": w,
                                       "warp_inst_per_query": w / N, "achieved_warp_inst_per_s": w / (t * 1e-3),
                                       "peak_warp_inst_per_s": peak_issue, "frac": w / (t * 1e-3) / peak_issue}
         elif dominant == "build":
@@ -557,11 +621,14 @@ SHAPE_CFG = {
     "kdd12": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0004, k=128, q=10_000, qseed=14),
     # the friendster 20-NN graph from scratch (the paper
     # gives no K/L/R for it: kdd12's K=4, L=32, R=64, 2^20 for a dataset of that scale)
-    "friendster": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0005, k=20, graph=True,
+    "friendster": dict(K=4, L=32, R=64, range_=1 << 20, seed=0x5EED0005, k=20, graph=True, heavy_thr=0.65,
                        paper="friendster 20-NN graph from scratch: 1578 s on 2x Xeon E5-2660 v4, 56 threads (P:505)"),
     # the 10 K-query url line is latency-scale, so also the full url graph
     # (Q = N = 2.39 M queries, ~L*R = 4096 candidates each: the CTA-per-query class)
     "url-graph": dict(shape="url", K=4, L=128, R=32, range_=1 << 15, seed=0x5EED0003, k=128, graph=True),
+    # saturated buckets beside the headline: the webspam rows and index with
+    # 2^10 buckets per table, so buckets hold ~342 arrivals > R and a query gathers ~L*R
+    "webspam-sat": dict(shape="webspam", K=4, L=50, R=128, range_=1 << 10, seed=0x5EED0002, k=128, graph=True),
 }
 
 
@@ -644,8 +711,23 @@ def run_shape_graph(args, cfg, shape):
     lens = np.diff(h_rp.numpy())
     hbm_peak, peak_kind = peaks()
     hash_ms = phase_ms[0] / args.steps
+    query_ms = phase_ms[2] / args.steps
     hash_bytes = 4 * nnz + 8 * (shape.N + 1) + 4 * cfg["L"] * shape.N
+    # after the timed region: candidates per query and the query-phase roofline (SURVEY 8(d)
+    # bytes), and the quality metric the paper quotes for this run, if any
+    M = graph_candidates(idx, d_rp, d_col, shape.N, cfg["L"], cfg["range_"]).double()
+    n_cand = float(M.sum().item())
+    qbytes = (12 * cfg["L"] + 8 * k) * shape.N + 4 * n_cand
+    cand = {"mean": float(M.mean().item()), "p99": float(torch.quantile(M[:1 << 20], 0.99).item()),
+            "max": float(M.max().item()), "of_LR": float(M.mean().item()) / (cfg["L"] * cfg["R"])}
+    del M
     idx.close()
+    quality = None
+    if cfg.get("heavy_thr") and not args.no_quality:
+        qs = np.sort(np.random.default_rng(13).choice(shape.N, size=args.quality_queries, replace=False))
+        quality = heavy_recall(h_rp, d_col, out_ids, qs, cfg["heavy_thr"])
+        quality["definition"] = ("recall of the neighbours with exact binary cosine > threshold in the reported "
+                                 f"top-{k}, over {qs.size} sampled rows (P:507)")
     return {
         "metric": METRIC, "value": shape.N / (ms * 1e-3), "unit": "queries/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "graph_time_s": ms * 1e-3,
@@ -655,9 +737,14 @@ def run_shape_graph(args, cfg, shape):
                           "achieved": hash_bytes / (hash_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                           "peak_kind": peak_kind, "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / hbm_peak,
                           "algorithmic_bytes": hash_bytes},
+        "query_roofline": {"kernel": "query phase", "bound": "hbm", "achieved": qbytes / (query_ms * 1e-3) / 1e9,
+                           "peak": hbm_peak, "unit": "GB/s", "frac": qbytes / (query_ms * 1e-3) / 1e9 / hbm_peak,
+                           "algorithmic_bytes": qbytes, "candidates": n_cand,
+                           "candidates_per_s": n_cand / (query_ms * 1e-3)},
+        "candidates_per_query": cand, "quality": quality,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": f"synthetic (synth/, {shape.name} shape, seed {shape.seed})",
-        "config": {"workload": f"{shape.name}-shaped approximate {k}-NN graph from scratch",
+        "config": {"workload": f"{args.workload}: {shape.name}-shaped approximate {k}-NN graph from scratch",
                    "N": shape.N, "D": shape.D, "nnz": nnz, "nnz_per_row": round(nnz / shape.N, 1),
                    "K": cfg["K"], "L": cfg["L"], "R": cfg["R"], "range": cfg["range_"], "k": k,
                    "seed": cfg["seed"], "parallelism": "1 GPU",
@@ -862,7 +949,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
     ap.add_argument("--quality-queries", type=int, default=1000)
-    ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster", "url-graph"], default="webspam",
+    ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster", "url-graph", "webspam-sat"],
+                    default="webspam",
                     help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines; "
                          "friendster / url-graph = full k-NN graphs of those shapes")
     args = ap.parse_args()

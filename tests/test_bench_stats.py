@@ -1,9 +1,11 @@
 """bench.py's data / quality statistics (pairwise cosine, 1-NN cosine, R@k,
 S@k of P:391-395) against a brute force written out with Python sets (CPU, small)."""
 import numpy as np
+import pytest
 import torch
 
 import bench
+import oracle
 import synth
 
 
@@ -52,3 +54,51 @@ def test_bench_entry_points_exist():
     for fn in ("run_ours", "run_shape", "run_reference", "cpu_baseline", "main", "data_quality_stats",
                "exact_cosine", "recall_at_k", "shape_stats"):
         assert callable(getattr(bench, fn)), fn
+
+
+@pytest.mark.gpu
+def test_gpu_exact_cosine_matches_oracle_brute_force():
+    """T5: the bench's GPU evaluator (deduplicated CSR x dense query mask, torch
+    sparse, fp32 products -> fp64 ratios) gives every exact binary cosine (Eq. 3)
+    within 1e-6 of the fp64 oracle O-2 (oracle.bruteforce_topk), and the same 1-NN value."""
+    shape = synth.SHAPES["webspam"].with_(N=3000)
+    rp, col = synth.generate(shape)
+    n = rp.size - 1
+    qs = np.random.default_rng(5).choice(n, size=40, replace=False)
+    d_col = torch.from_numpy(col.view(np.int32)).cuda()
+    crow, dcol, cnt, _ = bench.dedup_csr(torch.from_numpy(rp), d_col)
+    cos, best = bench.exact_cosine(crow, dcol, cnt, qs)
+    cos = cos.cpu().numpy()
+    o_ids, o_sim = oracle.bruteforce_topk(rp, col, qs, 50, metric="cosine")
+    for j in range(qs.size):
+        g = cos[o_ids[j].astype(np.int64), j]
+        assert np.max(np.abs(g - o_sim[j])) <= 1e-6
+        assert abs(float(best[j]) - o_sim[j, 0]) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_heavy_neighbour_recall_matches_brute_force():
+    """bench.heavy_recall (the friendster metric of P:507: recall of neighbours with cosine
+    above a threshold in the reported top-k), computed on the GPU through a column index,
+    equals the same recall from the oracle's exact brute force."""
+    shape = synth.SHAPES["friendster"].with_(N=4000, D=4000)
+    rp, col = synth.generate(shape)
+    n = rp.size - 1
+    k, thr = 20, 0.65
+    rng = np.random.default_rng(3)
+    out = rng.integers(0, n, size=(n, k)).astype(np.int32)
+    qs = np.sort(rng.choice(n, size=200, replace=False))
+    o_ids, o_sim = oracle.bruteforce_topk(rp, col, qs, 200, metric="cosine")
+    for j, q in enumerate(qs[::2]):  # plant half of the heavy neighbours of every other query
+        heavy = o_ids[2 * j][o_sim[2 * j] > thr]
+        out[q, :min(k, heavy.size // 2)] = heavy[:min(k, heavy.size // 2)]
+    got = bench.heavy_recall(torch.from_numpy(rp), torch.from_numpy(col.view(np.int32)).cuda(),
+                             torch.from_numpy(out).cuda(), qs, thr)
+    hit = tot = 0
+    for j, q in enumerate(qs):
+        assert o_sim[j, -1] <= thr or o_sim[j, -1] < 0, "brute-force list too short for the threshold"
+        heavy = set(o_ids[j][o_sim[j] > thr].tolist())
+        tot += len(heavy)
+        hit += len(heavy & set(out[q].tolist()))
+    assert got["heavy_neighbours"] == tot and tot > 0
+    assert abs(got["recall"] - hit / tot) < 1e-12

@@ -5,7 +5,7 @@
 # profiles/ afterwards.  Order matters: the bench reads the ncu --set full summary for
 # its roofline traffic, so that capture runs first and is installed into profiles/ here.
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 export PYTHONUNBUFFERED=1
@@ -31,6 +31,7 @@ timeout 600 python bench.py --workload url --steps 3 --warmup 3 > "$OUT/${TAG}_b
 timeout 900 python bench.py --workload kdd12 --steps 3 --warmup 3 > "$OUT/${TAG}_bench_kdd12.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --workload friendster --steps 3 --warmup 3 > "$OUT/${TAG}_bench_friendster.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --workload url-graph --steps 3 --warmup 3 > "$OUT/${TAG}_bench_url_graph.json" 2>> "$OUT/bench.log"
+timeout 900 python bench.py --workload webspam-sat --steps 5 --warmup 3 > "$OUT/${TAG}_bench_webspam_sat.json" 2>> "$OUT/bench.log"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/${TAG}_bench_reference.json" 2>> "$OUT/bench.log"
 # 4. the K x L x R sweep (80 graphs, ~1 min)
 timeout 1200 python tools/sweep.py --out "$OUT/${TAG}_sweep.json" > /dev/null 2>> "$OUT/bench.log"
