@@ -232,15 +232,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
 //   first[j*B + i] = the first position a <= T at which bin i's chain probes bin j
 //                    (255: never), data-independent (HASHSPEC H2).
 // An empty bin's donor is then the non-empty bin j minimising first[j*B + i] — the same
-// bin the chain reaches first — found with |NE| (<= nnz) uniform table lookups per lane,
-// no divergence.  A bin whose T probes all miss falls back to the circular scan from its
+// bin the chain reaches first.  Lane l owns bins 4l..4l+3 of every 128-bin chunk: for each
+// of the |NE| (<= nnz) non-empty bins j it loads the 4 table bytes of its bins in one word
+// and keeps two packed 16-bit minima of (first << 8 | rank of j in the NE list)
+// (__vminu2), so the argmin over j costs ~7 instructions per 4 bins, uniform, no
+// divergence.  A bin whose T probes all miss falls back to the circular scan from its
 // last probe, i.e. the first non-empty bin after it (a search in the sorted NE list).
 // One warp per row; persistent CTAs (the table is built once per CTA).
 constexpr uint32_t kSparseNnz = 32;
 constexpr uint32_t kSparseMaxB = 256;
 
+__host__ __device__ __forceinline__ uint32_t sparse_stride(uint32_t B) { return (B + 127) & ~127u; }
 __host__ __device__ __forceinline__ uint32_t sparse_warp_words(uint32_t B) {
-  return 2 * B + (B + 3) / 4 + (B + 3) / 4;  // v[B], code[B], u8 NE list, u8 empty list
+  return 2 * B + (B + 3) / 4;  // v[B], code[B], u8 NE list
 }
 
 template <bool kCodes, bool kAddrs>
@@ -252,17 +256,17 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  uint8_t* first = reinterpret_cast<uint8_t*>(smem);  // [B][B]
-  uint32_t* v = smem + (B * B + 3) / 4 + (size_t)warp * sparse_warp_words(B);
+  const uint32_t Bs = sparse_stride(B);               // table row stride (bytes), 128-multiple
+  uint8_t* first = reinterpret_cast<uint8_t*>(smem);  // [B][Bs], 255 = never
+  uint32_t* v = smem + B * Bs / 4 + (size_t)warp * sparse_warp_words(B);
   uint32_t* code = v + B;
   uint8_t* nel = reinterpret_cast<uint8_t*>(code + B);  // non-empty bins, ascending
-  uint8_t* eel = nel + ((B + 3) & ~3u);                 // empty bins
 
-  for (uint32_t x = threadIdx.x; x < (B * B + 3) / 4; x += blockDim.x) smem[x] = 0xFFFFFFFFu;
+  for (uint32_t x = threadIdx.x; x < B * Bs / 4; x += blockDim.x) smem[x] = 0xFFFFFFFFu;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x)
     for (uint32_t a = kProbes; a >= 1; --a)  // descending: the smallest position wins
-      first[__umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B) * B + i] = (uint8_t)a;
+      first[__umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B) * Bs + i] = (uint8_t)a;
   __syncthreads();
 
   const uint64_t nw = (uint64_t)gridDim.x * wpb;
@@ -280,49 +284,51 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
     __syncwarp();
     if (e0 + (int64_t)lane < e1) bin_min(v, B, keys, col_idx[e0 + lane]);  // H1
     __syncwarp();
-    // NE / empty lists (ascending bin order); non-empty bins keep their minimum
-    uint32_t nne = 0, ne = 0;
+    // NE list (ascending bin order)
+    uint32_t nne = 0;
     for (uint32_t i0 = 0; i0 < B; i0 += 32) {
       const uint32_t i = i0 + lane;
-      const uint32_t x = i < B ? v[i] : kEmpty;
-      const bool full = x != kEmpty;
-      if (full) code[i] = x;
+      const bool full = i < B && v[i] != kEmpty;
       const uint32_t mf = __ballot_sync(0xFFFFFFFFu, full);
-      const uint32_t me = __ballot_sync(0xFFFFFFFFu, i < B && !full);
       if (full) nel[nne + __popc(mf & lanemask_lt_d())] = (uint8_t)i;
-      if (i < B && !full) eel[ne + __popc(me & lanemask_lt_d())] = (uint8_t)i;
       nne += __popc(mf);
-      ne += __popc(me);
     }
     __syncwarp();
     const bool nonempty = nne > 0;
-    for (uint32_t e = lane; e < ne; e += 32) {  // H2 (R#4) by table lookups
-      const uint32_t i = eel[e];
-      uint32_t x = kEmpty;
-      if (nonempty) {
-        uint32_t best = 255, dj = 0;
-        for (uint32_t k = 0; k < nne; ++k) {
-          const uint32_t j = nel[k];
-          const uint32_t f = first[j * B + i];
-          if (f < best) {
-            best = f;
-            dj = j;
-          }
-        }
-        if (best == 255) {  // every probe missed: first non-empty bin after the T-th probe
-          const uint32_t j0 = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | kProbes)), B);
-          dj = nel[0];
-          for (uint32_t k = 0; k < nne; ++k) {
-            const uint32_t j = nel[k];
-            if (j > j0) {
-              dj = j;
-              break;
+    // H2 (R#4): per 128-bin chunk, lane l's bins 4l..4l+3 take the NE bin of smallest first
+    for (uint32_t c0 = 0; c0 < B; c0 += 128) {
+      const uint32_t ib = c0 + 4 * lane;
+      uint32_t m01 = 0xFFFFFFFFu, m23 = 0xFFFFFFFFu;  // (first << 8 | NE rank) per bin, 16-bit
+      for (uint32_t kk = 0; kk < nne; ++kk) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(first + nel[kk] * Bs + ib);
+        m01 = __vminu2(m01, __byte_perm(w, kk, 0x1404));  // bins ib, ib+1
+        m23 = __vminu2(m23, __byte_perm(w, kk, 0x3424));  // bins ib+2, ib+3
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t i = ib + q;
+        if (i >= B) break;
+        uint32_t x = v[i];
+        if (x == kEmpty && nonempty) {
+          const uint32_t r16 = ((q < 2 ? m01 : m23) >> (16 * (q & 1))) & 0xFFFFu;
+          uint32_t dj;
+          if ((r16 >> 8) != 255) {
+            dj = nel[r16 & 0xFF];
+          } else {  // every probe missed: first non-empty bin after the T-th probe
+            const uint32_t j0 = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | kProbes)), B);
+            dj = nel[0];
+            for (uint32_t kk = 0; kk < nne; ++kk) {
+              const uint32_t j = nel[kk];
+              if (j > j0) {
+                dj = j;
+                break;
+              }
             }
           }
+          x = v[dj];
         }
-        x = v[dj];
+        code[i] = x;
       }
-      code[i] = x;
     }
     __syncwarp();
     if (kCodes)
@@ -341,7 +347,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int launched = 0;
   int64_t skip_le = -1;
   if (B <= kSparseMaxB) {  // rows with <= kSparseNnz nonzeros: the table-driven kernel
-    const size_t smem = ((size_t)(B * B + 3) / 4 + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
+    const size_t smem = ((size_t)B * sparse_stride(B) / 4 + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
     ensure_smem_attr((const void*)k_doph_sparse<C, A>, 100 * 1024, true);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);

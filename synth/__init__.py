@@ -167,7 +167,7 @@ def edge_case_rows(seed: int = 7) -> list[np.ndarray]:
     rows.append(base.copy())
     rows.append(base[::-1].copy())                                        # permuted copy
     rows.append(np.concatenate([base, base[:50]]))                        # duplicated entries
-    rows.append(rng.integers(0, 1 << 32 - 1, size=70_000, dtype=np.uint64).astype(np.uint32))  # long row
+    rows.append(rng.integers(0, 1 << 32 - 1, size=1_000_000, dtype=np.uint64).astype(np.uint32))  # 10^6-nnz row
     rows.append(np.zeros(0, np.uint32))                                   # another empty
     for _ in range(6):
         rows.append(base.copy())                                          # identical rows

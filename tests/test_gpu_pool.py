@@ -125,11 +125,18 @@ def test_save_load_round_trip_then_further_inserts(tmp_path, F):
         a.save(str(tmp_path / "idx.npz"))
         want = a.query(d_rp, d_col, k)
         g0, i0, r0 = a.table_arrays()
+    # the anchor: the oracle's index over the first h rows answers the same
+    P = oracle.pool_size(F, L, rng)
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    T = oracle.build_pool(L, R, rng, P, seed, addrs[:h], np.arange(h, dtype=np.uint32))
+    o_ids, o_cnt = oracle.query_pool(T, seed, addrs, k)
     with flash.FlashIndex.load(str(tmp_path / "idx.npz")) as b:
         g1, i1, r1 = b.table_arrays()
         assert torch.equal(g0 - g0[0], g1 - g1[0]) and torch.equal(i0, i1) and torch.equal(r0, r1)
+        _check_pool(b, T)
         got = b.query(d_rp, d_col, k)
         assert torch.equal(want[0], got[0]) and torch.equal(want[1], got[1])
+        assert np.array_equal(flash.as_u32(got[0]), o_ids) and np.array_equal(flash.as_u32(got[1]), o_cnt)
         flash.flash_insert(b.h, d_rp[h:].contiguous(), d_col, n - h, h)
         with flash.FlashIndex(K, L, R, rng, seed, F=F) as c:
             c.insert(d_rp, d_col, 0)
