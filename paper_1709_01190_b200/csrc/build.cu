@@ -201,6 +201,224 @@ __global__ void __launch_bounds__(256) k_fill_tm(const uint32_t* __restrict__ ad
   }
 }
 
+// Grouped table-major passes (fresh builds of tables whose per-bucket arrays do not fit
+// L2, e.g. kdd12: 32 tables x 2^20 buckets, ~143 arrivals per bucket).  The plain
+// table-major scatter (k_count_tm / k_fill_tm) issues one global atomic and one isolated
+// 4-B store per (table, row) into a 600 MB-per-table pool, so almost every store is a
+// partial-sector write to HBM.  Instead the (table, row) entries are first partitioned by
+// bucket GROUP (2^gshift consecutive buckets, <= 2048 groups per table, so each chunk's
+// CTA has <= 2048 open output runs and the partial sectors combine in L2):
+//   k_gcount    CTA per (table, 2^21-row chunk): group histogram in shared memory;
+//   scan        (table, group, chunk)-major exclusive scan -> each chunk's slot range in
+//               every group (the entries of a group are contiguous, chunks in order);
+//   k_gscatter  the same CTAs write packed entries (bucket within the group << 21 | row
+//               within the chunk) into their group slots — runs of ~250 entries;
+//   k_gplace    1024-thread CTA per group, one per SM: counts its buckets (the arrivals,
+//               into `cursor` for k_pool_sizes), and places its rows bucket by bucket into
+//               the pool range the group occupies — exactly where the later exclusive scan
+//               of the bucket counts puts these buckets (a fresh build has no old kept ids,
+//               and group order is bucket order); the 148 ranges in flight (~290 KB each for
+//               kdd12) stay in L2, so the scattered stores combine there.
+// The bucket-contiguous pool then goes through the usual k_pool_sizes / scans / selects.
+constexpr uint32_t kGChunkLog2 = 21;  // rows per chunk: local row ids in 21 bits
+constexpr uint32_t kGMaxGroups = 2048;
+constexpr uint32_t kGMaxShift = 11;   // bucket within a group in 11 bits: range <= 2^24
+constexpr int kGThreads = 1024;
+constexpr int kGPlaceThreads = 1024;
+
+struct GroupGeom {
+  uint32_t gshift, ng, nch;
+};
+
+GroupGeom group_geom(uint32_t range, uint64_t n) {
+  uint32_t gs = 7;
+  while ((((uint64_t)range + (1ull << gs) - 1) >> gs) > kGMaxGroups) ++gs;
+  return {gs, (uint32_t)(((uint64_t)range + (1ull << gs) - 1) >> gs),
+          (uint32_t)((n + (1ull << kGChunkLog2) - 1) >> kGChunkLog2)};
+}
+
+__global__ void __launch_bounds__(kGThreads) k_gcount(const uint32_t* __restrict__ addrsT, uint64_t n,
+                                                      uint32_t range, GroupGeom g, uint64_t* __restrict__ ghist,
+                                                      unsigned long long* err) {
+  extern __shared__ uint32_t gcnt[];  // [ng]
+  const uint32_t j = blockIdx.x / g.nch, c = blockIdx.x - j * g.nch;
+  for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) gcnt[i] = 0;
+  __syncthreads();
+  const uint64_t r0 = (uint64_t)c << kGChunkLog2;
+  const uint64_t r1 = n - r0 < (1ull << kGChunkLog2) ? n : r0 + (1ull << kGChunkLog2);
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += 4 * kGThreads) {
+    uint32_t a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = r + u * kGThreads < r1 ? col[r + u * kGThreads] : kEmpty;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (a[u] < range) atomicAdd(&gcnt[a[u] >> g.gshift], 1u);
+      else if (a[u] != kEmpty) atomicAdd(err, 1ull);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) ghist[((uint64_t)j * g.ng + i) * g.nch + c] = gcnt[i];
+}
+
+// (tiles of kGTile rows are counting-sorted by group in shared memory first, so each
+// warp store writes runs of one group's consecutive slots)
+constexpr uint32_t kGTile = 16384;
+
+__host__ __device__ inline size_t gscatter_smem(uint32_t ng) {
+  return (size_t)ng * (8 + 4 + 4 + 4) + (size_t)kGTile * (4 + 2);
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) k_gscatter(const uint32_t* __restrict__ addrsT, uint64_t n,
+                                                           uint32_t range, GroupGeom g,
+                                                           const uint64_t* __restrict__ goffs, uint32_t* __restrict__ ent) {
+  extern __shared__ uint64_t gbase[];                              // [ng] slot bases of this chunk
+  uint32_t* gcur = reinterpret_cast<uint32_t*>(gbase + g.ng);       // [ng] slots used so far
+  uint32_t* tcnt = gcur + g.ng;                                     // [ng] this tile's counts
+  uint32_t* toff = tcnt + g.ng;                                     // [ng] this tile's group starts
+  uint32_t* stage = toff + g.ng;                                    // [kGTile] entries, by group
+  uint16_t* sgrp = reinterpret_cast<uint16_t*>(stage + kGTile);     // [kGTile] their groups
+  __shared__ uint32_t wsum[kGThreads / 32];
+  constexpr uint32_t E = kGTile / kGThreads;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t j = blockIdx.x / g.nch, c = blockIdx.x - j * g.nch;
+  for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) {
+    gbase[i] = goffs[((uint64_t)j * g.ng + i) * g.nch + c];
+    gcur[i] = 0;
+  }
+  const uint64_t r0 = (uint64_t)c << kGChunkLog2;
+  const uint64_t r1 = n - r0 < (1ull << kGChunkLog2) ? n : r0 + (1ull << kGChunkLog2);
+  const uint32_t* col = addrsT + (uint64_t)j * n;
+  const uint32_t gmask = (1u << g.gshift) - 1;
+  const uint32_t gpt = (g.ng + kGThreads - 1) / kGThreads;  // groups per thread in the scan
+  for (uint64_t t0 = r0; t0 < r1; t0 += kGTile) {
+    for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) tcnt[i] = 0;
+    uint32_t a[E], rk[E];
+#pragma unroll
+    for (uint32_t u = 0; u < E; ++u) {
+      const uint64_t r = t0 + u * kGThreads + threadIdx.x;
+      a[u] = r < r1 ? col[r] : kEmpty;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t u = 0; u < E; ++u)
+      if (a[u] < range) rk[u] = atomicAdd(&tcnt[a[u] >> g.gshift], 1u);
+    __syncthreads();
+    // exclusive scan of the tile's group counts (thread t: groups [t*gpt, t*gpt + gpt))
+    uint32_t run = 0;
+    for (uint32_t q = 0; q < gpt; ++q) run += threadIdx.x * gpt + q < g.ng ? tcnt[threadIdx.x * gpt + q] : 0u;
+    uint32_t x = run;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wib] = x;
+    __syncthreads();
+    uint32_t before = 0;
+    for (uint32_t w = 0; w < wib; ++w) before += wsum[w];
+    uint32_t pos = before + x - run;
+    for (uint32_t q = 0; q < gpt; ++q) {
+      const uint32_t gi = threadIdx.x * gpt + q;
+      if (gi < g.ng) {
+        toff[gi] = pos;
+        pos += tcnt[gi];
+      }
+    }
+    __syncthreads();
+    const uint32_t tot = toff[g.ng - 1] + tcnt[g.ng - 1];
+#pragma unroll
+    for (uint32_t u = 0; u < E; ++u)
+      if (a[u] < range) {
+        const uint32_t gi = a[u] >> g.gshift;
+        const uint32_t s = toff[gi] + rk[u];
+        stage[s] = ((a[u] & gmask) << kGChunkLog2) | (uint32_t)(t0 + u * kGThreads + threadIdx.x - r0);
+        sgrp[s] = (uint16_t)gi;
+      }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tot; i += blockDim.x) {
+      const uint32_t gi = sgrp[i];
+      ent[gbase[gi] + gcur[gi] + (i - toff[gi])] = stage[i];
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) gcur[i] += tcnt[i];
+  }
+}
+
+__host__ __device__ inline size_t gplace_smem(uint32_t gshift, uint32_t nch) {
+  return (size_t)(nch + 1) * 8 + ((size_t)4 << gshift);
+}
+
+__global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32_t t0, uint32_t range, GroupGeom g,
+                                                              const uint64_t* __restrict__ goffs,
+                                                              const uint32_t* __restrict__ ent, uint32_t id_base,
+                                                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ pool) {
+  extern __shared__ uint64_t co[];                                   // [nch + 1] chunk slot ranges
+  uint32_t* bc = reinterpret_cast<uint32_t*>(co + g.nch + 1);        // [2^gshift] counts -> cursors
+  __shared__ uint32_t wsum[kGPlaceThreads / 32];
+  const uint32_t gsz = 1u << g.gshift;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t ngroups = (uint64_t)W * g.ng;
+  for (uint64_t gid = blockIdx.x; gid < ngroups; gid += gridDim.x) {
+    const uint32_t j = (uint32_t)(gid / g.ng), gi = (uint32_t)(gid - (uint64_t)j * g.ng);
+    const uint32_t b0 = gi << g.gshift;
+    const uint32_t nbk = range - b0 < gsz ? range - b0 : gsz;
+    for (uint32_t c = threadIdx.x; c <= g.nch; c += blockDim.x) co[c] = goffs[gid * g.nch + c];
+    for (uint32_t b = threadIdx.x; b < gsz; b += blockDim.x) bc[b] = 0;
+    __syncthreads();
+    const uint64_t e0 = co[0], e1 = co[g.nch];
+    for (uint64_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) atomicAdd(&bc[ent[p] >> kGChunkLog2], 1u);
+    __syncthreads();
+    // the arrivals of these buckets (k_pool_sizes adds them) and their exclusive prefix
+    // (thread t owns buckets [t*per, t*per + per))
+    const uint32_t per = (gsz + kGPlaceThreads - 1) / kGPlaceThreads;
+    const uint32_t bl = threadIdx.x * per;
+    uint32_t run = 0;
+    for (uint32_t q = 0; q < per && bl + q < gsz; ++q) {
+      const uint32_t cnt = bc[bl + q];
+      if (bl + q < nbk) cursor[(uint64_t)(t0 + j) * range + b0 + bl + q] = cnt;
+      run += cnt;
+    }
+    uint32_t x = run;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wib] = x;
+    __syncthreads();
+    uint32_t before = 0;
+    for (uint32_t w = 0; w < wib; ++w) before += wsum[w];
+    uint32_t pos = before + x - run;
+    for (uint32_t q = 0; q < per && bl + q < gsz; ++q) {
+      const uint32_t cnt = bc[bl + q];
+      bc[bl + q] = pos;
+      pos += cnt;
+    }
+    __syncthreads();
+    // place the rows: warp-contiguous blocks of 32 slots, the chunk of the block's first slot
+    // by a warp-uniform binary search over the chunk ranges (a chunk's entries carry its
+    // rows' low 21 bits; a block straddles at most a few chunk ends)
+    for (uint64_t pb = e0 + (uint64_t)wib * 32; pb < e1; pb += blockDim.x) {
+      uint32_t lo = 0, hi = g.nch;  // the chunk c with co[c] <= pb < co[c + 1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (co[mid] <= pb) lo = mid;
+        else hi = mid;
+      }
+      const uint64_t p = pb + lane;
+      if (p < e1) {
+        uint32_t c = lo;
+        while (co[c + 1] <= p) ++c;
+        const uint32_t e = ent[p];
+        const uint32_t slot = atomicAdd(&bc[e >> kGChunkLog2], 1u);
+        pool[e0 + slot] = id_base + (c << kGChunkLog2) + (e & ((1u << kGChunkLog2) - 1));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Shared-memory build passes (tables whose bucket counters fit shared memory, e.g. webspam /
 // url: 2^15 buckets).  Global L2 atomics cap k_count / k_fill_new at ~1 atomic per L2 slice
 // per clock; here the W tables' (table, row) pairs — units j*n + r, table-major — are cut
@@ -941,6 +1159,13 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const uint32_t W = a.t1 > a.t0 ? a.t1 - a.t0 : 0;
   const bool sm_build = a.hbuf != nullptr && a.addrsT != nullptr && a.n && W && !a.shared;  // k_count_smem
   const bool tm = !sm_build && a.addrsT != nullptr && a.n && W && !a.shared;  // table-major passes (k_count_tm)
+  // grouped table-major passes: fresh builds whose group slot table fits the pool_cnt /
+  // keep_cnt scratch (W*ng*nch + 1 <= nb + 1), FLASH_BUILD_GROUPED=0 disables (tests)
+  const GroupGeom gg = group_geom(a.range, a.n);
+  const char* gp_env = getenv("FLASH_BUILD_GROUPED");
+  const bool grouped = tm && !a.goff_old && a.range <= (1u << 24) && (uint64_t)W * gg.ng * gg.nch <= (uint64_t)nb &&
+                       !(gp_env && gp_env[0] == '0');
+  uint32_t* pool = a.pool;  // the grouped passes leave the bucket-ordered pool in addrsT
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
   const uint32_t C = smem_build_ctas(W, a.n);
   if (sm_build) {
@@ -951,6 +1176,26 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     k_count_smem<<<C, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, W, C, a.cursor,
                                                                       a.hbuf, a.err);
     launches += 2;
+  } else if (grouped) {
+    k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
+                                                                   a.addrsT);
+    uint64_t* ghist = a.pool_cnt;  // scratch until k_pool_sizes
+    uint64_t* goffs = a.keep_cnt;
+    const uint64_t nslots = (uint64_t)W * gg.ng * gg.nch;
+    ensure_smem_attr((const void*)k_gscatter, gscatter_smem(gg.ng));
+    k_gcount<<<W * gg.nch, kGThreads, (size_t)gg.ng * 4, s>>>(a.addrsT, a.n, a.range, gg, ghist, a.err);
+    cudaMemsetAsync(ghist + nslots, 0, sizeof(uint64_t), s);
+    size_t tmp = a.scan_tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, ghist, goffs, (int64_t)nslots + 1, s);
+    k_gscatter<<<W * gg.nch, kGThreads, gscatter_smem(gg.ng), s>>>(a.addrsT, a.n, a.range, gg, goffs, a.pool);
+    const size_t psm = gplace_smem(gg.gshift, gg.nch);
+    ensure_smem_attr((const void*)k_gplace, psm);
+    const uint64_t pg = device_sms();  // one group per SM: the groups' pool ranges stay in L2
+    const uint64_t ngroups = (uint64_t)W * gg.ng;
+    k_gplace<<<(unsigned)(pg < ngroups ? pg : ngroups), kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, goffs, a.pool,
+                                                                                   a.id_base, a.cursor, a.addrsT);
+    pool = a.addrsT;
+    launches += 4;
   } else if (tm) {
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
@@ -1001,6 +1246,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     k_fill_smem<<<C, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, W, C, a.id_base,
                                                                  a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
     launches++;
+  } else if (grouped) {
+    // (placed by k_gplace)
   } else if (tm) {
     k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,
                                                       a.cursor, a.pool_off, a.pool);
@@ -1015,7 +1262,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   if (early) {  // the early-listed big buckets, concurrently with the kernels below
     cudaEventRecord(static_cast<cudaEvent_t>(a.side_fork), s);
     cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(a.side_fork), 0);
-    k_select_big<<<device_sms(), kBigThreads, 0, side>>>(a.range, a.R, a.keys, 0, a.pool_off, a.pool, a.goff_new,
+    k_select_big<<<device_sms(), kBigThreads, 0, side>>>(a.range, a.R, a.keys, 0, a.pool_off, pool, a.goff_new,
                                                         a.ids_new, a.early_list, early_count);
     side_used = true;
     launches += 1;
@@ -1026,16 +1273,16 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   uint32_t* reg_count = a.big_count + 2;
   const uint64_t small_warps = ((uint64_t)nb + kSmallChunk - 1) / kSmallChunk;  // 32 buckets per warp step
   const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < (uint64_t)device_sms() * 64 ? (small_warps + 7) / 8 : (uint64_t)device_sms() * 64);
-  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, early, a.pool_off, a.pool, a.goff_new,
+  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, early, a.pool_off, pool, a.goff_new,
                                              a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
                                              a.big_count);
-  k_select_mid<<<device_sms() * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, a.pool, a.goff_new,
+  k_select_mid<<<device_sms() * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, pool, a.goff_new,
                                        a.ids_new, a.big_list, a.big_count);
   launches += 1;
   k_select_warp<<<device_sms() * 3, kSelThreads, sel_smem, s>>>(a.range, a.R, a.keys, mid_list, mid_count, a.pool_off,
-                                                      a.pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
+                                                      pool, a.goff_new, a.ids_new, a.big_list, a.big_count);
   launches += 2;
-  k_select_big<<<device_sms(), kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, a.pool, a.goff_new,
+  k_select_big<<<device_sms(), kBigThreads, 0, s>>>(a.range, a.R, a.keys, force_big == 2, a.pool_off, pool, a.goff_new,
                                               a.ids_new, a.big_list, a.big_count);  // the late list
   launches += 1;
   if (side_used) {  // join everything queued on the side stream

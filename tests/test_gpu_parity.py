@@ -122,7 +122,10 @@ BUILD_CASES = [
 ]
 
 
-BUILD_SCHEDULES = {"rowmajor": ("0", "0"), "tablemajor": ("1", "1"), "smem": ("0", "1")}
+# (FLASH_BUILD_TM, FLASH_BUILD_SMEM, FLASH_BUILD_GROUPED): "tablemajor" takes the grouped
+# table-major passes on fresh builds, "tm_plain" the plain table-major scatter
+BUILD_SCHEDULES = {"rowmajor": ("0", "0", "1"), "tablemajor": ("1", "1", "1"), "smem": ("0", "1", "1"),
+                   "tm_plain": ("1", "1", "0")}
 
 
 @pytest.mark.parametrize("sched", list(BUILD_SCHEDULES))
@@ -133,6 +136,7 @@ def test_tables_bit_exact(monkeypatch, name, make, K, L, R, rng, sched):
     passes (a CTA per table slice: tables whose counters fit shared memory)."""
     monkeypatch.setenv("FLASH_BUILD_TM", BUILD_SCHEDULES[sched][0])
     monkeypatch.setenv("FLASH_BUILD_SMEM", BUILD_SCHEDULES[sched][1])
+    monkeypatch.setenv("FLASH_BUILD_GROUPED", BUILD_SCHEDULES[sched][2])
     rp, col = make()
     n = rp.size - 1
     seed = 0xB0 + R
@@ -193,6 +197,7 @@ def test_tables_bit_exact_on_the_exact_cta_path(monkeypatch, mode):
 def test_incremental_inserts_equal_one_build(monkeypatch, sched):
     monkeypatch.setenv("FLASH_BUILD_TM", BUILD_SCHEDULES[sched][0])
     monkeypatch.setenv("FLASH_BUILD_SMEM", BUILD_SCHEDULES[sched][1])
+    monkeypatch.setenv("FLASH_BUILD_GROUPED", BUILD_SCHEDULES[sched][2])
     rp, col = shape_slice("url", 5000)
     n = rp.size - 1
     K, L, R, rng, seed = 3, 20, 16, 1 << 9, 99
