@@ -757,34 +757,59 @@ def run_shape_graph(args, cfg, shape):
 
 
 def run_shape(args):
-    """N=1 line for the url / kdd12 shapes: one step = index all N rows (H1-H3, B1-B2) +
-    10K queries (H1-H3 of the query rows, Q1-Q3).  value = queries/s of the query phase;
-    the index time and hash nnz/s are reported beside it."""
+    """Line for the url / kdd12 shapes: one step = index all N rows (H1-H3, B1-B2) + 10K
+    sampled queries (H1-H3 of the query rows, Q1-Q3).  value = queries/s of the query phase;
+    the index time and hash nnz/s are reported beside it.  Under torchrun (N > 1) the rows
+    are sharded over the GPUs and indexed / queried through the multi-GPU handle (kdd12's
+    "tables sharded over 8 B200", BASELINE.json configs[3]); max over ranks."""
     import torch
 
     from paper_1709_01190_b200 import flash
 
     rank, world, local = dist_env()
-    assert world == 1, "--workload url/kdd12 runs on one GPU"
     cfg = SHAPE_CFG[args.workload]
     shape = synth.SHAPES[cfg.get("shape", args.workload)]
     if cfg.get("graph"):
+        assert world == 1, "the graph workloads other than the headline run on one GPU"
         return run_shape_graph(args, cfg, shape)
+    import torch.distributed as dist
+
+    from paper_1709_01190_b200 import dist as fdist
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # N > 1 (torchrun; or --dist-handle at N = 1): the multi-GPU handle — tables partitioned
+    # over the GPUs, rank g indexes its contiguous row shard (ids = global row numbers) and
+    # answers the sampled queries that fall in its shard, both collectively (flash.h)
+    use_dist = world > 1 or args.dist_handle
+    if use_dist and not dist.is_initialized():
+        for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(key, val)
+        dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
-    h_rp, h_col, nnz = gen_local(shape, [0, shape.N], 0)
-    log(f"generated {shape.N} rows nnz={nnz} in {time.time() - t0:.1f}s")
+    import ctypes
+
+    all_lens = np.empty(shape.N, dtype=np.int64)
+    synth._load().synth_row_lengths(ctypes.byref(synth._cparams(shape)), 0, shape.N, all_lens.ctypes.data)
+    bounds = fdist.shard_bounds(all_lens, world) if world > 1 else [0, shape.N]
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    n_local = r1 - r0
+    h_rp, h_col, nnz_local = gen_local(shape, bounds, rank)
+    nnz = int(all_lens.sum())
+    log(f"[rank {rank}] generated rows {r0}..{r1} nnz={nnz_local} in {time.time() - t0:.1f}s")
     rows = np.sort(np.random.default_rng(cfg["qseed"]).choice(shape.N, size=cfg["q"], replace=False))
-    q_rp, q_col = sample_query_csr(h_rp.numpy(), h_col.numpy(), rows)
+    mine = rows[(rows >= r0) & (rows < r1)]
+    q_rp, q_col = sample_query_csr(h_rp.numpy(), h_col.numpy(), mine - r0)
     d_rp, d_col = h_rp.to(dev), h_col.to(dev)
     dq_rp = torch.from_numpy(q_rp).to(dev)
     dq_col = torch.from_numpy(np.ascontiguousarray(q_col).view(np.int32)).to(dev)
-    excl = torch.from_numpy(rows.astype(np.uint32).view(np.int32)).to(dev)
+    excl = torch.from_numpy(mine.astype(np.uint32).view(np.int32)).to(dev)
     k = cfg["k"]
-    out_ids = torch.empty((cfg["q"], k), dtype=torch.int32, device=dev)
-    out_cnt = torch.empty((cfg["q"], k), dtype=torch.int32, device=dev)
-    idx = flash.FlashIndex(cfg["K"], cfg["L"], cfg["R"], cfg["range_"], cfg["seed"])
+    nq = int(mine.size)
+    out_ids = torch.empty((max(nq, 1), k), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty((max(nq, 1), k), dtype=torch.int32, device=dev)
+    idx = (fdist.create_dist_index(cfg["K"], cfg["L"], cfg["R"], cfg["range_"], cfg["seed"]) if use_dist
+           else flash.FlashIndex(cfg["K"], cfg["L"], cfg["R"], cfg["range_"], cfg["seed"]))
     stream = torch.cuda.current_stream()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
 
@@ -792,10 +817,10 @@ def run_shape(args):
         idx.clear()
         if ev:
             ev[0].record(stream)
-        flash.flash_insert(idx.h, d_rp, d_col, shape.N, 0)
+        flash.flash_insert(idx.h, d_rp, d_col, n_local, r0)
         if ev:
             ev[1].record(stream)
-        flash.flash_query_topk(idx.h, dq_rp, dq_col, cfg["q"], k, excl, out_ids, out_cnt)
+        flash.flash_query_topk(idx.h, dq_rp, dq_col, nq, k, excl, out_ids, out_cnt)
         if ev:
             ev[2].record(stream)
 
@@ -804,39 +829,53 @@ def run_shape(args):
     torch.cuda.synchronize()
     flash.flash_reset_counters(idx.h)
     flash.flash_set_profiling(idx.h, True)
+    if use_dist:
+        dist.barrier()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             step(evs[i])
         torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
     index_ms = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
     query_ms = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
     phase_ms, phase_calls = flash.flash_phase_ms(idx.h)
     launches = flash.flash_launch_count(idx.h)
     flash.flash_set_profiling(idx.h, False)
-    stats = shape_stats(idx, idx.hash_addrs(dq_rp, dq_col), np.diff(h_rp.numpy()), cfg["L"], cfg["R"],
-                        cfg["range_"])
-    # the hash phase covers the N indexed rows and the Q query rows; split by nnz
+    if world > 1:  # the slowest rank
+        t = torch.tensor([index_ms, query_ms] + list(phase_ms[:3]), dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        index_ms, query_ms = float(t[0]), float(t[1])
+        phase_ms = [float(x) for x in t[2:]] + [0.0]
+    stats = (shape_stats(idx, idx.hash_addrs(dq_rp, dq_col), np.diff(h_rp.numpy()), cfg["L"], cfg["R"],
+                         cfg["range_"]) if not use_dist else {"nnz_mean": float(all_lens.mean())})
+    # the hash phase covers the indexed rows and the query rows; split by nnz
     hash_ms_all = phase_ms[0] / args.steps
     q_nnz = int(q_rp[-1])
-    hash_ms_index = hash_ms_all * nnz / (nnz + q_nnz)
+    hash_ms_index = hash_ms_all * nnz_local / max(nnz_local + q_nnz, 1)
     hbm_peak, peak_kind = peaks()
     L_ = cfg["L"]
     hash_bytes = 4 * nnz + 8 * (shape.N + 1) + 4 * L_ * shape.N
     idx.close()
+    if use_dist:
+        dist.barrier()
+    if rank != 0:
+        return None
     return {
         "metric": METRIC,
         "value": cfg["q"] / (query_ms * 1e-3),
         "unit": "queries/s",
-        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": index_ms + query_ms,
         "index_time_s": index_ms * 1e-3,
         "query_time_s": query_ms * 1e-3,
         "hash_nnz_per_s": nnz / (hash_ms_index * 1e-3),
         "phase_ms_per_step": {"hash": hash_ms_all, "build": phase_ms[1] / args.steps,
                               "query": phase_ms[2] / args.steps},
-        "hash_roofline": {"kernel": "k_doph", "bound": "hbm", "achieved": hash_bytes / (hash_ms_index * 1e-3) / 1e9,
-                          "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
-                          "frac": hash_bytes / (hash_ms_index * 1e-3) / 1e9 / hbm_peak,
+        "hash_roofline": {"kernel": "k_doph", "bound": "hbm",
+                          "achieved": hash_bytes / (hash_ms_index * 1e-3) / 1e9,
+                          "peak": hbm_peak * world, "unit": "GB/s", "peak_kind": peak_kind,
+                          "frac": hash_bytes / (hash_ms_index * 1e-3) / 1e9 / (hbm_peak * world),
                           "algorithmic_bytes": hash_bytes,
                           "note": "densification makes this shape ALU-bound (DESIGN.md §6)"},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
@@ -844,7 +883,9 @@ def run_shape(args):
         "config": {"workload": f"{args.workload}-shaped: index all rows + {cfg['q']} sampled queries, top-{k}",
                    "N": shape.N, "D": shape.D, "nnz": nnz, "nnz_per_row": round(nnz / shape.N, 1),
                    "K": cfg["K"], "L": L_, "R": cfg["R"], "range": cfg["range_"], "k": k,
-                   "seed": cfg["seed"], "query_seed": cfg["qseed"], "parallelism": "1 GPU",
+                   "seed": cfg["seed"], "query_seed": cfg["qseed"],
+                   "parallelism": (f"rows x{world} (hash, queries); tables x{world} (build, gather); "
+                                   "flash_create_dist") if use_dist else "1 GPU",
                    "l2_policy": f"inputs larger than L2 (col_idx {4 * nnz / 1e9:.1f} GB vs 126 MB L2); no flush"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -949,13 +990,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the data statistics and R@k/S@k")
     ap.add_argument("--quality-queries", type=int, default=1000)
+    ap.add_argument("--dist-handle", action="store_true",
+                    help="url / kdd12 at N = 1 through the multi-GPU handle (flash_create_dist, NCCL world 1)")
     ap.add_argument("--workload", choices=["webspam", "url", "kdd12", "friendster", "url-graph", "webspam-sat"],
                     default="webspam",
                     help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines; "
                          "friendster / url-graph = full k-NN graphs of those shapes")
     args = ap.parse_args()
+    # the JSON line must be the only stdout line: NCCL's version banner goes to stdout unless
+    # its log level says otherwise
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     if args.workload != "webspam" and args.impl == "ours":
-        print(json.dumps(run_shape(args)), flush=True)
+        res = run_shape(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
         return
     if args.impl == "reference":
         res = run_reference(args)
