@@ -4,7 +4,8 @@ cf. the paper's Fig. 5/6 sweeps, P:401-425): K in {2..6}, L in {16, 32, 64, 128}
 (device-timed, median of --reps after a warm-up) with its hash / build / query split, and
 R@k / S@k of 1,000 sampled rows against exact binary cosine (computed once).
 
-    python tools/sweep.py [--out profiles/r01_sweep.json] [--reps 3] [--K 2,3,4,5,6] ...
+    python tools/sweep.py [--out profiles/r02_sweep.json] [--reps 3] [--K 2,3,4,5,6] ...
+    torchrun --nproc-per-node N tools/sweep.py   (multi-GPU handle; timings only)
 """
 import argparse
 import json
@@ -29,7 +30,7 @@ def ints(s):
 
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.json"))
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_sweep.json"))
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--K", type=ints, default=[2, 3, 4, 5, 6])
 ap.add_argument("--L", type=ints, default=[16, 32, 64, 128])
@@ -37,13 +38,67 @@ ap.add_argument("--R", type=ints, default=[32, 64, 128, 256])
 ap.add_argument("--queries", type=int, default=1000)
 args = ap.parse_args()
 
-torch.cuda.set_device(0)
+rank, world, local = bench.dist_env()
+torch.cuda.set_device(local)
 HBM_PEAK = bench.peaks()[0]
 shape = synth.SHAPES["webspam"]
+N, k = shape.N, 128
+if world > 1:
+    # torchrun: every point through the multi-GPU handle (rows sharded, tables partitioned);
+    # the graph is byte-identical at every GPU count, so the quality numbers of the 1-GPU sweep
+    # stand and only the timings are taken (max over ranks)
+    import ctypes
+
+    import torch.distributed as dist
+
+    from paper_1709_01190_b200 import dist as fdist
+
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lens = np.empty(N, dtype=np.int64)
+    synth._load().synth_row_lengths(ctypes.byref(synth._cparams(shape)), 0, N, lens.ctypes.data)
+    bounds = fdist.shard_bounds(lens, world)
+    h_rp, h_col, nnz = bench.gen_local(shape, bounds, rank)
+    d_rp, d_col = h_rp.cuda(), h_col.cuda()
+    n_local = bounds[rank + 1] - bounds[rank]
+    out_ids = torch.empty((max(n_local, 1), k), dtype=torch.int32, device="cuda")
+    out_cnt = torch.empty_like(out_ids)
+    stream = torch.cuda.current_stream()
+    rows = []
+    for K in args.K:
+        for L in args.L:
+            for R in args.R:
+                rec = {"K": K, "L": L, "R": R, "range": 1 << 15, "k": k, "n_gpus": world}
+                idx = fdist.create_dist_index(K, L, R, 1 << 15, bench.SEED)
+                times = []
+                for rep in range(args.reps + 1):
+                    idx.clear()
+                    dist.barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    flash.flash_knn_graph(idx.h, d_rp, d_col, n_local, k, out_ids, out_cnt)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    if rep > 0:
+                        times.append(float(t.item()))
+                idx.close()
+                g = statistics.median(times)
+                rec.update({"graph_ms": g, "queries_per_s": N / (g * 1e-3)})
+                rows.append(rec)
+                if rank == 0:
+                    print(json.dumps(rec), flush=True)
+    if rank == 0:
+        meta = {"workload": "webspam-shaped k-NN graph sweep (synth/ seed 2, N=350000), multi-GPU handle",
+                "n_gpus": world, "timing": f"device events, max over ranks, median of {args.reps} graphs"}
+        with open(args.out, "w") as f:
+            json.dump({"meta": meta, "points": rows}, f, indent=1)
+    dist.destroy_process_group()
+    sys.exit(0)
 t0 = time.time()
 h_rp, h_col, nnz = bench.gen_local(shape, [0, shape.N], 0)
 d_rp, d_col = h_rp.cuda(), h_col.cuda()
-N, k = shape.N, 128
 print(f"generated {N} rows, {nnz} nnz in {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
 t0 = time.time()
 crow, col, cnt, key = bench.dedup_csr(h_rp, d_col)
