@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(256) k_fill_tm(const uint32_t* __restrict__ ad
 // The bucket-contiguous pool then goes through the usual k_pool_sizes / scans / selects.
 constexpr uint32_t kGChunkLog2 = 21;  // rows per chunk: local row ids in 21 bits
 constexpr uint32_t kGMaxGroups = 2048;
-constexpr uint32_t kGMaxShift = 11;   // bucket within a group in 11 bits: range <= 2^24
 constexpr int kGThreads = 1024;
 constexpr int kGPlaceThreads = 1024;
 

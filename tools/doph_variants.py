@@ -17,8 +17,10 @@ import synth  # noqa: E402
 from paper_1709_01190_b200 import build as B  # noqa: E402
 from paper_1709_01190_b200 import flash  # noqa: E402
 
-VARIANTS = {"notable": ["FLASH_DOPH_NOTABLE"], "tp4": ["FLASH_DOPH_TPROBES=4"], "tp8": ["FLASH_DOPH_TPROBES=8"],
-            "tp16": ["FLASH_DOPH_TPROBES=16"], "tp32": ["FLASH_DOPH_TPROBES=32"]}
+# (variants measured this round, their code since removed: probe-chain tables for K*L in
+# (256, 768] — FLASH_DOPH_TPROBES / FLASH_DOPH_NOTABLE — and a cp.async.bulk column ring —
+# FLASH_DOPH_BULK[_STAGES])
+VARIANTS = {"base": []}
 CFG = {"url": (4, 128, 1 << 15, 0x5EED0003), "webspam": (4, 50, 1 << 15, 0x5EED0002),
        "kdd12": (4, 32, 1 << 20, 0x5EED0004)}
 
