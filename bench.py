@@ -382,10 +382,13 @@ def run_ours(args):
     if one_gpu:
         local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.dist_handle:
         if one_gpu:
             dist.init_process_group("gloo")
         else:
+            for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"),
+                             ("WORLD_SIZE", "1")):
+                os.environ.setdefault(key, val)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = synth.SHAPES["webspam"]
     t0 = time.time()
@@ -406,7 +409,7 @@ def run_ours(args):
     out_cnt = torch.empty((n_local, TOPK), dtype=torch.int32, device=dev)
     # N > 1: the library's multi-GPU handle (tables partitioned over the GPUs, candidates to
     # the query owners; north_star (d)), or the torch.distributed sharded-build schedule
-    use_dist_handle = world > 1 and args.mode == "exchange"
+    use_dist_handle = (world > 1 or args.dist_handle) and args.mode == "exchange"
     idx = (fdist.create_dist_index(K, L, R, RANGE, SEED) if use_dist_handle
            else flash.FlashIndex(K, L, R, RANGE, SEED))
     stream = torch.cuda.current_stream()

@@ -316,9 +316,15 @@ __global__ void k_dist_gather(const uint32_t* __restrict__ x1, uint32_t W, uint3
     if (lr >= bounds[g + 1] - bounds[g]) continue;
     const uint64_t q = bounds[g] + lr;
     const uint32_t sz = W ? sizes[q] : 0u;
-    if (lane == 0) pseg[g][(uint64_t)me * B + j] = sz;
+    const uint64_t rel = offs[q] - offs[bounds[g] + round * B];  // within this sender's region
+    if (lane == 0) {
+      pseg[g][(uint64_t)me * B + j] = sz;                        // segment size
+      pseg[g][nv + (uint64_t)me * B + j] = (uint32_t)rel;        // and start (< 2^32: <= 4 GiB)
+    }
     if (!sz) continue;
-    uint32_t* dst = pcand[g] + region + (offs[q] - offs[bounds[g] + round * B]);
+    uint32_t* dst = pcand[g] + region + rel;
+    // 32 buckets at a time: lane b holds bucket b's extent and its exclusive position; each
+    // 32 consecutive output positions find their bucket by a binary search over the lanes
     for (uint32_t j0 = 0; j0 < W; j0 += 32) {
       uint64_t st = 0;
       uint32_t bsz = 0;
@@ -330,35 +336,37 @@ __global__ void k_dist_gather(const uint32_t* __restrict__ x1, uint32_t W, uint3
           bsz = (uint32_t)(goff[i + 1] - st);
         }
       }
-      const uint32_t nb = W - j0 < 32 ? W - j0 : 32;
-      for (uint32_t b = 0; b < nb; ++b) {
-        const uint64_t bst = __shfl_sync(0xFFFFFFFFu, st, b);
-        const uint32_t bs = __shfl_sync(0xFFFFFFFFu, bsz, b);
-        for (uint32_t e = lane; e < bs; e += 32) dst[e] = __ldg(ids + bst + e);
-        dst += bs;
+      uint32_t incl = bsz;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
       }
+      const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const uint64_t base = st - (incl - bsz);  // ids + base + p: position p's id, p in this bucket
+      for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        // the bucket of p: the first lane b with incl_b > p (never an empty bucket)
+        uint32_t lo = 0;
+#pragma unroll
+        for (uint32_t step = 16; step; step >>= 1)
+          if (__shfl_sync(0xFFFFFFFFu, incl, lo + step - 1) <= p) lo += step;
+        const uint64_t bb = __shfl_sync(0xFFFFFFFFu, base, lo);
+        if (p < tot) dst[p] = __ldg(ids + bb + p);
+      }
+      dst += tot;
     }
   }
 }
 
-// Owner side: segment (s, j) of this round starts at region(s) + the exclusive scan of
-// segs[s][0..j) (one CTA per sender s).
-constexpr int kSegThreads = 256;
-__global__ void __launch_bounds__(kSegThreads) k_dist_seg_offsets(const uint32_t* __restrict__ segs, uint64_t B,
-                                                                  uint64_t nb, const uint64_t* __restrict__ region,
-                                                                  uint64_t* __restrict__ goffq) {
-  using Scan = cub::BlockScan<uint64_t, kSegThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  const uint64_t s = blockIdx.x;
-  uint64_t carry = region[s];
-  for (uint64_t j0 = 0; j0 < nb; j0 += kSegThreads) {
-    const uint64_t j = j0 + threadIdx.x;
-    const uint64_t v = j < nb ? segs[s * B + j] : 0;
-    uint64_t ex, tot;
-    Scan(tmp).ExclusiveSum(v, ex, tot);
-    if (j < nb) goffq[s * B + j] = carry + ex;
-    carry += tot;
-    __syncthreads();
+// Owner side: segment (s, j) of this round starts at region(s) + the start the sender stored
+// beside its size (segs[nv + s*B + j]).
+__global__ void k_dist_seg_offsets(const uint32_t* __restrict__ segs, uint64_t B, uint64_t nb, int world,
+                                   const uint64_t* __restrict__ region, uint64_t* __restrict__ goffq) {
+  const uint64_t nv = (uint64_t)world * B;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = v / B, j = v - s * B;
+    if (j < nb) goffq[v] = region[s] + segs[nv + v];
   }
 }
 
@@ -413,7 +421,7 @@ flash_status prepare(flash_index* h, uint64_t N, uint64_t maxn, cudaStream_t s) 
   d->batch = B;
   for (int p = 0; p < 2; ++p) {
     TRY(ensure(d->cand[p], cand_need));
-    TRY(ensure(d->segs[p], (uint64_t)d->world * B * 4));
+    TRY(ensure(d->segs[p], (uint64_t)d->world * B * 8));  // sizes, then starts
   }
   TRY(d->tr->map(d->x1.p, d->px1));
   for (int p = 0; p < 2; ++p) {
@@ -519,8 +527,9 @@ flash_status query_rounds(flash_index* h, uint32_t k, const uint32_t* exclude, b
     const uint64_t lo = r * B;
     if (lo >= mine) continue;
     const uint64_t nb = std::min(B, mine - lo);
-    k_dist_seg_offsets<<<d->world, kSegThreads, 0, s>>>(d->segs[p].as<uint32_t>(), B, nb, dregion,
-                                                 d->goffq.as<uint64_t>());
+    const uint64_t sv = (uint64_t)d->world * B;
+    k_dist_seg_offsets<<<(unsigned)std::min<uint64_t>((sv + 255) / 256, (uint64_t)device_sms() * 8), 256, 0, s>>>(
+        d->segs[p].as<uint32_t>(), B, nb, d->world, dregion, d->goffq.as<uint64_t>());
     h->launches++;
     QueryArgs a;
     memset(&a, 0, sizeof a);

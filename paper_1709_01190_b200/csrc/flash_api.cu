@@ -95,13 +95,14 @@ flash_status enter(const flash_index* hc, cudaStream_t s) {
 }
 
 Phase::Phase(const flash_index* hc, int p, cudaStream_t st) : h(const_cast<flash_index*>(hc)), phase(p), s(st) {
-  if (h->profiling) {
+  if (h->profiling && h->phase_depth[p]++ == 0) {  // the outermost scope of this phase times it
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
   }
 }
 Phase::~Phase() {
+  if (h->profiling) --h->phase_depth[phase];
   if (a) {
     cudaEventRecord(b, s);
     h->pending.push_back({phase, a, b});

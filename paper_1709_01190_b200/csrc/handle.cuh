@@ -90,6 +90,7 @@ struct flash_index {
 
   // profiling
   int profiling = 0;
+  int phase_depth[4] = {0, 0, 0, 0};  // open Phase scopes per phase (nested ones are not timed twice)
   std::vector<flash::api::PendingPhase> pending;
   double phase_ms[4] = {0, 0, 0, 0};
   uint64_t phase_calls[4] = {0, 0, 0, 0};
