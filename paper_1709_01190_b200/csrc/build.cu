@@ -804,10 +804,10 @@ __device__ __forceinline__ void sort_store_upto(const uint32_t* buf, uint32_t n,
 }
 
 // B2, buckets with 33..256 members (and R <= 256): one warp per bucket, members in
-// registers (8 per lane).  When m > R the bottom-R priority threshold is found by a
-// bitwise radix select over the 32-bit priorities (a warp reduction per bit, stopping as
-// soon as the keep-th smallest is pinned down, ~log2(m) bits); the kept ids are then
-// sorted ascending in registers.  Exact priority ties at the threshold (probability
+// registers (8 per lane).  When m > R the bottom-R priority threshold is found by a radix
+// select over the 32-bit priorities in 4-bit digits (a 16-bin shared-memory histogram per
+// digit, stopping as soon as the R-th smallest is pinned down, ~log16(m) + 1 digits); the
+// kept ids are then sorted ascending in registers.  Exact priority ties at the threshold (probability
 // ~m^2/2^33) go to the exact CTA path.
 __global__ void __launch_bounds__(256)
 k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restrict__ mid_list,
@@ -815,6 +815,7 @@ k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restri
              const uint32_t* __restrict__ pool, const uint64_t* __restrict__ goff,
              uint32_t* __restrict__ ids_out, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
   __shared__ uint32_t kept_s[8][kMidMax];
+  __shared__ uint32_t hist_s[8][16];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t* kbuf = kept_s[w];
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -834,31 +835,36 @@ k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restri
       uint32_t pr[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) pr[u] = lane + 32u * u < m ? prio_of(tb, id[u]) : 0xFFFFFFFFu;
-      // radix select: the R-th smallest priority lies in [prefix, prefix + 2^(bit+1))
-      uint32_t prefix = 0, need = R, tot = m, ubound = 0;
+      // radix select over 4-bit digits, most significant first: a per-warp shared-memory
+      // histogram of the candidates still matching `prefix`; the R-th smallest priority lies
+      // in digit d of the current position, everything in the digits below d is kept
+      uint32_t* hist = hist_s[w];
+      uint32_t prefix = 0, need = R, ubound = 0;
       bool done = false;
-      for (int bit = 31; bit >= 0 && !done; --bit) {
-        const uint32_t hi_mask = bit == 31 ? 0u : ~((2u << bit) - 1u);
-        uint32_t c = 0;
+      for (int sh = 28; sh >= 0 && !done; sh -= 4) {
+        const uint32_t hi_mask = sh == 28 ? 0u : ~((16u << sh) - 1u);
+        if (lane < 16) hist[lane] = 0;
+        __syncwarp();
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          c += (lane + 32u * u < m) && (pr[u] & hi_mask) == prefix && !((pr[u] >> bit) & 1u);
-        const uint32_t c0 = __reduce_add_sync(kFull, c);
-        if (need <= c0) {
-          tot = c0;
-          if (need == c0) {
-            ubound = prefix + (1u << bit);  // keep every priority < ubound
-            done = true;
-          }
-        } else {
-          need -= c0;
-          tot -= c0;
-          prefix |= 1u << bit;
-          if (need == tot) {
-            ubound = prefix + (1u << bit);  // may wrap to 0 at the very top: handled below
-            done = true;
-          }
+          if ((lane + 32u * u < m) && (pr[u] & hi_mask) == prefix) atomicAdd(&hist[(pr[u] >> sh) & 15u], 1u);
+        __syncwarp();
+        const uint32_t hc = lane < 16 ? hist[lane] : 0u;
+        uint32_t x = hc;
+#pragma unroll
+        for (uint32_t o = 1; o < 16; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
         }
+        const uint32_t d = __ffs(__ballot_sync(kFull, lane < 16 && x >= need)) - 1;
+        const uint32_t below = __shfl_sync(kFull, x - hc, d), cd = __shfl_sync(kFull, hc, d);
+        need -= below;  // still needed inside digit d (1 <= need <= cd)
+        prefix |= d << sh;
+        if (need == cd) {
+          ubound = prefix + (1u << sh);  // keep every priority < ubound (0: 2^32)
+          done = true;
+        }
+        __syncwarp();
       }
       if (!done) {  // priorities tie at the threshold: exact CTA path
         push_big(i, big_list, big_count);
