@@ -395,23 +395,31 @@ __global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32
       pos += cnt;
     }
     __syncthreads();
-    // place the rows: warp-contiguous blocks of 32 slots, the chunk of the block's first slot
-    // by a warp-uniform binary search over the chunk ranges (a chunk's entries carry its
-    // rows' low 21 bits; a block straddles at most a few chunk ends)
-    for (uint64_t pb = e0 + (uint64_t)wib * 32; pb < e1; pb += blockDim.x) {
-      uint32_t lo = 0, hi = g.nch;  // the chunk c with co[c] <= pb < co[c + 1]
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (co[mid] <= pb) lo = mid;
+    // place the rows: each warp walks a contiguous range of 32-slot blocks, finding the chunk
+    // of its first slot by a binary search over the chunk ranges and advancing it from there
+    // (a chunk's entries carry its rows' low 21 bits; a block straddles few chunk ends)
+    const uint64_t nblk = (e1 - e0 + 31) >> 5;
+    const uint64_t wb0 = nblk * wib / (kGPlaceThreads / 32), wb1 = nblk * (wib + 1) / (kGPlaceThreads / 32);
+    uint32_t c = 0;
+    if (wb0 < wb1) {
+      const uint64_t pb = e0 + (wb0 << 5);
+      uint32_t hi = g.nch;  // the chunk c with co[c] <= pb < co[c + 1]
+      while (hi - c > 1) {
+        const uint32_t mid = (c + hi) >> 1;
+        if (co[mid] <= pb) c = mid;
         else hi = mid;
       }
+    }
+    for (uint64_t blk = wb0; blk < wb1; ++blk) {
+      const uint64_t pb = e0 + (blk << 5);
+      while (co[c + 1] <= pb) ++c;
       const uint64_t p = pb + lane;
       if (p < e1) {
-        uint32_t c = lo;
-        while (co[c + 1] <= p) ++c;
+        uint32_t cl = c;
+        while (co[cl + 1] <= p) ++cl;
         const uint32_t e = ent[p];
         const uint32_t slot = atomicAdd(&bc[e >> kGChunkLog2], 1u);
-        pool[e0 + slot] = id_base + (c << kGChunkLog2) + (e & ((1u << kGChunkLog2) - 1));
+        pool[e0 + slot] = id_base + (cl << kGChunkLog2) + (e & ((1u << kGChunkLog2) - 1));
       }
     }
     __syncthreads();
