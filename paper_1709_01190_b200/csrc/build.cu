@@ -348,13 +348,20 @@ __host__ __device__ inline size_t gplace_smem(uint32_t gshift, uint32_t nch) {
   return (size_t)(nch + 1) * 8 + ((size_t)4 << gshift);
 }
 
+// kMode 0: count each group's buckets into `cursor` (the arrivals k_pool_sizes adds);
+// 1: place the rows, bucket b's slots starting at pool_off[b] (the scan of the counts, which
+// for a fresh build is exactly where the group ranges of k_gscatter put them); 2: both in
+// one pass (the bucket starts from a block scan of the counts; when nothing has to run
+// beside the placement)
+template <int kMode>
 __global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32_t t0, uint32_t range, GroupGeom g,
                                                               const uint64_t* __restrict__ goffs,
                                                               const uint32_t* __restrict__ ent, uint32_t id_base,
-                                                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ pool) {
+                                                              uint32_t* __restrict__ cursor,
+                                                              const uint64_t* __restrict__ pool_off,
+                                                              uint32_t* __restrict__ pool) {
   extern __shared__ uint64_t co[];                                   // [nch + 1] chunk slot ranges
-  uint32_t* bc = reinterpret_cast<uint32_t*>(co + g.nch + 1);        // [2^gshift] counts -> cursors
-  __shared__ uint32_t wsum[kGPlaceThreads / 32];
+  uint32_t* bc = reinterpret_cast<uint32_t*>(co + g.nch + 1);        // [2^gshift] counts / cursors
   const uint32_t gsz = 1u << g.gshift;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t ngroups = (uint64_t)W * g.ng;
@@ -362,37 +369,41 @@ __global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32
     const uint32_t j = (uint32_t)(gid / g.ng), gi = (uint32_t)(gid - (uint64_t)j * g.ng);
     const uint32_t b0 = gi << g.gshift;
     const uint32_t nbk = range - b0 < gsz ? range - b0 : gsz;
+    const uint64_t tb = (uint64_t)(t0 + j) * range + b0;
     for (uint32_t c = threadIdx.x; c <= g.nch; c += blockDim.x) co[c] = goffs[gid * g.nch + c];
-    for (uint32_t b = threadIdx.x; b < gsz; b += blockDim.x) bc[b] = 0;
     __syncthreads();
     const uint64_t e0 = co[0], e1 = co[g.nch];
-    for (uint64_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) atomicAdd(&bc[ent[p] >> kGChunkLog2], 1u);
-    __syncthreads();
-    // the arrivals of these buckets (k_pool_sizes adds them) and their exclusive prefix
-    // (thread t owns buckets [t*per, t*per + per))
-    const uint32_t per = (gsz + kGPlaceThreads - 1) / kGPlaceThreads;
-    const uint32_t bl = threadIdx.x * per;
-    uint32_t run = 0;
-    for (uint32_t q = 0; q < per && bl + q < gsz; ++q) {
-      const uint32_t cnt = bc[bl + q];
-      if (bl + q < nbk) cursor[(uint64_t)(t0 + j) * range + b0 + bl + q] = cnt;
-      run += cnt;
-    }
-    uint32_t x = run;
+    if (kMode != 1) {
+      for (uint32_t b = threadIdx.x; b < gsz; b += blockDim.x) bc[b] = 0;
+      __syncthreads();
+      for (uint64_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) atomicAdd(&bc[ent[p] >> kGChunkLog2], 1u);
+      __syncthreads();
+      for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) cursor[tb + b] = bc[b];
+      __syncthreads();
+      if (kMode == 0) continue;
+      // exclusive scan of the group's counts (thread t owns buckets [t*per, t*per + per))
+      __shared__ uint32_t wsum[kGPlaceThreads / 32];
+      const uint32_t per = (gsz + kGPlaceThreads - 1) / kGPlaceThreads;
+      const uint32_t bl = threadIdx.x * per;
+      uint32_t run = 0;
+      for (uint32_t q = 0; q < per && bl + q < gsz; ++q) run += bc[bl + q];
+      uint32_t x = run;
 #pragma unroll
-    for (uint32_t o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[wib] = x;
-    __syncthreads();
-    uint32_t before = 0;
-    for (uint32_t w = 0; w < wib; ++w) before += wsum[w];
-    uint32_t pos = before + x - run;
-    for (uint32_t q = 0; q < per && bl + q < gsz; ++q) {
-      const uint32_t cnt = bc[bl + q];
-      bc[bl + q] = pos;
-      pos += cnt;
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[wib] = x;
+      __syncthreads();
+      uint32_t pos = x - run;
+      for (uint32_t w = 0; w < wib; ++w) pos += wsum[w];
+      for (uint32_t q = 0; q < per && bl + q < gsz; ++q) {
+        const uint32_t cnt = bc[bl + q];
+        bc[bl + q] = pos;
+        pos += cnt;
+      }
+    } else {
+      for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) bc[b] = (uint32_t)(pool_off[tb + b] - e0);
     }
     __syncthreads();
     // place the rows: each warp walks a contiguous range of 32-slot blocks, finding the chunk
@@ -1144,6 +1155,11 @@ uint32_t smem_build_ctas(uint32_t W, uint64_t n) {
 
 bool smem_build_fits(uint32_t range) { return range <= kSmemBuildMaxRange; }
 
+uint64_t build_group_slots(uint32_t range, uint64_t n, uint32_t W) {
+  const GroupGeom g = group_geom(range, n);
+  return (uint64_t)W * g.ng * g.nch + 1;
+}
+
 size_t build_scan_tmp_bytes(uint64_t nb) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
@@ -1176,9 +1192,11 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   // keep_cnt scratch (W*ng*nch + 1 <= nb + 1), FLASH_BUILD_GROUPED=0 disables (tests)
   const GroupGeom gg = group_geom(a.range, a.n);
   const char* gp_env = getenv("FLASH_BUILD_GROUPED");
-  const bool grouped = tm && !a.goff_old && a.range <= (1u << 24) && (uint64_t)W * gg.ng * gg.nch <= (uint64_t)nb &&
+  const bool grouped = tm && !a.goff_old && a.gslots && a.range <= (1u << 24) &&
+                       (uint64_t)W * gg.ng * gg.nch <= (uint64_t)nb &&  // (the scan's temp storage is sized for nb)
                        !(gp_env && gp_env[0] == '0');
   uint32_t* pool = a.pool;  // the grouped passes leave the bucket-ordered pool in addrsT
+  unsigned gplace_grid = 1;
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
   const uint32_t C = smem_build_ctas(W, a.n);
   if (sm_build) {
@@ -1192,8 +1210,8 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   } else if (grouped) {
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
-    uint64_t* ghist = a.pool_cnt;  // scratch until k_pool_sizes
-    uint64_t* goffs = a.keep_cnt;
+    uint64_t* ghist = a.gslots;  // group histograms, scanned in place into slot offsets
+    uint64_t* goffs = a.gslots;
     const uint64_t nslots = (uint64_t)W * gg.ng * gg.nch;
     ensure_smem_attr((const void*)k_gscatter, gscatter_smem(gg.ng));
     k_gcount<<<W * gg.nch, kGThreads, (size_t)gg.ng * 4, s>>>(a.addrsT, a.n, a.range, gg, ghist, a.err);
@@ -1202,13 +1220,20 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, ghist, goffs, (int64_t)nslots + 1, s);
     k_gscatter<<<W * gg.nch, kGThreads, gscatter_smem(gg.ng), s>>>(a.addrsT, a.n, a.range, gg, goffs, a.pool);
     const size_t psm = gplace_smem(gg.gshift, gg.nch);
-    ensure_smem_attr((const void*)k_gplace, psm);
-    const uint64_t pg = device_sms();  // one group per SM: the groups' pool ranges stay in L2
     const uint64_t ngroups = (uint64_t)W * gg.ng;
-    k_gplace<<<(unsigned)(pg < ngroups ? pg : ngroups), kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, goffs, a.pool,
-                                                                                   a.id_base, a.cursor, a.addrsT);
+    gplace_grid = (unsigned)((uint64_t)device_sms() < ngroups ? device_sms() : ngroups);  // one group per SM
+    if (a.after_scan) {  // count now, place after the scans, so the callback's work overlaps it
+      ensure_smem_attr((const void*)k_gplace<0>, psm);
+      ensure_smem_attr((const void*)k_gplace<1>, psm);
+      k_gplace<0><<<gplace_grid, kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, goffs, a.pool, a.id_base, a.cursor,
+                                                           nullptr, nullptr);
+    } else {  // count and place in one pass
+      ensure_smem_attr((const void*)k_gplace<2>, psm);
+      k_gplace<2><<<gplace_grid, kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, goffs, a.pool, a.id_base, a.cursor,
+                                                           nullptr, a.addrsT);
+    }
     pool = a.addrsT;
-    launches += 4;
+    launches += 3;
   } else if (tm) {
     k_transpose_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.addrs, a.n, a.astride, a.t0 - a.acol0, W,
                                                                    a.addrsT);
@@ -1260,7 +1285,12 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                                                  a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
     launches++;
   } else if (grouped) {
-    // (placed by k_gplace)
+    if (a.after_scan) {  // (after the scans: the callback's work above overlaps the placement)
+      const size_t psm = gplace_smem(gg.gshift, gg.nch);
+      k_gplace<1><<<gplace_grid, kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, a.gslots, a.pool, a.id_base, nullptr,
+                                                           a.pool_off, a.addrsT);
+      launches++;
+    }
   } else if (tm) {
     k_fill_tm<<<(unsigned)(chunks * W), 256, 0, s>>>(a.addrsT, a.n, a.t0, a.range, (uint32_t)chunks, a.id_base,
                                                       a.cursor, a.pool_off, a.pool);

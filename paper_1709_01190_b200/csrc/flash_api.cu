@@ -184,7 +184,7 @@ void free_handle(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->raddr, &h->qraddr, &h->hbuf, &h->h_rp, &h->h_col,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->raddr, &h->qraddr, &h->hbuf, &h->gslots, &h->h_rp, &h->h_col,
                     &h->h_ids, &h->h_cnt, &h->zero})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
@@ -247,6 +247,8 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   if ((tm || smb) && t1 > t0) TRY(ensure(h->addrsT, sizeof(uint32_t) * n * (t1 - t0)));
   if (smb)
     TRY(ensure(h->hbuf, sizeof(uint32_t) * ((size_t)(t1 - t0) + smem_build_ctas(t1 - t0, n)) * h->range));
+  const bool grouped = tm && !h->have_tables && t1 > t0 && n > 0;  // (launch_build may still decline)
+  if (grouped) TRY(ensure(h->gslots, sizeof(uint64_t) * build_group_slots(h->range, n, t1 - t0)));
 
   Phase ph(h, 1, s);
   BuildArgs a;
@@ -256,6 +258,7 @@ flash_status do_insert_addrs(flash_index* h, const uint32_t* addrs, uint64_t n, 
   a.acol0 = cols ? t0 : 0;
   a.addrsT = ((tm || smb) && t1 > t0) ? h->addrsT.as<uint32_t>() : nullptr;
   a.hbuf = smb ? h->hbuf.as<uint32_t>() : nullptr;
+  a.gslots = grouped ? h->gslots.as<uint64_t>() : nullptr;
   a.shared = h->shared;
   a.n = n;
   a.id_base = id_base;

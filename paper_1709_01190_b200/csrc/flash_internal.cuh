@@ -142,6 +142,8 @@ struct BuildArgs {
   void* side_stream;          // with early_list: k_select_big runs these on this stream,
   void* side_fork;            //   concurrently with the other select kernels (events fork /
   void* side_join;            //   join it with the caller's stream)
+  uint64_t* gslots;           // [build_group_slots(range, n, t1-t0)] scratch of the grouped
+                              // table-major passes (fresh table-major builds), or null
   unsigned long long* err;    // device error counter
   void* scan_tmp;
   size_t scan_tmp_bytes;
@@ -154,6 +156,7 @@ struct BuildArgs {
 size_t build_scan_tmp_bytes(uint64_t nb);
 uint32_t smem_build_ctas(uint32_t W, uint64_t n);  // CTAs of the shared-memory passes (hbuf: (C + W) slots)
 bool smem_build_fits(uint32_t range);
+uint64_t build_group_slots(uint32_t range, uint64_t n, uint32_t W);
 int launch_build(const BuildArgs& a, cudaStream_t s);
 
 struct QueryArgs {
