@@ -244,7 +244,11 @@ constexpr uint32_t kSparseMaxB = 256;
 
 __host__ __device__ __forceinline__ uint32_t sparse_stride(uint32_t B) { return (B + 127) & ~127u; }
 __host__ __device__ __forceinline__ uint32_t sparse_warp_words(uint32_t B) {
-  return 2 * B + (B + 3) / 4;  // v[B], code[B], u8 NE list
+  return 2 * B + (B + 3) / 4 + 8;  // v[B], code[B], u8 NE list, NE bitmap (<= 256 bins)
+}
+// the CTA tables: first[B][Bs] and jt[Bs] (each bin's T-th probe), in 32-bit words
+__host__ __device__ __forceinline__ uint32_t sparse_table_words(uint32_t B) {
+  return (B + 1) * sparse_stride(B) / 4;
 }
 
 template <bool kCodes, bool kAddrs>
@@ -258,15 +262,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const uint32_t Bs = sparse_stride(B);               // table row stride (bytes), 128-multiple
   uint8_t* first = reinterpret_cast<uint8_t*>(smem);  // [B][Bs], 255 = never
-  uint32_t* v = smem + B * Bs / 4 + (size_t)warp * sparse_warp_words(B);
+  uint8_t* jt = first + B * Bs;                        // [Bs] bin i's T-th (last) probe
+  uint32_t* v = smem + sparse_table_words(B) + (size_t)warp * sparse_warp_words(B);
   uint32_t* code = v + B;
   uint8_t* nel = reinterpret_cast<uint8_t*>(code + B);  // non-empty bins, ascending
+  uint32_t* nebits = code + B + (B + 3) / 4;            // [8] non-empty bins as a bitmap
 
   for (uint32_t x = threadIdx.x; x < B * Bs / 4; x += blockDim.x) smem[x] = 0xFFFFFFFFu;
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x)
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
     for (uint32_t a = kProbes; a >= 1; --a)  // descending: the smallest position wins
       first[__umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B) * Bs + i] = (uint8_t)a;
+    jt[i] = (uint8_t)__umulhi(fmix32(keys.s_dens ^ ((i << 8) | kProbes)), B);
+  }
   __syncthreads();
 
   const uint64_t nw = (uint64_t)gridDim.x * wpb;
@@ -291,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
       const bool full = i < B && v[i] != kEmpty;
       const uint32_t mf = __ballot_sync(0xFFFFFFFFu, full);
       if (full) nel[nne + __popc(mf & lanemask_lt_d())] = (uint8_t)i;
+      if (lane == 0) nebits[i0 >> 5] = mf;
       nne += __popc(mf);
     }
     __syncwarp();
@@ -314,16 +323,16 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
           uint32_t dj;
           if ((r16 >> 8) != 255) {
             dj = nel[r16 & 0xFF];
-          } else {  // every probe missed: first non-empty bin after the T-th probe
-            const uint32_t j0 = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | kProbes)), B);
-            dj = nel[0];
-            for (uint32_t kk = 0; kk < nne; ++kk) {
-              const uint32_t j = nel[kk];
-              if (j > j0) {
-                dj = j;
-                break;
-              }
+          } else {  // every probe missed: the first non-empty bin after the T-th probe, circularly
+            const uint32_t nwb = (B + 31) >> 5;
+            uint32_t jj = jt[i] + 1u;
+            if (jj == B) jj = 0;
+            uint32_t wi = jj >> 5, word = nebits[wi] & (0xFFFFFFFFu << (jj & 31));
+            while (!word) {  // (the row is non-empty: a bit is found within nwb + 1 words)
+              wi = wi + 1 == nwb ? 0u : wi + 1;
+              word = nebits[wi];
             }
+            dj = wi * 32 + __ffs(word) - 1;
           }
           x = v[dj];
         }
@@ -347,7 +356,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   int launched = 0;
   int64_t skip_le = -1;
   if (B <= kSparseMaxB) {  // rows with <= kSparseNnz nonzeros: the table-driven kernel
-    const size_t smem = ((size_t)B * sparse_stride(B) / 4 + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
+    const size_t smem = ((size_t)sparse_table_words(B) + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
     ensure_smem_attr((const void*)k_doph_sparse<C, A>, 100 * 1024, true);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_sparse<C, A>, kThreads, smem);
