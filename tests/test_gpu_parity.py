@@ -346,6 +346,24 @@ def test_knn_graph_bit_exact(monkeypatch, name, make, K, L, R, rng, k, kern):
         assert np.array_equal(out_c.numpy().view(np.uint32), o_cnt)
 
 
+@pytest.mark.parametrize("grouped", ["1", "0"])
+def test_table_major_build_over_several_row_chunks(monkeypatch, grouped):
+    """2.3 M rows into 2^20-bucket tables: the grouped table-major passes span two 2^21-row
+    chunks and 512-bucket groups (the kdd12 geometry at a small L), the plain scatter as the
+    control; tables bit-exact against the oracle."""
+    monkeypatch.setenv("FLASH_BUILD_TM", "1")
+    monkeypatch.setenv("FLASH_BUILD_GROUPED", grouped)
+    rp, col = shape_slice("kdd12", 2_300_000)
+    n = rp.size - 1
+    K, L, R, rng, seed = 4, 3, 8, 1 << 20, 0x5EED0004
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    T = oracle.build(L, R, rng, seed, addrs, np.arange(n, dtype=np.uint32) + 7)
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert(d_rp, d_col, 7)
+        _check_tables(idx, T)
+
+
 def test_knn_graph_ids_beyond_the_bitmap_kernel():
     """800,000 rows: the ids no longer fit the bitmap kernel's shared-memory bitmap, so every
     query goes to the sort kernels — also in flash_knn_graph, whose size-class plan runs
