@@ -1000,18 +1000,26 @@ def main():
                     help="webspam = the headline graph (default); url / kdd12 = secondary N=1 lines; "
                          "friendster / url-graph = full k-NN graphs of those shapes")
     args = ap.parse_args()
-    # the JSON line must be the only stdout line: NCCL's version banner goes to stdout unless
-    # its log level says otherwise
+    # the JSON line must be the only stdout line: NCCL prints its version banner to stdout
+    # whatever NCCL_DEBUG says, so fd 1 is pointed at stderr for the run and the line is
+    # written to the saved original
     os.environ.setdefault("NCCL_DEBUG", "WARN")
+    sys.stdout.flush()
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+
+    def emit(res):
+        os.write(out_fd, (json.dumps(res) + "\n").encode())
+
     if args.workload != "webspam" and args.impl == "ours":
         res = run_shape(args)
         if res is not None:
-            print(json.dumps(res), flush=True)
+            emit(res)
         return
     if args.impl == "reference":
         res = run_reference(args)
         if res is not None:
-            print(json.dumps(res), flush=True)
+            emit(res)
         return
     res = run_ours(args)
     rank, world, _ = dist_env()
@@ -1019,7 +1027,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cb, _ = cpu_baseline(args.ref_sample, steps=1)
             res["cpu_baseline"] = cb
-        print(json.dumps(res), flush=True)
+        emit(res)
     if world > 1:
         import torch.distributed as dist
 
