@@ -38,6 +38,8 @@ namespace {
 
 constexpr int kMarkThreads = 256;
 constexpr uint32_t kMarkWarps = kMarkThreads / 32;
+constexpr uint32_t kConsWarps = kMarkWarps - 1;  // consumer warps (Q2-Q3); the last warp is the producer (Q1)
+constexpr uint32_t kConsThreads = kConsWarps * 32;
 constexpr uint32_t kRepLog2 = 8;
 constexpr uint32_t kRepSlots = 1u << kRepLog2;  // open-addressing table of repeated ids
 constexpr uint32_t kRepMax = 112;               // distinct repeated ids ranked here (more: fallback)
@@ -48,10 +50,25 @@ constexpr uint32_t kScanWpt = 8;                // bitmap words per thread per s
 constexpr size_t kMarkMaxBitmapBytes = 96 * 1024;  // >= 2 CTAs per SM (and u16 word indices)
 constexpr uint32_t kMarkMinCandidates = 768;     // fewer: the size-class sort kernels
 
+#ifdef FLASH_QPROF  // per-phase cycle counters of thread 0 (diagnostic builds only: build.py --qprof)
+__device__ unsigned long long g_mprof[8];
+#define MMARK(i)                                                                 \
+  do {                                                                           \
+    const long long now_ = clock64();                                            \
+    if (tid == 0) atomicAdd(&g_mprof[i], (unsigned long long)(now_ - mp_last)); \
+    mp_last = now_;                                                              \
+  } while (0)
+#else
+#define MMARK(i) \
+  do {           \
+  } while (0)
+#endif
+
 struct MarkHdr {
-  uint32_t nsingle, nrep, overflow, excl, nhi;
-  uint32_t wsum[kMarkWarps];
-  uint32_t rsum[2][kMarkWarps];
+  uint32_t nrep, overflow;
+  uint32_t M[2], excl[2];  // per query buffer (Q1 output): candidates, excluded id
+  uint64_t q[2];           // and the query's index
+  uint32_t rsum[2][kConsWarps];
 };
 
 __host__ __device__ inline uint32_t mark_words(uint32_t max_id) {  // bitmap words, multiple of 128
@@ -64,12 +81,12 @@ __host__ __device__ inline uint32_t mark_stage(uint64_t mmax) {
 }
 
 __host__ __device__ inline size_t mark_smem_bytes(uint32_t nwords, uint32_t L, uint64_t mmax) {
-  size_t b = (size_t)nwords * 4                  // id bitmap
-             + (size_t)kRepSlots * 10            // repeated ids, their extra occurrences, slot list
-             + (size_t)kRepMax * 8               // ranked repeated ids (u64 keys)
-             + (size_t)((L + 1) & ~1u) * 8       // base of each non-empty bucket (16-B multiple)
-             + (size_t)mark_bmap_words(mmax) * 8  // bucket-start bitmap over positions + prefix
-             + (size_t)mark_stage(mmax) * 2;     // staged bitmap word indices (reset)
+  size_t b = (size_t)nwords * 4                      // id bitmap
+             + (size_t)kRepSlots * 10                // repeated ids, their extra occurrences, slot list
+             + (size_t)kRepMax * 8                   // ranked repeated ids (u64 keys)
+             + (size_t)2 * ((L + 1) & ~1u) * 8       // base of each non-empty bucket (x2 queries)
+             + (size_t)2 * mark_bmap_words(mmax) * 8  // bucket-start bitmap over positions (x2)
+             + (size_t)mark_stage(mmax) * 2;         // staged bitmap word indices (reset)
   return (b + 15) & ~(size_t)15;
 }
 
@@ -97,52 +114,56 @@ __device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], uint32_t j) {
   return (j & 4) ? cd : ab;
 }
 
-__global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const uint32_t* __restrict__ qlist,
-                                                            const uint32_t* __restrict__ qcount, uint32_t nwords,
-                                                            uint32_t rep_max, uint32_t* __restrict__ fb_list,
-                                                            uint32_t* __restrict__ fb_count) {
+// named barriers (id 0 is __syncthreads): 1 = the consumer warps, 2 + b = buffer b full
+// (the producer arrives, the consumers wait), 4 + b = buffer b empty (the consumers arrive,
+// the producer waits)
+// (immediate ids, so that ptxas reserves only the barriers used)
+template <uint32_t kId, uint32_t kN>
+__device__ __forceinline__ void bar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+template <uint32_t kId, uint32_t kN>
+__device__ __forceinline__ void bar_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+constexpr uint32_t kBarCons = 1, kBarFull = 2, kBarEmpty = 4;
+__device__ __forceinline__ void bar_full_sync(uint32_t b) {
+  if (b) bar_sync<kBarFull + 1, kMarkThreads>(); else bar_sync<kBarFull, kMarkThreads>();
+}
+__device__ __forceinline__ void bar_full_arrive(uint32_t b) {
+  if (b) bar_arrive<kBarFull + 1, kMarkThreads>(); else bar_arrive<kBarFull, kMarkThreads>();
+}
+__device__ __forceinline__ void bar_empty_sync(uint32_t b) {
+  if (b) bar_sync<kBarEmpty + 1, kMarkThreads>(); else bar_sync<kBarEmpty, kMarkThreads>();
+}
+__device__ __forceinline__ void bar_empty_arrive(uint32_t b) {
+  if (b) bar_arrive<kBarEmpty + 1, kMarkThreads>(); else bar_arrive<kBarEmpty, kMarkThreads>();
+}
+__device__ __forceinline__ void bar_cons() { bar_sync<kBarCons, kConsThreads>(); }
+
+__global__ void __launch_bounds__(kMarkThreads, 4)
+    k_query_mark(QueryArgs a, const uint32_t* __restrict__ qlist, const uint32_t* __restrict__ qcount,
+                 uint32_t nwords, uint32_t rep_max, uint32_t* __restrict__ fb_list, uint32_t* __restrict__ fb_count) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ MarkHdr hdr;
   const uint32_t L = a.L, k = a.k;
+  const uint32_t Lp = (L + 1) & ~1u;
   const uint32_t nbw = mark_bmap_words(a.mmax);
   const uint32_t stage_cap = mark_stage(a.mmax);
   uint32_t* bits = reinterpret_cast<uint32_t*>(sm);                     // [nwords]
   uint32_t* rkey = bits + nwords;                                       // [kRepSlots]
   uint32_t* rcnt = rkey + kRepSlots;                                    // [kRepSlots]
   uint64_t* rlist = reinterpret_cast<uint64_t*>(rcnt + kRepSlots);      // [kRepMax]
-  const uint32_t** nbase = reinterpret_cast<const uint32_t**>(rlist + kRepMax);  // [L]
-  // word w of the bucket-start bitmap over positions: .x = the starts in [32w, 32w + 32),
+  const uint32_t** nbase = reinterpret_cast<const uint32_t**>(rlist + kRepMax);  // [2][Lp]
+  // word w of a bucket-start bitmap over positions: .x = the starts in [32w, 32w + 32),
   // .y = the number of starts below 32w
-  uint2* bmap = reinterpret_cast<uint2*>(nbase + ((L + 1) & ~1u));     // [nbw]
-  uint16_t* stage = reinterpret_cast<uint16_t*>(bmap + nbw);            // [stage_cap], 16-B aligned
+  uint2* bmap = reinterpret_cast<uint2*>(nbase + 2 * Lp);              // [2][nbw]
+  uint16_t* stage = reinterpret_cast<uint16_t*>(bmap + 2 * nbw);        // [stage_cap], 16-B aligned
   uint16_t* rslot = stage + stage_cap;                                  // [kRepSlots] slots in use
   const uint32_t tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  const uint32_t nwq = (L + 31) >> 5;  // warps holding a bucket
   const uint32_t* __restrict__ gids = a.ids;
   const uint32_t lim = a.shared ? a.shared : a.range;
   const uint32_t nbits = nwords * 32u;
-  const uint32_t s_bits = (uint32_t)__cvta_generic_to_shared(bits);
-  const uint32_t s_rkey = (uint32_t)__cvta_generic_to_shared(rkey);
-  const uint32_t s_rcnt = (uint32_t)__cvta_generic_to_shared(rcnt);
-  uint32_t lanele;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(lanele));
-
-  // thread tid < L: table tid's bucket of query q (issued a phase before it is consumed)
-  auto bucket_addr = [&](uint64_t q) -> uint32_t {
-    return a.direct ? (uint32_t)q : a.addrs[q * L + tid];
-  };
-  auto bucket_extent = [&](uint32_t ad, uint64_t& st, uint32_t& sz) {
-    st = 0;
-    sz = 0;
-    if (ad < lim) {
-      const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)tid * a.range + ad;
-      st = a.goff[i];
-      sz = a.seg_len ? a.seg_len[i] : (uint32_t)(a.goff[i + 1] - st);
-    }
-  };
-  auto exclude_of = [&](uint64_t q) -> uint32_t {
-    return a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
-  };
   const uint64_t nq = qlist ? (uint64_t)*qcount : a.nq;  // this launch's queries
   auto query_at = [&](uint64_t it) -> uint64_t { return qlist ? (uint64_t)qlist[it] : it; };
 
@@ -153,113 +174,185 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const 
       rkey[j] = kEmpty;
       rcnt[j] = 0;
     }
-    for (uint32_t j = tid; j < nbw; j += kMarkThreads) bmap[j] = make_uint2(0, 0);
+    for (uint32_t j = tid; j < 2 * nbw; j += kMarkThreads) bmap[j] = make_uint2(0, 0);
     for (uint32_t j = tid; j < stage_cap; j += kMarkThreads) stage[j] = 0;
-    if (tid == 0) {
-      hdr.nrep = hdr.overflow = 0;
-      hdr.excl = blockIdx.x < nq ? exclude_of(query_at(blockIdx.x)) : kEmpty;
-    }
-  }
-  uint32_t cur_ad = kEmpty, cur_sz = 0;
-  uint64_t cur_st = 0;
-  if (tid < L && blockIdx.x < nq) {
-    cur_ad = bucket_addr(query_at(blockIdx.x));
-    bucket_extent(cur_ad, cur_st, cur_sz);
+    if (tid == 0) hdr.nrep = hdr.overflow = 0;
   }
   __syncthreads();
 
-  for (uint64_t it = blockIdx.x; it < nq; it += gridDim.x) {
-    const uint64_t q = query_at(it);
-    const bool more = it + gridDim.x < nq;
-    const uint64_t qn = more ? query_at(it + gridDim.x) : 0;  // this CTA's next query (prefetched)
-
-    // ---- Q1: scan of (size, non-empty) over the L buckets (sizes clamped above L*R: the
-    //      sum then stays below 2^24; ranks < 2^8) ----
-    const uint32_t sz = cur_sz <= a.mmax ? cur_sz : (uint32_t)a.mmax + 1;
-    const uint32_t v = sz | ((uint32_t)(sz > 0) << 24);
-    uint32_t x = v, nx_ad = kEmpty;
-    if (wib < nwq) {
-      if (cur_ad != kEmpty && cur_ad >= lim) atomicAdd(a.err, 1ull);  // an address outside the table
+  if (wib == kConsWarps) {
+    // ==== the producer warp: Q1 of this CTA's queries, into two alternating buffers.  Lane
+    //      `lane` holds tables t = 4 lane + u (u < 4).  Loads run ahead: a query's extents
+    //      one query early, its addresses two, its index three. ====
+    uint32_t nad[4];               // addresses of query j + 1
+    uint64_t est[4], nst[4];       // extents: of query j (est/esz), of query j + 1 (nst/nsz)
+    uint32_t esz[4], nsz[4];
+    uint64_t eq = 0, nq1 = 0, q2 = 0;  // query indices j, j + 1, j + 2
+    uint32_t eex = kEmpty, nex = kEmpty;
+    const uint64_t g = gridDim.x;
+    auto addrs_of = [&](uint64_t q) {
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t t = 4 * lane + u;
+        nad[u] = t < L ? (a.direct ? (uint32_t)q : a.addrs[q * L + t]) : kEmpty;
+      }
+    };
+    auto extents_of = [&](uint64_t q) {  // of the addresses in nad -> nst/nsz/nex
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t t = 4 * lane + u, ad = nad[u];
+        nst[u] = 0;
+        nsz[u] = 0;
+        if (ad < lim) {
+          const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)t * a.range + ad;
+          nst[u] = a.goff[i];
+          nsz[u] = a.seg_len ? a.seg_len[i] : (uint32_t)(a.goff[i + 1] - nst[u]);
+        } else if (ad != kEmpty) {
+          atomicAdd(a.err, 1ull);  // an address outside the table
+        }
+      }
+      nex = a.exclude ? a.exclude[q] : (a.exclude_self ? a.self_base + (uint32_t)q : kEmpty);
+    };
+    uint64_t it = blockIdx.x;
+    if (it < nq) {
+      eq = query_at(it);
+      addrs_of(eq);
+      extents_of(eq);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        est[u] = nst[u];
+        esz[u] = nsz[u];
+      }
+      eex = nex;
+    }
+    if (it + g < nq) {
+      nq1 = query_at(it + g);
+      addrs_of(nq1);
+    }
+    if (it + 2 * g < nq) q2 = query_at(it + 2 * g);
+    uint32_t j = 0;
+    for (; it < nq; it += g, ++j) {
+      const uint32_t b = j & 1;
+      if (it + g < nq) extents_of(nq1);     // query j + 1 (its addresses arrived last round)
+      if (it + 2 * g < nq) addrs_of(q2);    // query j + 2
+      const uint64_t q3 = it + 3 * g < nq ? query_at(it + 3 * g) : 0;
+      // Q1 of query j: a warp scan of (size, non-empty) over its L buckets (sizes clamped
+      // above L*R: the sum then stays below 2^24; ranks < 2^8), the start bitmap and one
+      // base pointer per non-empty bucket, so that position p's bucket is a popc away
+      uint32_t v[4], tot = 0;
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t sz = esz[u] <= a.mmax ? esz[u] : (uint32_t)a.mmax + 1;
+        v[u] = tot;
+        tot += sz | ((uint32_t)(sz > 0) << 24);
+      }
+      uint32_t incl = tot;
 #pragma unroll
       for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-        if (lane >= o) x += y;
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
       }
-      if (lane == 31) hdr.wsum[wib] = x;
-      if (tid < L && more) nx_ad = bucket_addr(qn);  // prefetch: the next query's addresses
-    }
-    __syncthreads();
-    const uint32_t excl = hdr.excl;
-    const uint32_t wsl = lane < nwq ? hdr.wsum[lane] : 0u;
-    const uint32_t before_w = __reduce_add_sync(0xFFFFFFFFu, lane < wib ? wsl : 0u);
-    const uint32_t M = __reduce_add_sync(0xFFFFFFFFu, wsl) & 0xFFFFFFu;
-    if (sz > 0 && M <= a.mmax) {
-      const uint32_t ex = before_w + x - v;  // exclusive prefix: position | rank << 24
-      const uint32_t pos = ex & 0xFFFFFFu, r = ex >> 24;
-      nbase[r] = gids + (int64_t)(cur_st - (uint64_t)pos);
-      atomicOr(&bmap[pos >> 5].x, 1u << (pos & 31));
-      // words whose position just below them lies in this bucket: r + 1 starts below them
-      for (uint32_t w = (pos + 32) >> 5; w <= (pos + sz) >> 5; ++w) bmap[w].y = r + 1;
-    }
-    uint32_t* oid = a.out_ids + q * k;
-    uint32_t* ocnt = a.out_counts + q * k;
-    if (M > a.mmax || M == 0) {  // more than L*R candidates (bad direct segments): error + pads
-      if (M && tid == 0) atomicAdd(a.err, 1ull);
-      for (uint32_t j = tid; j < k; j += kMarkThreads) {
-        oid[j] = kEmpty;
-        ocnt[j] = 0;
-      }
-      if (tid < L) {
-        cur_ad = nx_ad;
-        bucket_extent(cur_ad, cur_st, cur_sz);
-      }
-      __syncthreads();  // hdr is rewritten for the next query
-      if (tid == 0 && more) hdr.excl = exclude_of(qn);
-      __syncthreads();
-      continue;
-    }
-    __syncthreads();
-
-    // ---- Q2: gather 32-position blocks (block b -> warp b mod 8, 4 in flight), mark the
-    //      bitmap, table the repeats.  Position p lies in bucket (#starts <= p) - 1.  The
-    //      excluded id is marked like any other and taken out at Q3a. ----
-    const bool staged = M <= stage_cap;
-    {
-      const uint32_t nblk = (M + 31) >> 5;
-      for (uint32_t b0 = wib; b0 < nblk; b0 += 4 * kMarkWarps) {
-        uint32_t idv[4];
+      const uint32_t M = __shfl_sync(0xFFFFFFFFu, incl, 31) & 0xFFFFFFu;
+      const uint32_t base = incl - tot;
+      if (j >= 2) bar_empty_sync(b);  // the consumers are done with buffer b
+      if (M <= a.mmax) {
+        uint2* bm = bmap + b * nbw;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t b = b0 + u * kMarkWarps, p = b * 32 + lane;
+        for (uint32_t u = 0; u < 4; ++u) {
+          const uint32_t sz = esz[u];
+          if (sz > 0) {
+            const uint32_t ex = base + v[u];  // exclusive prefix: position | rank << 24
+            const uint32_t pos = ex & 0xFFFFFFu, r = ex >> 24;
+            nbase[b * Lp + r] = gids + (int64_t)(est[u] - (uint64_t)pos);
+            atomicOr(&bm[pos >> 5].x, 1u << (pos & 31));
+            // words whose position just below them lies in this bucket: r + 1 starts below
+            for (uint32_t w = (pos + 32) >> 5; w <= (pos + sz) >> 5; ++w) bm[w].y = r + 1;
+          }
+        }
+      }
+      if (lane == 0) {
+        hdr.M[b] = M;
+        hdr.excl[b] = eex;
+        hdr.q[b] = eq;
+      }
+      bar_full_arrive(b);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        est[u] = nst[u];
+        esz[u] = nsz[u];
+      }
+      eex = nex;
+      eq = nq1;
+      nq1 = q2;
+      q2 = q3;
+    }
+    // match the consumers' last two arrivals on the empty barriers
+    for (uint32_t r = j >= 2 ? j - 2 : 0; r < j; ++r) bar_empty_sync(r & 1);
+    return;
+  }
+
+  // ==== the consumer warps (kConsWarps): Q2-Q3 of one query at a time ====
+  const uint32_t s_bits = (uint32_t)__cvta_generic_to_shared(bits);
+  const uint32_t s_rkey = (uint32_t)__cvta_generic_to_shared(rkey);
+  const uint32_t s_rcnt = (uint32_t)__cvta_generic_to_shared(rcnt);
+  uint32_t lanele;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(lanele));
+#ifdef FLASH_QPROF
+  long long mp_last = clock64();
+#endif
+  uint32_t cb = 0;  // this query's Q1 buffer
+  for (uint64_t it = blockIdx.x; it < nq; it += gridDim.x, cb ^= 1) {
+    // this query's Q1 is written; every consumer is past the previous query's reset
+    bar_full_sync(cb);
+    MMARK(0);
+    const uint32_t M = hdr.M[cb], excl = hdr.excl[cb];
+    const uint64_t q = hdr.q[cb];
+    const bool bad = M > a.mmax || M == 0;  // more than L*R candidates (bad direct segments): error + pads
+    const bool staged = M <= stage_cap;
+
+    // ---- Q2: gather 32-position blocks (block b -> warp b mod kConsWarps, 8 in flight per
+    //      lane), mark the bitmap, table the repeats.  Position p lies in bucket
+    //      (#starts <= p) - 1.  The excluded id (R#14) is dropped here. ----
+    if (!bad) {
+      const uint2* bm = bmap + cb * nbw;
+      const uint32_t* const* nbs = nbase + cb * Lp;
+      const uint32_t nblk = (M + 31) >> 5;
+      for (uint32_t b0 = wib; b0 < nblk; b0 += 8 * kConsWarps) {
+        uint32_t idv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t b = b0 + u * kConsWarps, p = b * 32 + lane;
           idv[u] = kEmpty;
           if (p < M) {
-            const uint2 e = bmap[b];
-            idv[u] = __ldg(nbase[e.y + __popc(e.x & lanele) - 1] + p);
+            const uint2 e = bm[b];
+            idv[u] = __ldg(nbs[e.y + __popc(e.x & lanele) - 1] + p);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           const uint32_t id = idv[u];
-          const uint32_t p = (b0 + u * kMarkWarps) * 32 + lane;
+          const uint32_t p = (b0 + u * kConsWarps) * 32 + lane;
           if (id < nbits) {
             if (staged) stage[p] = (uint16_t)(id >> 5);
-            const uint32_t bit = 1u << (id & 31);
-            const uint32_t old = smem_or(s_bits + ((id >> 5) << 2), bit);
-            if (old & bit) {  // a repeat: one more occurrence of id in the table
-              uint32_t s = (id * 0x9E3779B1u) >> (32 - kRepLog2);
+            if (id != excl) {
+              const uint32_t bit = 1u << (id & 31);
+              const uint32_t old = smem_or(s_bits + ((id >> 5) << 2), bit);
+              if (old & bit) {  // a repeat: one more occurrence of id in the table
+                uint32_t s = (id * 0x9E3779B1u) >> (32 - kRepLog2);
 #pragma unroll 1
-              for (uint32_t probe = 0;; ++probe) {
-                const uint32_t c = smem_cas(s_rkey + (s << 2), kEmpty, id);
-                if (c == kEmpty || c == id) {
-                  smem_add(s_rcnt + (s << 2), 1u);
-                  if (c == kEmpty) rslot[atomicAdd(&hdr.nrep, 1u)] = (uint16_t)s;
-                  break;
+                for (uint32_t probe = 0;; ++probe) {
+                  const uint32_t c = smem_cas(s_rkey + (s << 2), kEmpty, id);
+                  if (c == kEmpty || c == id) {
+                    smem_add(s_rcnt + (s << 2), 1u);
+                    if (c == kEmpty) rslot[atomicAdd(&hdr.nrep, 1u)] = (uint16_t)s;
+                    break;
+                  }
+                  if (probe == kRepProbes) {  // (a crowded table) -> the fallback kernel
+                    atomicExch(&hdr.overflow, 1u);
+                    break;
+                  }
+                  s = (s + 1) & (kRepSlots - 1);
                 }
-                if (probe == kRepProbes) {  // (a crowded table) -> the fallback kernel
-                  atomicExch(&hdr.overflow, 1u);
-                  break;
-                }
-                s = (s + 1) & (kRepSlots - 1);
               }
             }
           } else if (id != kEmpty) {
@@ -269,85 +362,49 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const 
         }
       }
     }
-    if (tid < L) {
-      cur_ad = nx_ad;
-      bucket_extent(cur_ad, cur_st, cur_sz);  // prefetch: the next query's bucket extents
-    }
-    __syncthreads();
+    bar_cons();  // B: the gather is done
+    MMARK(1);
 
-    // ---- Q3a (warp 0): compact the listed repeated ids into (count desc, id asc) keys,
-    //      clear their bits and the excluded id's (the bitmap then holds exactly the ids
-    //      seen once, excluded id aside) and the slots; the other warps reset the start
-    //      bitmap.  distinct ids = M - extra occurrences (ids above max_id aside). ----
-    if (wib == 0) {
-      const uint32_t nrep = hdr.nrep;
-      const bool ovf = hdr.overflow != 0 || nrep > rep_max;
-      uint32_t extra = 0;
-      bool xrep = false;
-      for (uint32_t j = lane; j < nrep; j += 32) {
-        const uint32_t s = rslot[j], key = rkey[s], c = rcnt[s];
-        extra += c;
-        xrep |= key == excl;
-        if (!ovf) {
-          rlist[j] = key == excl ? ~0ull : ((uint64_t)(0xFFFFFFFEu - (c + 1)) << 32) | key;
-          atomicAnd(&bits[key >> 5], ~(1u << (key & 31)));
-        }
-        rkey[s] = kEmpty;
-        rcnt[s] = 0;
+    // ---- Q3a: each listed repeated id becomes a (count desc, id asc) key and leaves the
+    //      bitmap, which then holds exactly the ids seen once; its slot is cleared.  Full
+    //      multiplicity = 1 + extra (R#11).  The start bitmap is cleared for the producer. ----
+    const uint32_t nrep = hdr.nrep;
+    const bool ovf = !bad && (hdr.overflow != 0 || nrep > rep_max);
+    for (uint32_t e = tid; e < nrep; e += kConsThreads) {
+      const uint32_t s = rslot[e], key = rkey[s], c = rcnt[s];
+      if (!ovf) {
+        rlist[e] = ((uint64_t)(0xFFFFFFFEu - (c + 1)) << 32) | key;
+        atomicAnd(&bits[key >> 5], ~(1u << (key & 31)));
       }
-      extra = __reduce_add_sync(0xFFFFFFFFu, extra);
-      xrep = __any_sync(0xFFFFFFFFu, xrep);
-      if (lane == 0) {
-        if (ovf) {
-          fb_list[atomicAdd(fb_count, 1u)] = (uint32_t)q;
-          hdr.overflow = 1;
-        } else {
-          bool xonce = false;  // the excluded id seen exactly once: its bit goes too
-          if (!xrep && excl < nbits) {
-            const uint32_t w = bits[excl >> 5], bit = 1u << (excl & 31);
-            xonce = (w & bit) != 0;
-            if (xonce) bits[excl >> 5] = w & ~bit;
-          }
-          hdr.nhi = nrep;  // listed entries (the excluded id's included)
-          hdr.nrep = nrep - (xrep ? 1u : 0u);
-          hdr.nsingle = M - extra - nrep - (xonce ? 1u : 0u);
-        }
-      }
-    } else {
-      for (uint32_t j = tid - 32; j <= (M >> 5) + 1 && j < nbw; j += kMarkThreads - 32) bmap[j].x = 0;
+      rkey[s] = kEmpty;
+      rcnt[s] = 0;
     }
-    __syncthreads();
-    const bool overflow = hdr.overflow != 0;
-    const uint32_t nrep = hdr.nrep, nlist = hdr.nhi;
-    if (!overflow) {
-      // ---- Q3b (warp 0): rank the repeated ids (count desc, id asc) ----
-      const uint32_t nhi = nrep < k ? nrep : k;
-      if (wib == 0) {
-        // (the listed entries: nrep, plus the excluded id's key ~0 when it repeated, which
-        //  ranks last and is not written)
-        const uint32_t nl = nlist;
-        for (uint32_t e0 = 0; e0 < nl; e0 += 32) {
-          const uint32_t e = e0 + lane;
-          const uint64_t me = e < nl ? rlist[e] : ~0ull;
-          uint32_t rank = 0;
-          if (nl <= 32) {
-            for (uint32_t j = 0; j < nl; ++j) rank += __shfl_sync(0xFFFFFFFFu, me, j) < me;
-          } else {
-            for (uint32_t j = 0; j < nl; ++j) rank += rlist[j] < me;
-          }
-          if (e < nl && rank < nhi) {
-            oid[rank] = (uint32_t)me;
-            ocnt[rank] = 0xFFFFFFFEu - (uint32_t)(me >> 32);
-          }
-        }
+    if (!bad) {
+      uint2* bm = bmap + cb * nbw;
+      for (uint32_t w = tid; w <= (M >> 5) + 1 && w < nbw; w += kConsThreads) bm[w].x = 0;
+    }
+    bar_empty_arrive(cb);  // buffer cb may be refilled
+    if (tid == 0) {
+      if (ovf) fb_list[atomicAdd(fb_count, 1u)] = (uint32_t)q;
+      if (bad && M) atomicAdd(a.err, 1ull);
+    }
+    bar_cons();  // C: the bitmap holds the singletons, rlist the repeated ids
+    MMARK(2);
+
+    uint32_t* oid = a.out_ids + q * k;
+    uint32_t* ocnt = a.out_counts + q * k;
+    if (bad) {
+      for (uint32_t j = tid; j < k; j += kConsThreads) {
+        oid[j] = kEmpty;
+        ocnt[j] = 0;
       }
-      // ---- Q3c: the smallest `target` singletons, in ascending id order ----
-      const uint32_t need = k - nhi;
-      const uint32_t nsingle = hdr.nsingle;
-      const uint32_t target = need < nsingle ? need : nsingle;
+    } else if (!ovf) {
+      // ---- Q3c: the smallest `need` singletons, in ascending id order (R#12) ----
+      const uint32_t nhi = nrep < k ? nrep : k;
+      const uint32_t target = k - nhi;
       uint32_t* osg = oid + nhi;
       uint32_t found = 0, buf = 0;
-      for (uint32_t w0 = 0; found < target && w0 < nwords; w0 += kMarkThreads * kScanWpt) {
+      for (uint32_t w0 = 0; found < target && w0 < nwords; w0 += kConsThreads * kScanWpt) {
         const uint32_t wt = w0 + tid * kScanWpt;
         uint32_t wv[kScanWpt];
         const bool in = wt < nwords;  // (nwords is a multiple of kScanWpt)
@@ -369,8 +426,8 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const 
           if (lane >= o) incl += y;
         }
         if (lane == 31) hdr.rsum[buf][wib] = incl;
-        __syncthreads();
-        const uint32_t rs = lane < kMarkWarps ? hdr.rsum[buf][lane] : 0u;
+        bar_cons();
+        const uint32_t rs = lane < kConsWarps ? hdr.rsum[buf][lane] : 0u;
         const uint32_t wpre = __reduce_add_sync(0xFFFFFFFFu, lane < wib ? rs : 0u);
         const uint32_t rtot = __reduce_add_sync(0xFFFFFFFFu, rs);
         uint32_t pos = found + wpre + incl - c;
@@ -392,36 +449,57 @@ __global__ void __launch_bounds__(kMarkThreads) k_query_mark(QueryArgs a, const 
         found += rtot;
         buf ^= 1;
       }
+      MMARK(3);
+      // ---- Q3b (warp 0): rank the repeated ids (count desc, id asc) ----
+      if (wib == 0) {
+        for (uint32_t e0 = 0; e0 < nrep; e0 += 32) {
+          const uint32_t e = e0 + lane;
+          const uint64_t me = e < nrep ? rlist[e] : ~0ull;
+          uint32_t rank = 0;
+          if (nrep <= 32) {
+            for (uint32_t j = 0; j < nrep; ++j) rank += __shfl_sync(0xFFFFFFFFu, me, j) < me;
+          } else {
+            for (uint32_t j = 0; j < nrep; ++j) rank += rlist[j] < me;
+          }
+          if (e < nrep && rank < nhi) {
+            oid[rank] = (uint32_t)me;
+            ocnt[rank] = 0xFFFFFFFEu - (uint32_t)(me >> 32);
+          }
+        }
+      }
       // counts of the singletons, then pads (EMPTY, 0)
-      for (uint32_t j = nhi + tid; j < k; j += kMarkThreads) {
-        const bool pad = j >= nhi + target;
+      const uint32_t nsg = found < target ? found : target;
+      for (uint32_t j = nhi + tid; j < k; j += kConsThreads) {
+        const bool pad = j >= nhi + nsg;
         if (pad) oid[j] = kEmpty;
         ocnt[j] = pad ? 0u : 1u;
       }
     }
-    __syncthreads();
+    MMARK(4);
 
-    // ---- reset for the next query (its Q1 barrier orders this before its gather) ----
-    if (staged) {  // 8 staged word indices per thread
-      for (uint32_t j = tid * 8; j < M; j += kMarkThreads * 8) {
-        const uint4 s4 = *reinterpret_cast<const uint4*>(stage + j);
-        bits[s4.x & 0xFFFFu] = 0;
-        bits[s4.x >> 16] = 0;
-        bits[s4.y & 0xFFFFu] = 0;
-        bits[s4.y >> 16] = 0;
-        bits[s4.z & 0xFFFFu] = 0;
-        bits[s4.z >> 16] = 0;
-        bits[s4.w & 0xFFFFu] = 0;
-        bits[s4.w >> 16] = 0;
+    // ---- reset for the next query (its full barrier orders it before the next gather):
+    //      the bitmap is no longer read once every consumer has passed barrier C or the
+    //      last scan round's ----
+    if (!bad) {
+      if (staged) {  // 8 staged word indices per thread
+        for (uint32_t j = tid * 8; j < M; j += kConsThreads * 8) {
+          const uint4 s4 = *reinterpret_cast<const uint4*>(stage + j);
+          bits[s4.x & 0xFFFFu] = 0;
+          bits[s4.x >> 16] = 0;
+          bits[s4.y & 0xFFFFu] = 0;
+          bits[s4.y >> 16] = 0;
+          bits[s4.z & 0xFFFFu] = 0;
+          bits[s4.z >> 16] = 0;
+          bits[s4.w & 0xFFFFu] = 0;
+          bits[s4.w >> 16] = 0;
+        }
+      } else {
+        uint4* b4 = reinterpret_cast<uint4*>(bits);
+        for (uint32_t j = tid; j < nwords / 4; j += kConsThreads) b4[j] = make_uint4(0, 0, 0, 0);
       }
-    } else {
-      uint4* b4 = reinterpret_cast<uint4*>(bits);
-      for (uint32_t j = tid; j < nwords / 4; j += kMarkThreads) b4[j] = make_uint4(0, 0, 0, 0);
     }
-    if (tid == 0) {
-      hdr.nrep = hdr.overflow = 0;
-      if (more) hdr.excl = exclude_of(qn);
-    }
+    if (tid == 0) hdr.nrep = hdr.overflow = 0;  // (read by every consumer before barrier C)
+    MMARK(5);
   }
 }
 
@@ -472,3 +550,14 @@ int launch_query_mark(const QueryArgs& a, const uint32_t* list, const uint32_t* 
 }
 
 }  // namespace flash
+
+#ifdef FLASH_QPROF
+extern "C" int flash_debug_mprof(unsigned long long out[8], int reset) {
+  if (cudaMemcpyFromSymbol(out, flash::g_mprof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(flash::g_mprof, z, sizeof z);
+  }
+  return 0;
+}
+#endif

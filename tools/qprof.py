@@ -22,10 +22,12 @@ ids = torch.empty((shape.N, k), dtype=torch.int32, device="cuda")
 cnt = torch.empty_like(ids)
 buf = (ctypes.c_ulonglong * 8)()
 prof = hasattr(lib, "flash_debug_qprof")
+mbuf = (ctypes.c_ulonglong * 8)()
 lib.flash_set_profiling(idx.h, 1)
 for rep in range(3):
     if prof:
         lib.flash_debug_qprof(buf, 1)
+        lib.flash_debug_mprof(mbuf, 1)
     idx.clear()
     flash.flash_knn_graph(idx.h, d_rp, d_col, shape.N, k, ids, cnt)
     torch.cuda.synchronize()
@@ -39,6 +41,14 @@ print(VARIANT, "phase ms (mean of 2): " + " ".join(f"{n} {ph[i] / max(nc[i], 1):
 if not prof:
     sys.exit(0)
 lib.flash_debug_qprof(buf, 0)
+lib.flash_debug_mprof(mbuf, 0)
+# the bitmap kernel (query_mark.cu), consumer thread 0 of each CTA: cycles between its barriers
+mnames = ["wait for Q1 (full barrier)", "Q2 gather+mark", "Q3a compact", "Q3c scan", "Q3b rank + pads",
+          "reset"]
+mtot = sum(mbuf[i] for i in range(6))
+for i, nm in enumerate(mnames):
+    print(f"mark {nm:22s} {mbuf[i] / shape.N:10.0f} cycles/query  {100 * mbuf[i] / max(mtot, 1):5.1f}%")
+print(f"mark total {mtot / shape.N:.0f} cycles/query (per CTA; queries not on the bitmap path count 0)")
 names = ["Q1 buckets", "Q2a count", "scan", "Q2b scatter", "bin sort", "Q3a runs", "Q3b/c select+write"]
 tot = sum(buf[i] for i in range(7))
 for i, nm in enumerate(names):
