@@ -12,6 +12,9 @@
 // flash_hash asks for them.  The bin update is a shared-memory atomicMin (RED.MIN): on
 // B200 it issues at the LDS rate (profiles/r01_microbench_smem.txt), so no
 // read-before-update filter is needed.
+#include <algorithm>
+#include <cstdlib>
+
 #include "flash_internal.cuh"
 
 namespace flash {
@@ -52,6 +55,10 @@ __device__ __forceinline__ uint32_t lanemask_lt_d() {
   return m;
 }
 
+__device__ __forceinline__ void smem_min(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void bin_min(uint32_t* v, uint32_t B, const HashKeys& k, uint32_t c) {
   const uint32_t h = perm(k, c);
   atomicMin(&v[__umulhi(h, B)], h);
@@ -64,11 +71,25 @@ __device__ __forceinline__ void bin_min(uint32_t* v, uint32_t B, const HashKeys&
 __device__ __forceinline__ void write_addrs(const uint32_t* code, bool nonempty, uint32_t K, uint32_t L,
                                             uint32_t range, const HashKeys& keys, const AddrOut& out,
                                             uint64_t n_rows, uint64_t r, uint32_t lane) {
+  // K % 4 == 0 with a 16-B aligned code array: the tuple in 16-byte shared loads (lanes 16 B
+  // apart: conflict-free, where 4-byte loads at a 4K-byte lane stride conflict K-way)
+  const bool vec = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(code) & 15) == 0;
   for (uint32_t t = lane; t < L; t += 32) {
     uint32_t a = kEmpty;
     if (nonempty) {
       uint32_t x = fmix32(keys.s_addr ^ t);
-      for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
+      if (vec) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(code + t * K);
+        for (uint32_t j = 0; j < K / 4; ++j) {
+          const uint4 q = c4[j];
+          x = fmix32(x ^ q.x);
+          x = fmix32(x ^ q.y);
+          x = fmix32(x ^ q.z);
+          x = fmix32(x ^ q.w);
+        }
+      } else {
+        for (uint32_t j = 0; j < K; ++j) x = fmix32(x ^ code[t * K + j]);
+      }
       a = __umulhi(x, range);
     }
     if (out.world == 1) {
@@ -348,6 +369,203 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rows that leave most of B > 256 bins empty (nnz <= B/2: the url shape, ~116 nnz into 512
+// bins, ~100 non-empty).  Probing (k_doph) spends ~1/p dependent hash + load probes per
+// empty bin, p = |NE|/B ~ 0.2, with divergent chain lengths (url: ~3,900 warp-instructions
+// per row).  Here the chains are inverted once per CTA:
+//   inv[j]   = kMidC entries (a << 11 | i) with probe(i, a) = j, taken in increasing a
+//              (a <= kMidT1) until the list is full; short lists are padded with entries
+//              that hit a dummy slot;
+//   cover[i] = the depth up to which every probe of bin i's chain is listed (one less than
+//              the first of its entries a full list dropped; else kMidT1).
+// A row scatters, for each non-empty bin j, the key (a << 11 | j) of all kMidC entries of
+// inv[j] into best[i] with shared-memory atomicMin (every list has the same length: lanes
+// take (bin, 8-entry chunk) items, no divergence).  When best[i]'s depth is <= cover[i] it
+// is the first position at which bin i's chain reaches a non-empty bin, so its j is the
+// donor of R#4; otherwise (rare: ~0.8^cover[i]) the warp's lanes probe positions
+// cover[i]+1..T in parallel (one ballot per 32 probes), then the circular scan.  Densified
+// codes are written in place after every miss is resolved (a donor is always an originally
+// non-empty bin, which nothing overwrites).  Lane l owns bins 128c + 4l .. +3 (16-byte
+// shared-memory accesses, conflict-free).
+constexpr uint32_t kMidMaxB = 2047;  // 11-bit bin field; B itself is the dummy slot
+constexpr uint32_t kMidT1 = 31;      // deepest listed chain position (5-bit field)
+constexpr uint32_t kMidC = 32;       // entries per inverted list (4 chunks of 8; FLASH_DOPH_MIDC: 8/16/32)
+constexpr int kMidThreads = 512;
+
+__host__ __device__ __forceinline__ uint32_t mid_pad(uint32_t B) { return (B + 127) & ~127u; }
+__host__ __device__ __forceinline__ uint32_t mid_table_words(uint32_t B, uint32_t C) {
+  return B * C / 2 + (B + 3) / 4;  // inv u16[B][C], cover u8[B]
+}
+__host__ __device__ __forceinline__ uint32_t mid_warp_words(uint32_t B) {
+  // v[Bp] (codes in place), best[Bp + 4] (dummy slot B), NE list u16[B/2 + 2]
+  return (mid_pad(B) + mid_pad(B) + 4 + (B / 2 + 2) / 2 + 3) & ~3u;  // (16-B aligned)
+}
+
+template <bool kCodes, bool kAddrs>
+__global__ void __launch_bounds__(kMidThreads, 2) k_doph_mid(const int64_t* __restrict__ row_ptr,
+                                                          const uint32_t* __restrict__ col_idx,
+                                                          uint64_t n_rows, uint32_t K, uint32_t L,
+                                                          uint32_t range, HashKeys keys,
+                                                          uint32_t* __restrict__ codes, AddrOut out,
+                                                          uint32_t T1, uint32_t C, int64_t mid_le) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t B = K * L, Bp = mid_pad(B), nc = Bp >> 7;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const uint32_t nchk = C / 8;
+  const uint4* inv = reinterpret_cast<const uint4*>(smem);                    // [B][C / 8]
+  uint8_t* cover = reinterpret_cast<uint8_t*>(smem + B * C / 2);              // [B]
+  uint32_t* v = smem + ((mid_table_words(B, C) + 3) & ~3u) + (size_t)warp * mid_warp_words(B);
+  uint32_t* best = v + Bp;                                                     // [Bp + 4]
+  uint16_t* nel = reinterpret_cast<uint16_t*>(best + Bp + 4);                 // [B / 2 + 2]
+  uint4* v4 = reinterpret_cast<uint4*>(v);
+  uint4* best4 = reinterpret_cast<uint4*>(best);
+  const uint32_t* cover4 = reinterpret_cast<const uint32_t*>(cover);
+
+  // ---- the CTA table, in increasing depth a (warp 0's v serves as the list cursors) ----
+  {
+    uint32_t* cnt = v - (size_t)warp * mid_warp_words(B);
+    uint16_t* ent = reinterpret_cast<uint16_t*>(smem);
+    const uint32_t pad = (31u << 11) | B;  // -> the dummy slot best[B]
+    for (uint32_t x = threadIdx.x; x < B * C; x += blockDim.x) ent[x] = (uint16_t)pad;
+    for (uint32_t j = threadIdx.x; j < B; j += blockDim.x) {
+      cnt[j] = 0;
+      cover[j] = (uint8_t)T1;
+    }
+    for (uint32_t a = 1; a <= T1; ++a) {
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+        const uint32_t j = __umulhi(fmix32(keys.s_dens ^ ((i << 8) | a)), B);
+        const uint32_t pos = atomicAdd(&cnt[j], 1u);
+        if (pos < C) ent[j * C + pos] = (uint16_t)((a << 11) | i);
+        else if (cover[i] == T1) cover[i] = (uint8_t)(a - 1);
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t x = lane; x < (Bp + 4) / 4; x += 32) best4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  __syncwarp();
+
+  const uint64_t nw = (uint64_t)gridDim.x * wpb;
+  for (uint64_t r0 = ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 += nw * 32) {
+    const uint64_t rl = r0 + lane;
+    const int64_t my_e0 = rl < n_rows ? row_ptr[rl] : 0, my_e1 = rl < n_rows ? row_ptr[rl + 1] : 0;
+    uint32_t todo = __ballot_sync(0xFFFFFFFFu, rl < n_rows && my_e1 - my_e0 <= mid_le);
+    while (todo) {  // the others are k_doph's
+      const uint32_t src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t r = r0 + src;
+      const int64_t e0 = __shfl_sync(0xFFFFFFFFu, my_e0, src), e1 = __shfl_sync(0xFFFFFFFFu, my_e1, src);
+      for (uint32_t c = 0; c < nc; ++c) v4[c * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      __syncwarp();
+      // ---- H1: 4 loads in flight per lane ----
+      for (int64_t e = e0 + lane; e < e1; e += 128) {
+        uint32_t cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cv[u] = e + 32 * u < e1 ? ld_stream(col_idx + e + 32 * u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e + 32 * u < e1) bin_min(v, B, keys, cv[u]);
+      }
+      __syncwarp();
+      // ---- the non-empty bins, listed in (bin mod 4, lane) order per chunk ----
+      uint32_t nne = 0;
+      for (uint32_t c = 0; c < nc; ++c) {
+        const uint4 q = v4[c * 32 + lane];
+        const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          const bool full = x[k] != kEmpty;  // (bins >= B stay EMPTY)
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, full);
+          if (full) nel[nne + __popc(m & lanemask_lt_d())] = (uint16_t)(c * 128 + 4 * lane + k);
+          nne += __popc(m);
+        }
+      }
+      __syncwarp();
+      if (nne) {
+        // ---- H2a: scatter (a << 11 | j) of the NE bins' lists, one 8-entry chunk per item ----
+        const uint32_t s_best = (uint32_t)__cvta_generic_to_shared(best);
+        for (uint32_t it = lane; it < nne * nchk; it += 32) {
+          const uint32_t j = nel[nchk == 2 ? it >> 1 : (nchk == 1 ? it : it / nchk)];
+          const uint4 q = inv[j * nchk + (it - (it / nchk) * nchk)];
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // per entry: mask, address, key, RED.MIN
+            const uint32_t hi = w[u] >> 16;
+            smem_min(s_best + ((w[u] & 0x7FFu) << 2), (w[u] & 0xF800u) | j);
+            smem_min(s_best + ((hi & 0x7FFu) << 2), (hi & 0xF800u) | j);
+          }
+        }
+        __syncwarp();
+        // ---- H2b: bins the lists do not settle (no listed hit, or one deeper than cover[i])
+        //      probe on from depth cover[i] + 1 on pre-densification v, one bin at a time, the
+        //      warp's lanes evaluating 32 consecutive positions per ballot (a lane-parallel
+        //      probing loop over the missed bins measured slower: url 10.9 vs 8.2 ms) ----
+        for (uint32_t c = 0; c < nc; ++c) {
+          const uint4 qv = v4[c * 32 + lane], qb = best4[c * 32 + lane];
+          const uint32_t cov = cover4[c * 32 + lane];  // (bins >= B: never a miss)
+          const uint32_t x[4] = {qv.x, qv.y, qv.z, qv.w}, kb[4] = {qb.x, qb.y, qb.z, qb.w};
+          uint32_t mk = 0;
+#pragma unroll
+          for (uint32_t k = 0; k < 4; ++k) {
+            const uint32_t i = c * 128 + 4 * lane + k;
+            const uint32_t depth = kb[k] == kEmpty ? 32u : kb[k] >> 11;
+            if (i < B && x[k] == kEmpty && depth > ((cov >> (8 * k)) & 0xFFu)) mk |= 1u << k;
+          }
+          uint32_t lm = __ballot_sync(0xFFFFFFFFu, mk != 0);
+          while (lm) {  // warp-uniform: one missed bin at a time
+            const uint32_t sl = __ffs(lm) - 1;
+            const uint32_t smk = __shfl_sync(0xFFFFFFFFu, mk, sl);
+            const uint32_t k = __ffs(smk) - 1;
+            if (lane == sl) mk &= mk - 1;
+            if ((smk & (smk - 1)) == 0) lm &= lm - 1;
+            const uint32_t bi = c * 128 + 4 * sl + k;
+            uint32_t donor = kEmpty;
+            for (uint32_t a0 = cover[bi] + 1u; a0 <= kProbes && donor == kEmpty; a0 += 32) {
+              const uint32_t a = a0 + lane;
+              const uint32_t jp = __umulhi(fmix32(keys.s_dens ^ ((bi << 8) | a)), B);
+              const bool hit = a <= kProbes && v[jp] != kEmpty;
+              const uint32_t hm = __ballot_sync(0xFFFFFFFFu, hit);
+              if (hm) donor = __shfl_sync(0xFFFFFFFFu, jp, __ffs(hm) - 1);
+            }
+            if (donor == kEmpty) {  // circular scan after the T-th probe (the row is non-empty)
+              const uint32_t st = __umulhi(fmix32(keys.s_dens ^ ((bi << 8) | kProbes)), B) + 1;
+              for (uint32_t o0 = 0; o0 < B && donor == kEmpty; o0 += 32) {
+                uint32_t p = st + o0 + lane;
+                while (p >= B) p -= B;
+                const bool hit = o0 + lane < B && v[p] != kEmpty;
+                const uint32_t hm = __ballot_sync(0xFFFFFFFFu, hit);
+                if (hm) donor = __shfl_sync(0xFFFFFFFFu, p, __ffs(hm) - 1);
+              }
+            }
+            if (lane == 0) best[bi] = donor;  // depth 0: taken as is below
+          }
+        }
+        __syncwarp();
+        // ---- H2c: densify in place, reset best ----
+        for (uint32_t c = 0; c < nc; ++c) {
+          uint4 qv = v4[c * 32 + lane];
+          const uint4 qb = best4[c * 32 + lane];
+          best4[c * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          const uint32_t base = c * 128 + 4 * lane;
+          if (qv.x == kEmpty && base + 0 < B) qv.x = v[qb.x & 0x7FFu];
+          if (qv.y == kEmpty && base + 1 < B) qv.y = v[qb.y & 0x7FFu];
+          if (qv.z == kEmpty && base + 2 < B) qv.z = v[qb.z & 0x7FFu];
+          if (qv.w == kEmpty && base + 3 < B) qv.w = v[qb.w & 0x7FFu];
+          __syncwarp();  // (every lane's donor reads of this chunk precede its stores)
+          v4[c * 32 + lane] = qv;
+        }
+        if (lane == 0) best[B] = kEmpty;
+      }
+      __syncwarp();
+      if (kCodes)
+        for (uint32_t i = lane; i < B; i += 32) codes[r * B + i] = v[i];
+      if (kAddrs) write_addrs(v, nne > 0, K, L, range, keys, out, n_rows, r, lane);
+      __syncwarp();
+    }
+  }
+}
+
 template <bool C, bool A>
 int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
              uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
@@ -368,6 +586,40 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
                                                                  codes, out);
     ++launched;
     skip_le = kSparseNnz;
+  } else if (B <= kMidMaxB) {  // rows with <= B/2 nonzeros: the inverted-chain kernel
+    // FLASH_DOPH_MID_LE (tests, tuning): the row-length cut, -1 = off; FLASH_DOPH_T1 (tests):
+    // a shallower inverted depth T1 (more rows' bins take the probing path)
+    const char* e = getenv("FLASH_DOPH_MID_LE");
+    int64_t mid_le = e ? strtoll(e, nullptr, 10) : (int64_t)(B / 2);
+    if (mid_le > (int64_t)(B / 2)) mid_le = B / 2;
+    const char* et = getenv("FLASH_DOPH_T1");
+    uint32_t T1 = et ? (uint32_t)strtoul(et, nullptr, 10) : kMidT1;
+    T1 = T1 < 1 ? 1 : (T1 > kMidT1 ? kMidT1 : T1);
+    const char* ec = getenv("FLASH_DOPH_MIDC");
+    uint32_t mc = ec ? (uint32_t)strtoul(ec, nullptr, 10) : kMidC;
+    mc = mc <= 8 ? 8 : (mc <= 16 ? 16 : 32);
+    if (mid_le >= 0) {
+      // as many warps (<= 16) as fit beside the table in one CTA's shared memory
+      const size_t tbytes = (size_t)((mid_table_words(B, mc) + 3) & ~3u) * 4, wbytes = (size_t)mid_warp_words(B) * 4;
+      const size_t cap = 227 * 1024;
+      const uint32_t wpb = tbytes + 4 * wbytes <= cap ? (uint32_t)std::min<size_t>(kMidThreads / 32, (cap - tbytes) / wbytes) : 0;
+      const size_t smem = tbytes + wpb * wbytes;
+      if (wpb && ensure_smem_attr((const void*)k_doph_mid<C, A>, smem, true)) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_doph_mid<C, A>, wpb * 32, smem);
+        if (per_sm >= 1) {
+          uint64_t blocks = (uint64_t)device_sms() * per_sm;
+          const uint64_t need = (n_rows + wpb * 32 - 1) / (wpb * 32);  // 32 rows per warp-chunk
+          if (blocks > need) blocks = need;
+          if (blocks) {
+            k_doph_mid<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range,
+                                                                      keys, codes, out, T1, mc, mid_le);
+            ++launched;
+          }
+          skip_le = mid_le;
+        }
+      }
+    }
   }
   const size_t per_warp = (size_t)warp_words(B) * sizeof(uint32_t);
   int wpb = (int)((96 * 1024) / per_warp);

@@ -55,6 +55,12 @@ HASH_CASES = [
     ("url_slice", lambda: shape_slice("url", 4000), 4, 128, 1 << 15),
     ("kdd12_slice", lambda: shape_slice("kdd12", 20000), 4, 32, 1 << 20),
     ("wide_K", lambda: shape_slice("url", 500), 64, 2, 12345),
+    # the inverted-chain kernel (k_doph_mid: 256 < K*L <= 2047, rows with nnz <= K*L/2)
+    ("kdd12_B512", lambda: shape_slice("kdd12", 6000), 4, 128, 1 << 20),
+    ("url_B1024", lambda: shape_slice("url", 1500), 8, 128, 1 << 15),
+    ("edge_B512", edge_csr, 4, 128, 1000),
+    ("url_B2047", lambda: shape_slice("url", 600), 23, 89, 1 << 15),
+    ("tiny_B260", lambda: synth.generate("tiny"), 2, 130, 1 << 15),
 ]
 
 
@@ -72,6 +78,26 @@ def test_hash_codes_and_addresses_bit_exact(name, make, K, L, rng):
         # addresses alone (the insert/graph kernel variant)
         _, a2 = idx.hash(d_rp, d_col, codes=False)
         assert np.array_equal(flash.as_u32(a2), o_addrs)
+
+
+@pytest.mark.parametrize("T1,mid_le", [("1", None), ("8", None), ("31", None), (None, "-1"), (None, "40")])
+def test_hash_inverted_chain_kernel_settings(monkeypatch, T1, mid_le):
+    """k_doph_mid under other inverted-chain depths T1 (T1 = 1 sends most empty bins to the
+    parallel probes and the circular scan) and row-length cuts (-1 = every row probes in
+    k_doph; 40 = a mix of both kernels), bit-exact vs the oracle."""
+    if T1 is not None:
+        monkeypatch.setenv("FLASH_DOPH_T1", T1)
+    if mid_le is not None:
+        monkeypatch.setenv("FLASH_DOPH_MID_LE", mid_le)
+    for name, K, L, n in (("url", 4, 128, 1200), ("kdd12", 4, 128, 3000), ("tiny", 3, 100, 800)):
+        rp, col = shape_slice(name, n)
+        seed = 0x5EED0000 + K * 131 + L
+        d_rp, d_col = flash.to_device_csr(rp, col)
+        with flash.FlashIndex(K, L, 8, 1 << 15, seed) as idx:
+            codes, addrs = idx.hash(d_rp, d_col)
+            o_codes = oracle.doph(K, L, seed, rp, col)
+            assert np.array_equal(flash.as_u32(codes), o_codes), name
+            assert np.array_equal(flash.as_u32(addrs), oracle.addresses(K, L, 1 << 15, seed, o_codes)), name
 
 
 def test_hash_row_slice_with_absolute_offsets_and_unaligned_col_idx():

@@ -41,7 +41,8 @@ out = torch.empty((shape.N, L), dtype=torch.int32, device="cuda")
 ref = None
 for name in VARIANTS:
     flash._lib = None
-    flash.load_library(os.path.join(ROOT, "paper_1709_01190_b200", f"libflash_d_{name}.so"))
+    flash.load_library(flash.LIB_PATH if name == "base" else
+                       os.path.join(ROOT, "paper_1709_01190_b200", f"libflash_d_{name}.so"))
     h = flash.flash_create(K, L, 32, rng, seed)
     ts = []
     for r in range(args.reps + 1):
@@ -58,4 +59,4 @@ for name in VARIANTS:
         ref = out.clone()
     else:
         same = bool(torch.equal(ref, out))
-    print(f"{args.shape} {name}: hash {statistics.median(ts):.3f} ms (min {min(ts):.3f}) same={same}", flush=True)
+    print(f"{args.shape} {name} C={os.environ.get("FLASH_DOPH_MIDC", "-")} le={os.environ.get("FLASH_DOPH_MID_LE", "-")}: hash {statistics.median(ts):.3f} ms (min {min(ts):.3f}) same={same}", flush=True)
