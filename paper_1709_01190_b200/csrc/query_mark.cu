@@ -185,8 +185,9 @@ __global__ void __launch_bounds__(kMarkThreads, 4)
     //      `lane` holds tables t = 4 lane + u (u < 4).  Loads run ahead: a query's extents
     //      one query early, its addresses two, its index three. ====
     uint32_t nad[4];               // addresses of query j + 1
-    uint64_t est[4], nst[4];       // extents: of query j (est/esz), of query j + 1 (nst/nsz)
-    uint32_t esz[4], nsz[4];
+    uint64_t est[4], nst[4];       // extents: of query j (est/esz), of query j + 1 (nst/nen,
+    uint32_t esz[4];               // raw: the end offset or segment length, subtracted at use
+    uint64_t nen[4];
     uint64_t eq = 0, nq1 = 0, q2 = 0;  // query indices j, j + 1, j + 2
     uint32_t eex = kEmpty, nex = kEmpty;
     const uint64_t g = gridDim.x;
@@ -202,11 +203,11 @@ __global__ void __launch_bounds__(kMarkThreads, 4)
       for (uint32_t u = 0; u < 4; ++u) {
         const uint32_t t = 4 * lane + u, ad = nad[u];
         nst[u] = 0;
-        nsz[u] = 0;
+        nen[u] = 0;
         if (ad < lim) {
           const uint64_t i = a.shared ? (uint64_t)ad : (uint64_t)t * a.range + ad;
           nst[u] = a.goff[i];
-          nsz[u] = a.seg_len ? a.seg_len[i] : (uint32_t)(a.goff[i + 1] - nst[u]);
+          nen[u] = a.seg_len ? (uint64_t)a.seg_len[i] : a.goff[i + 1];
         } else if (ad != kEmpty) {
           atomicAdd(a.err, 1ull);  // an address outside the table
         }
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kMarkThreads, 4)
 #pragma unroll
       for (uint32_t u = 0; u < 4; ++u) {
         est[u] = nst[u];
-        esz[u] = nsz[u];
+        esz[u] = a.seg_len ? (uint32_t)nen[u] : (uint32_t)(nen[u] - nst[u]);
       }
       eex = nex;
     }
@@ -265,9 +266,23 @@ __global__ void __launch_bounds__(kMarkThreads, 4)
             const uint32_t pos = ex & 0xFFFFFFu, r = ex >> 24;
             nbase[b * Lp + r] = gids + (int64_t)(est[u] - (uint64_t)pos);
             atomicOr(&bm[pos >> 5].x, 1u << (pos & 31));
-            // words whose position just below them lies in this bucket: r + 1 starts below
-            for (uint32_t w = (pos + 32) >> 5; w <= (pos + sz) >> 5; ++w) bm[w].y = r + 1;
           }
+        }
+        __syncwarp();
+        // .y of each word: the starts below it (an exclusive scan of the words' popcounts,
+        // lanes over words; was a per-bucket fill loop, divergent with the bucket sizes)
+        uint32_t carry = 0;
+        for (uint32_t w0 = 0; w0 < (M + 31) >> 5; w0 += 32) {
+          const uint32_t w = w0 + lane;
+          const uint32_t c = w < nbw ? __popc(bm[w].x) : 0u;
+          uint32_t in = c;
+#pragma unroll
+          for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, in, o);
+            if (lane >= o) in += y;
+          }
+          if (w < nbw) bm[w].y = carry + in - c;
+          carry += __shfl_sync(0xFFFFFFFFu, in, 31);
         }
       }
       if (lane == 0) {
@@ -279,7 +294,7 @@ __global__ void __launch_bounds__(kMarkThreads, 4)
 #pragma unroll
       for (uint32_t u = 0; u < 4; ++u) {
         est[u] = nst[u];
-        esz[u] = nsz[u];
+        esz[u] = a.seg_len ? (uint32_t)nen[u] : (uint32_t)(nen[u] - nst[u]);
       }
       eex = nex;
       eq = nq1;
