@@ -19,6 +19,9 @@
 // as the fallback).
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "flash_internal.cuh"
 
 namespace flash {
@@ -376,7 +379,18 @@ __global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32
     if (kMode != 1) {
       for (uint32_t b = threadIdx.x; b < gsz; b += blockDim.x) bc[b] = 0;
       __syncthreads();
-      for (uint64_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) atomicAdd(&bc[ent[p] >> kGChunkLog2], 1u);
+      // 4 entry loads in flight per thread before their counter updates
+      for (uint64_t p0 = e0 + threadIdx.x; p0 < e1; p0 += 4 * (uint64_t)blockDim.x) {
+        uint32_t ev[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t p = p0 + (uint64_t)u * blockDim.x;
+          ev[u] = p < e1 ? ent[p] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ev[u] != 0xFFFFFFFFu) atomicAdd(&bc[ev[u] >> kGChunkLog2], 1u);
+      }
       __syncthreads();
       for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) cursor[tb + b] = bc[b];
       __syncthreads();
@@ -421,16 +435,26 @@ __global__ void __launch_bounds__(kGPlaceThreads, 1) k_gplace(uint32_t W, uint32
         else hi = mid;
       }
     }
-    for (uint64_t blk = wb0; blk < wb1; ++blk) {
-      const uint64_t pb = e0 + (blk << 5);
-      while (co[c + 1] <= pb) ++c;
-      const uint64_t p = pb + lane;
-      if (p < e1) {
-        uint32_t cl = c;
-        while (co[cl + 1] <= p) ++cl;
-        const uint32_t e = ent[p];
-        const uint32_t slot = atomicAdd(&bc[e >> kGChunkLog2], 1u);
-        pool[e0 + slot] = id_base + (cl << kGChunkLog2) + (e & ((1u << kGChunkLog2) - 1));
+    for (uint64_t blk0 = wb0; blk0 < wb1; blk0 += 4) {  // 4 blocks' entry loads in flight per lane
+      uint32_t ev[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t p = e0 + ((blk0 + u) << 5) + lane;
+        ev[u] = blk0 + u < wb1 && p < e1 ? ent[p] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (blk0 + u >= wb1) break;
+        const uint64_t pb = e0 + ((blk0 + u) << 5);
+        while (co[c + 1] <= pb) ++c;
+        const uint64_t p = pb + lane;
+        if (p < e1) {
+          uint32_t cl = c;
+          while (co[cl + 1] <= p) ++cl;
+          const uint32_t e = ev[u];
+          const uint32_t slot = atomicAdd(&bc[e >> kGChunkLog2], 1u);
+          pool[e0 + slot] = id_base + (cl << kGChunkLog2) + (e & ((1u << kGChunkLog2) - 1));
+        }
       }
     }
     __syncthreads();
@@ -828,6 +852,92 @@ __device__ __forceinline__ void sort_store_upto(const uint32_t* buf, uint32_t n,
 // digit, stopping as soon as the R-th smallest is pinned down, ~log16(m) + 1 digits); the
 // kept ids are then sorted ascending in registers.  Exact priority ties at the threshold (probability
 // ~m^2/2^33) go to the exact CTA path.
+// one bucket of m <= 32*E members (E = ceil(m / 32): only the register slots that hold
+// members are hashed, counted and compacted)
+// (false: priorities tie at the threshold, nothing written — the caller lists the bucket for
+// the exact CTA path)
+template <int E>
+__device__ __forceinline__ bool select_mid_bucket(uint32_t i, uint32_t m, uint64_t p0, uint32_t range, uint32_t R,
+                                                  const HashKeys& keys, const uint32_t* pool, uint32_t* out,
+                                                  uint32_t* kbuf, uint32_t* hist, uint32_t lane) {
+  uint32_t id[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) id[u] = lane + 32u * u < m ? pool[p0 + lane + 32u * u] : kEmpty;
+  uint32_t keep = m;
+  if (m > R) {
+    const uint32_t t = i / range, b = i - t * range;
+    const uint64_t tb = prio_bucket_key(keys, t, b);
+    uint32_t pr[E];
+#pragma unroll
+    for (int u = 0; u < E; ++u) pr[u] = lane + 32u * u < m ? prio_of(tb, id[u]) : 0xFFFFFFFFu;
+    // radix select over 4-bit digits, most significant first: a per-warp shared-memory
+    // histogram of the candidates still matching `prefix`; the R-th smallest priority lies
+    // in digit d of the current position, everything in the digits below d is kept
+    uint32_t prefix = 0, need = R, ubound = 0;
+    bool done = false;
+    for (int sh = 28; sh >= 0 && !done; sh -= 4) {
+      const uint32_t hi_mask = sh == 28 ? 0u : ~((16u << sh) - 1u);
+      if (lane < 16) hist[lane] = 0;
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < E; ++u)
+        if ((lane + 32u * u < m) && (pr[u] & hi_mask) == prefix) atomicAdd(&hist[(pr[u] >> sh) & 15u], 1u);
+      __syncwarp();
+      const uint32_t hc = lane < 16 ? hist[lane] : 0u;
+      uint32_t x = hc;
+#pragma unroll
+      for (uint32_t o = 1; o < 16; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t d = __ffs(__ballot_sync(kFull, lane < 16 && x >= need)) - 1;
+      const uint32_t below = __shfl_sync(kFull, x - hc, d), cd = __shfl_sync(kFull, hc, d);
+      need -= below;  // still needed inside digit d (1 <= need <= cd)
+      prefix |= d << sh;
+      if (need == cd) {
+        ubound = prefix + (1u << sh);  // keep every priority < ubound (0: 2^32)
+        done = true;
+      }
+      __syncwarp();
+    }
+    if (!done) return false;  // priorities tie at the threshold: exact CTA path
+    // compact the kept ids (priority < ubound; ubound == 0 means 2^32) into shared memory
+    uint32_t base = 0;
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const bool k_ = (lane + 32u * u < m) && (ubound == 0 || pr[u] < ubound);
+      const uint32_t bal = __ballot_sync(kFull, k_);
+      if (k_) kbuf[base + __popc(bal & lanemask_lt())] = id[u];
+      base += __popc(bal);
+    }
+    keep = R;
+  } else {
+#pragma unroll
+    for (int u = 0; u < E; ++u)
+      if (lane + 32u * u < m) kbuf[lane + 32u * u] = id[u];
+  }
+  __syncwarp();
+  sort_store_upto<8>(kbuf, keep, out);  // kept ids ascending (R#10)
+  __syncwarp();
+  return true;
+}
+
+// select_mid_bucket with E = ceil(m / 32) (warp-uniform), m <= kMidMax
+__device__ __forceinline__ bool select_mid_any(uint32_t i, uint32_t m, uint64_t p0, uint32_t range, uint32_t R,
+                                               const HashKeys& keys, const uint32_t* pool, uint32_t* out,
+                                               uint32_t* kbuf, uint32_t* hist, uint32_t lane) {
+  switch ((m + 31) >> 5) {
+    case 0:
+    case 1: return select_mid_bucket<1>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    case 2: return select_mid_bucket<2>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    case 3: return select_mid_bucket<3>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    case 4: return select_mid_bucket<4>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    case 5: return select_mid_bucket<5>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    case 6: return select_mid_bucket<6>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+    default: return select_mid_bucket<8>(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane);
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restrict__ mid_list,
              const uint32_t* __restrict__ mid_count, const uint64_t* __restrict__ pool_off,
@@ -837,6 +947,7 @@ k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restri
   __shared__ uint32_t hist_s[8][16];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t* kbuf = kept_s[w];
+  uint32_t* hist = hist_s[w];
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   const uint32_t nmid = *mid_count;
   for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + w; it < nmid; it += nw) {
@@ -844,69 +955,161 @@ k_select_mid(uint32_t range, uint32_t R, HashKeys keys, const uint32_t* __restri
     const uint64_t p0 = pool_off[i];
     const uint32_t m = (uint32_t)(pool_off[i + 1] - p0);
     uint32_t* out = ids_out + goff[i];
-    uint32_t id[8];
+    if (!select_mid_any(i, m, p0, range, R, keys, pool, out, kbuf, hist, lane)) push_big(i, big_list, big_count);
+  }
+}
+
+// Grouped placement fused with the bottom-R select (fresh builds of big tables on the
+// grouped path, R <= kMidMax; after the bucket counts are scanned).  One 1,024-thread CTA
+// per group at a time: the group's buckets go in sub-ranges of kGSelSub; the members of a
+// sub-range's buckets with <= kMidMax members are placed into shared memory (bucket-major,
+// at the block scan of their counts) instead of the pool, and each warp then selects the
+// bottom-R of its buckets there (select_mid_any) and writes the kept ids, ascending, to
+// their final place — the pool write and the selects' re-read of it (19 GB each for kdd12)
+// disappear.  Larger buckets, and every bucket of a sub-range whose members exceed the
+// stage, are placed into the pool as k_gplace does and listed for the select kernels
+// (reg_list: k_select_mid, mid_list: k_select_warp, > kWarpMax: k_pool_sizes' early list
+// or big_list); a bucket whose priorities tie at the threshold is copied to the pool and
+// listed for the exact CTA path.
+constexpr uint32_t kGSelSub = 256;
+
+__host__ __device__ inline size_t gsel_fixed_smem(uint32_t nch) {
+  return (size_t)(nch + 1) * 8 + (size_t)(3 * kGSelSub + 1 + 32) * 4 + (size_t)(kGPlaceThreads / 32) * (kMidMax + 16) * 4;
+}
+
+__global__ void __launch_bounds__(kGPlaceThreads, 1)
+k_gplace_sel(uint32_t W, uint32_t t0, uint32_t range, GroupGeom g, const uint64_t* __restrict__ goffs,
+             const uint32_t* __restrict__ ent, uint32_t id_base, const uint64_t* __restrict__ pool_off,
+             uint32_t* __restrict__ pool, uint32_t stage_cap, uint32_t R, HashKeys keys,
+             const uint64_t* __restrict__ goff, uint32_t* __restrict__ ids_out, int early_listed,
+             uint32_t* __restrict__ mid_list, uint32_t* __restrict__ mid_count,
+             uint32_t* __restrict__ reg_list, uint32_t* __restrict__ reg_count,
+             uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  extern __shared__ uint64_t co[];                                        // [nch + 1] chunk slot ranges
+  uint32_t* msz = reinterpret_cast<uint32_t*>(co + g.nch + 1);            // [kGSelSub] members
+  uint32_t* soff = msz + kGSelSub;                                        // [kGSelSub + 1] stage offsets
+  uint32_t* cur = soff + kGSelSub + 1;                                    // [kGSelSub] placement cursors
+  uint32_t* wsum = cur + kGSelSub;                                        // [32]
+  uint32_t* kbuf_all = wsum + 32;                                         // [32][kMidMax]
+  uint32_t* hist_all = kbuf_all + (kGPlaceThreads / 32) * kMidMax;        // [32][16]
+  uint32_t* stage = hist_all + (kGPlaceThreads / 32) * 16;                // [stage_cap]
+  const uint32_t gsz = 1u << g.gshift;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* kbuf = kbuf_all + wib * kMidMax;
+  uint32_t* hist = hist_all + wib * 16;
+  const uint64_t ngroups = (uint64_t)W * g.ng;
+  for (uint64_t gid = blockIdx.x; gid < ngroups; gid += gridDim.x) {
+    const uint32_t j = (uint32_t)(gid / g.ng), gi = (uint32_t)(gid - (uint64_t)j * g.ng);
+    const uint32_t b0 = gi << g.gshift;
+    const uint32_t nbk = range - b0 < gsz ? range - b0 : gsz;
+    const uint64_t tb = (uint64_t)(t0 + j) * range + b0;
+    for (uint32_t c = threadIdx.x; c <= g.nch; c += blockDim.x) co[c] = goffs[gid * g.nch + c];
+    __syncthreads();
+    const uint64_t e0 = co[0], e1 = co[g.nch];
+    for (uint32_t s0 = 0; s0 < nbk; s0 += kGSelSub) {
+      const uint32_t ns = nbk - s0 < kGSelSub ? nbk - s0 : kGSelSub;
+      // members per bucket, and the stage offsets of the staged ones (a block scan)
+      uint32_t m = 0, sv = 0;
+      if (threadIdx.x < kGSelSub) {
+        if (threadIdx.x < ns) {
+          const uint64_t i = tb + s0 + threadIdx.x;
+          m = (uint32_t)(pool_off[i + 1] - pool_off[i]);
+        }
+        sv = m <= kMidMax ? m : 0u;
+        uint32_t x = sv;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) id[u] = lane + 32u * u < m ? pool[p0 + lane + 32u * u] : kEmpty;
-    uint32_t keep = m;
-    if (m > R) {
-      const uint32_t t = i / range, b = i - t * range;
-      const uint64_t tb = prio_bucket_key(keys, t, b);
-      uint32_t pr[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) pr[u] = lane + 32u * u < m ? prio_of(tb, id[u]) : 0xFFFFFFFFu;
-      // radix select over 4-bit digits, most significant first: a per-warp shared-memory
-      // histogram of the candidates still matching `prefix`; the R-th smallest priority lies
-      // in digit d of the current position, everything in the digits below d is kept
-      uint32_t* hist = hist_s[w];
-      uint32_t prefix = 0, need = R, ubound = 0;
-      bool done = false;
-      for (int sh = 28; sh >= 0 && !done; sh -= 4) {
-        const uint32_t hi_mask = sh == 28 ? 0u : ~((16u << sh) - 1u);
-        if (lane < 16) hist[lane] = 0;
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if ((lane + 32u * u < m) && (pr[u] & hi_mask) == prefix) atomicAdd(&hist[(pr[u] >> sh) & 15u], 1u);
-        __syncwarp();
-        const uint32_t hc = lane < 16 ? hist[lane] : 0u;
-        uint32_t x = hc;
-#pragma unroll
-        for (uint32_t o = 1; o < 16; o <<= 1) {
+        for (uint32_t o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(kFull, x, o);
           if (lane >= o) x += y;
         }
-        const uint32_t d = __ffs(__ballot_sync(kFull, lane < 16 && x >= need)) - 1;
-        const uint32_t below = __shfl_sync(kFull, x - hc, d), cd = __shfl_sync(kFull, hc, d);
-        need -= below;  // still needed inside digit d (1 <= need <= cd)
-        prefix |= d << sh;
-        if (need == cd) {
-          ubound = prefix + (1u << sh);  // keep every priority < ubound (0: 2^32)
-          done = true;
+        if (lane == 31) wsum[wib] = x;
+        msz[threadIdx.x] = m;
+        cur[threadIdx.x] = 0;
+        sv = x - sv;  // exclusive within the warp
+      }
+      __syncthreads();
+      if (threadIdx.x < kGSelSub) {
+        uint32_t before = 0;
+        for (uint32_t w = 0; w < wib; ++w) before += wsum[w];
+        soff[threadIdx.x] = before + sv;
+        if (threadIdx.x == kGSelSub - 1) soff[kGSelSub] = before + sv + (m <= kMidMax ? m : 0u);
+      }
+      __syncthreads();
+      const bool overflow = soff[kGSelSub] > stage_cap;
+      // place: each warp walks a contiguous range of 32-slot blocks of the group's entries
+      // (as k_gplace), 4 blocks' loads in flight per lane; entries of other sub-ranges skip
+      const uint64_t nblk = (e1 - e0 + 31) >> 5;
+      const uint64_t wb0 = nblk * wib / (kGPlaceThreads / 32), wb1 = nblk * (wib + 1) / (kGPlaceThreads / 32);
+      uint32_t c = 0;
+      if (wb0 < wb1) {
+        const uint64_t pb = e0 + (wb0 << 5);
+        uint32_t hi = g.nch;
+        while (hi - c > 1) {
+          const uint32_t mid = (c + hi) >> 1;
+          if (co[mid] <= pb) c = mid;
+          else hi = mid;
         }
-        __syncwarp();
       }
-      if (!done) {  // priorities tie at the threshold: exact CTA path
-        push_big(i, big_list, big_count);
-        continue;
-      }
-      // compact the kept ids (priority < ubound; ubound == 0 means 2^32) into shared memory
-      uint32_t base = 0;
+      // (positions relative to e0 in 32 bits: a group holds < 2^32 entries; the next chunk
+      // end is kept in a register, so a block costs one compare unless it crosses it)
+      const uint32_t* gent = ent + e0;
+      const uint32_t ge = (uint32_t)(e1 - e0);
+      uint32_t cend = (uint32_t)(co[c + 1] - e0);
+      for (uint32_t blk0 = (uint32_t)wb0; blk0 < (uint32_t)wb1; blk0 += 4) {
+        uint32_t ev[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool k_ = (lane + 32u * u < m) && (ubound == 0 || pr[u] < ubound);
-        const uint32_t bal = __ballot_sync(kFull, k_);
-        if (k_) kbuf[base + __popc(bal & lanemask_lt())] = id[u];
-        base += __popc(bal);
-      }
-      keep = R;
-    } else {
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t p = ((blk0 + u) << 5) + lane;
+          ev[u] = blk0 + u < (uint32_t)wb1 && p < ge ? gent[p] : 0xFFFFFFFFu;
+        }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (lane + 32u * u < m) kbuf[lane + 32u * u] = id[u];
+        for (int u = 0; u < 4; ++u) {
+          if (blk0 + u >= (uint32_t)wb1) break;
+          const uint32_t pb = (blk0 + u) << 5;
+          while (cend <= pb) cend = (uint32_t)(co[++c + 1] - e0);
+          const uint32_t p = pb + lane;
+          const uint32_t bl = (ev[u] >> kGChunkLog2) - s0;  // bucket within the sub-range
+          if (p < ge && bl < ns) {
+            uint32_t cl = c;
+            if (p >= cend) {  // (a block that straddles chunk ends)
+              ++cl;
+              while ((uint32_t)(co[cl + 1] - e0) <= p) ++cl;
+            }
+            const uint32_t id = id_base + (cl << kGChunkLog2) + (ev[u] & ((1u << kGChunkLog2) - 1));
+            const uint32_t slot = atomicAdd(&cur[bl], 1u);
+            if (!overflow && msz[bl] <= kMidMax) stage[soff[bl] + slot] = id;
+            else pool[pool_off[tb + s0 + bl] + slot] = id;
+          }
+        }
+      }
+      __syncthreads();
+      // select: warp per bucket
+      for (uint32_t b = wib; b < ns; b += kGPlaceThreads / 32) {
+        const uint64_t i = tb + s0 + b;
+        const uint32_t mb = msz[b];
+        if (mb == 0) continue;
+        if (overflow || mb > kMidMax) {  // in the pool: listed for the select kernels
+          if (lane == 0) {
+            if (mb > kWarpMax) {
+              if (!early_listed) big_list[atomicAdd(big_count, 1u)] = (uint32_t)i;  // else k_pool_sizes listed it
+            } else if (mb <= kMidMax) {
+              reg_list[atomicAdd(reg_count, 1u)] = (uint32_t)i;
+            } else {
+              mid_list[atomicAdd(mid_count, 1u)] = (uint32_t)i;
+            }
+          }
+          continue;
+        }
+        const uint32_t* src = stage + soff[b];
+        if (!select_mid_any((uint32_t)i, mb, 0, range, R, keys, src, ids_out + goff[i], kbuf, hist, lane)) {
+          const uint64_t po = pool_off[i];  // a priority tie: the exact CTA path reads the pool
+          for (uint32_t x = lane; x < mb; x += 32) pool[po + x] = src[x];
+          __syncwarp();
+          push_big((uint32_t)i, big_list, big_count);
+        }
+      }
+      __syncthreads();
     }
-    __syncwarp();
-    sort_store_upto<8>(kbuf, keep, out);  // kept ids ascending (R#10)
-    __syncwarp();
   }
 }
 
@@ -1195,6 +1398,13 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const bool grouped = tm && !a.goff_old && a.gslots && a.range <= (1u << 24) &&
                        (uint64_t)W * gg.ng * gg.nch <= (uint64_t)nb &&  // (the scan's temp storage is sized for nb)
                        !(gp_env && gp_env[0] == '0');
+  // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
+  // =2: and the CTA path skips its filter (exact radix select).  Tests only.
+  const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");
+  const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
+  // grouped placement fused with the select (k_gplace_sel; FLASH_BUILD_GSEL=0 disables, tests)
+  const char* gs_env = getenv("FLASH_BUILD_GSEL");
+  const bool gsel = grouped && a.R <= kMidMax && !force_big && !(gs_env && gs_env[0] == '0');
   uint32_t* pool = a.pool;  // the grouped passes leave the bucket-ordered pool in addrsT
   unsigned gplace_grid = 1;
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;
@@ -1222,7 +1432,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     const size_t psm = gplace_smem(gg.gshift, gg.nch);
     const uint64_t ngroups = (uint64_t)W * gg.ng;
     gplace_grid = (unsigned)((uint64_t)device_sms() < ngroups ? device_sms() : ngroups);  // one group per SM
-    if (a.after_scan) {  // count now, place after the scans, so the callback's work overlaps it
+    if (a.after_scan || gsel) {  // count now, place after the scans (the callback's work overlaps it)
       ensure_smem_attr((const void*)k_gplace<0>, psm);
       ensure_smem_attr((const void*)k_gplace<1>, psm);
       k_gplace<0><<<gplace_grid, kGPlaceThreads, psm, s>>>(W, a.t0, a.range, gg, goffs, a.pool, a.id_base, a.cursor,
@@ -1245,10 +1455,6 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
                                         a.err);
     launches++;
   }
-  // FLASH_DEBUG_FORCE_BIG=1: every bucket with > 32 members takes the CTA path;
-  // =2: and the CTA path skips its filter (exact radix select).  Tests only.
-  const char* fb = getenv("FLASH_DEBUG_FORCE_BIG");
-  const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
   // buckets with > kWarpMax members are listed here and selected on the side stream
   const bool early = a.early_list && a.side_stream && !force_big;
   uint32_t* early_count = a.big_count + 3;
@@ -1284,6 +1490,19 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     k_fill_smem<<<C, kSmemBuildThreads, (size_t)a.range * 4, s>>>(a.addrsT, a.n, a.t0, a.range, W, C, a.id_base,
                                                                  a.cursor, a.hbuf, a.pool_off, a.pool, prefixed);
     launches++;
+  } else if (gsel) {  // placement + bottom-R select of the small buckets, in one pass
+    const size_t fixed = gsel_fixed_smem(gg.nch);
+    const size_t gsm = 227 * 1024;
+    uint32_t stage_cap = (uint32_t)((gsm - fixed) / 4);
+    const char* cap_env = getenv("FLASH_BUILD_GSEL_CAP");  // tests: a smaller stage (sub-range overflow)
+    if (cap_env) stage_cap = std::min<uint32_t>(stage_cap, (uint32_t)strtoul(cap_env, nullptr, 10));
+    ensure_smem_attr((const void*)k_gplace_sel, gsm);
+    k_gplace_sel<<<gplace_grid, kGPlaceThreads, gsm, s>>>(W, a.t0, a.range, gg, a.gslots, a.pool, a.id_base, a.pool_off,
+                                                          a.addrsT, stage_cap, a.R, a.keys, a.goff_new, a.ids_new,
+                                                          early, a.cursor, a.big_count + 1,
+                                                          reinterpret_cast<uint32_t*>(a.pool_cnt), a.big_count + 2,
+                                                          a.big_list, a.big_count);
+    launches++;
   } else if (grouped) {
     if (a.after_scan) {  // (after the scans: the callback's work above overlaps the placement)
       const size_t psm = gplace_smem(gg.gshift, gg.nch);
@@ -1316,9 +1535,10 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   uint32_t* reg_count = a.big_count + 2;
   const uint64_t small_warps = ((uint64_t)nb + kSmallChunk - 1) / kSmallChunk;  // 32 buckets per warp step
   const unsigned small_blocks = (unsigned)((small_warps + 7) / 8 < (uint64_t)device_sms() * 64 ? (small_warps + 7) / 8 : (uint64_t)device_sms() * 64);
-  k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, early, a.pool_off, pool, a.goff_new,
-                                             a.ids_new, mid_list, mid_count, reg_list, reg_count, a.big_list,
-                                             a.big_count);
+  if (!gsel)  // (k_gplace_sel selected the small buckets and listed the rest)
+    k_select_small<<<small_blocks, 256, 0, s>>>(nb, a.range, a.R, a.keys, force_big, early, a.pool_off, pool,
+                                               a.goff_new, a.ids_new, mid_list, mid_count, reg_list, reg_count,
+                                               a.big_list, a.big_count);
   k_select_mid<<<device_sms() * 8, 256, 0, s>>>(a.range, a.R, a.keys, reg_list, reg_count, a.pool_off, pool, a.goff_new,
                                        a.ids_new, a.big_list, a.big_count);
   launches += 1;

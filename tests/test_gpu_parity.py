@@ -390,6 +390,37 @@ def test_table_major_build_over_several_row_chunks(monkeypatch, grouped):
         _check_tables(idx, T)
 
 
+@pytest.mark.parametrize("rng,R,cap", [(1 << 14, 64, None), (1 << 14, 64, "3000"), (1 << 13, 200, None),
+                                       (1 << 14, 16, None), (1 << 14, 64, "0")])
+def test_grouped_build_fused_select(monkeypatch, rng, R, cap):
+    """The grouped table-major passes with the fused placement + select (k_gplace_sel):
+    ~140 / ~280 members per bucket (the register select in shared memory; buckets over 256
+    listed for the warp select), heavy buckets from repeated rows (> 512: the CTA path), a
+    small stage (FLASH_BUILD_GSEL_CAP: sub-ranges that overflow go through the pool and the
+    select kernels), and FLASH_BUILD_GSEL=0 as the control; tables bit-exact vs the oracle."""
+    monkeypatch.setenv("FLASH_BUILD_TM", "1")
+    monkeypatch.setenv("FLASH_BUILD_SMEM", "0")
+    monkeypatch.setenv("FLASH_BUILD_GROUPED", "1")
+    if cap == "0":
+        monkeypatch.setenv("FLASH_BUILD_GSEL", "0")
+    elif cap is not None:
+        monkeypatch.setenv("FLASH_BUILD_GSEL_CAP", cap)
+    rp, col = shape_slice("kdd12", 2_300_000)
+    rows = [col[rp[i]:rp[i + 1]] for i in range(0, 3000)]
+    heavy = synth.csr_from_rows([rows[5]] * 1500 + rows)  # one row 1,500 times: a bucket per table
+    rp = np.concatenate([heavy[0], heavy[0][-1] + rp[1:]])
+    col = np.concatenate([heavy[1], col])
+    n = rp.size - 1
+    K, L, seed = 4, 3, 0x5EED0004
+    addrs = oracle.addresses(K, L, rng, seed, oracle.doph(K, L, seed, rp, col))
+    T = oracle.build(L, R, rng, seed, addrs, np.arange(n, dtype=np.uint32))
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, R, rng, seed) as idx:
+        idx.insert(d_rp, d_col, 0)
+        _check_tables(idx, T)
+        assert idx.errors() == 0
+
+
 def test_knn_graph_ids_beyond_the_bitmap_kernel():
     """800,000 rows: the ids no longer fit the bitmap kernel's shared-memory bitmap, so every
     query goes to the sort kernels — also in flash_knn_graph, whose size-class plan runs
