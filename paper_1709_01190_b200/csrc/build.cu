@@ -1404,7 +1404,11 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
   const int force_big = fb ? (fb[0] == '2' ? 2 : 1) : 0;
   // grouped placement fused with the select (k_gplace_sel; FLASH_BUILD_GSEL=0 disables, tests)
   const char* gs_env = getenv("FLASH_BUILD_GSEL");
-  const bool gsel = grouped && a.R <= kMidMax && !force_big && !(gs_env && gs_env[0] == '0');
+  // it pays where most buckets select (kdd12: ~143 arrivals per bucket, R = 64); where most
+  // keep every member (friendster: ~63 per bucket, R = 64) k_select_small's staged copies win
+  // (friendster build 97 vs 139 ms fused); FLASH_BUILD_GSEL=1 forces it (tests)
+  const bool gsel = grouped && a.R <= kMidMax && !force_big &&
+                    (gs_env ? gs_env[0] == '1' : a.n > (uint64_t)a.R * a.range);
   uint32_t* pool = a.pool;  // the grouped passes leave the bucket-ordered pool in addrsT
   unsigned gplace_grid = 1;
   const uint64_t chunks = (a.n + kTmRows - 1) / kTmRows;

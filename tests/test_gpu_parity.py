@@ -401,9 +401,8 @@ def test_grouped_build_fused_select(monkeypatch, rng, R, cap):
     monkeypatch.setenv("FLASH_BUILD_TM", "1")
     monkeypatch.setenv("FLASH_BUILD_SMEM", "0")
     monkeypatch.setenv("FLASH_BUILD_GROUPED", "1")
-    if cap == "0":
-        monkeypatch.setenv("FLASH_BUILD_GSEL", "0")
-    elif cap is not None:
+    monkeypatch.setenv("FLASH_BUILD_GSEL", "0" if cap == "0" else "1")
+    if cap not in (None, "0"):
         monkeypatch.setenv("FLASH_BUILD_GSEL_CAP", cap)
     rp, col = shape_slice("kdd12", 2_300_000)
     rows = [col[rp[i]:rp[i + 1]] for i in range(0, 3000)]
