@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
                                                    uint64_t n_rows, uint32_t K, uint32_t L,
                                                    uint32_t range, HashKeys keys,
                                                    uint32_t* __restrict__ codes, AddrOut out,
-                                                   int64_t skip_le) {
+                                                   int64_t skip_le, const uint32_t* __restrict__ long_rows,
+                                                   uint32_t long_cap) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31;
@@ -240,6 +241,14 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
 
   // one warp per row, the block scheduler balances skewed row lengths; rows with <= skip_le
   // nonzeros belong to k_doph_sparse (their extents are read here anyway)
+  const uint32_t nlong = long_rows ? long_rows[long_cap] : 0xFFFFFFFFu;
+  if (nlong <= long_cap) {  // the rows k_doph_sparse listed
+    for (uint32_t x = blockIdx.x * wpb + warp; x < nlong; x += gridDim.x * wpb) {
+      const uint64_t r = long_rows[x];
+      do_row(r, row_ptr[r], row_ptr[r + 1]);
+    }
+    return;
+  }
   for (uint64_t r = (uint64_t)blockIdx.x * wpb + warp; r < n_rows; r += (uint64_t)gridDim.x * wpb) {
     const int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
     if (e1 - e0 > skip_le) do_row(r, e0, e1);
@@ -277,7 +286,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
                                                           const uint32_t* __restrict__ col_idx,
                                                           uint64_t n_rows, uint32_t K, uint32_t L,
                                                           uint32_t range, HashKeys keys,
-                                                          uint32_t* __restrict__ codes, AddrOut out) {
+                                                          uint32_t* __restrict__ codes, AddrOut out,
+                                                          uint32_t* __restrict__ long_rows, uint32_t long_cap) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -304,6 +314,17 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
    const uint64_t rl = r0 + lane;
    const int64_t my_e0 = rl < n_rows ? row_ptr[rl] : 0, my_e1 = rl < n_rows ? row_ptr[rl + 1] : 0;
    uint32_t todo = __ballot_sync(0xFFFFFFFFu, rl < n_rows && my_e1 - my_e0 <= (int64_t)kSparseNnz);
+   if (long_rows) {  // list the others for k_doph (past long_cap they are counted only)
+     const bool lg = rl < n_rows && my_e1 - my_e0 > (int64_t)kSparseNnz;
+     const uint32_t lm = __ballot_sync(0xFFFFFFFFu, lg);
+     if (lm) {
+       uint32_t base = 0;
+       if (lane == 0) base = atomicAdd(&long_rows[long_cap], (uint32_t)__popc(lm));
+       base = __shfl_sync(0xFFFFFFFFu, base, 0);
+       const uint32_t x = base + __popc(lm & lanemask_lt_d());
+       if (lg && x < long_cap) long_rows[x] = (uint32_t)rl;
+     }
+   }
    while (todo) {  // the others are k_doph's
     const uint32_t src = __ffs(todo) - 1;
     todo &= todo - 1;
@@ -569,7 +590,7 @@ __global__ void __launch_bounds__(kMidThreads, 2) k_doph_mid(const int64_t* __re
 template <bool C, bool A>
 int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
              uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
-             cudaStream_t s) {
+             cudaStream_t s, uint32_t* long_rows, uint32_t long_cap) {
   const uint32_t B = K * L;
   int launched = 0;
   int64_t skip_le = -1;
@@ -582,11 +603,15 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     uint64_t blocks = (uint64_t)device_sms() * per_sm;
     const uint64_t need = (n_rows + kThreads - 1) / kThreads;  // 32 rows per warp-chunk
     if (blocks > need) blocks = need;
+    if (long_rows) cudaMemsetAsync(long_rows + long_cap, 0, sizeof(uint32_t), s);
     k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                                 codes, out);
+                                                                 codes, out, long_rows, long_cap);
     ++launched;
     skip_le = kSparseNnz;
-  } else if (B <= kMidMaxB) {  // rows with <= B/2 nonzeros: the inverted-chain kernel
+  } else {
+    long_rows = nullptr;  // (only the sparse kernel lists the rows it leaves)
+  }
+  if (B > kSparseMaxB && B <= kMidMaxB) {  // rows with <= B/2 nonzeros: the inverted-chain kernel
     // FLASH_DOPH_MID_LE (tests, tuning): the row-length cut, -1 = off; FLASH_DOPH_T1 (tests):
     // a shallower inverted depth T1 (more rows' bins take the probing path)
     const char* e = getenv("FLASH_DOPH_MID_LE");
@@ -635,7 +660,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return launched;
   k_doph<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                         codes, out, skip_le);
+                                                         codes, out, skip_le, long_rows, long_cap);
   return launched + 1;
 }
 
@@ -643,11 +668,13 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
 
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
-                cudaStream_t s) {
+                cudaStream_t s, uint32_t* long_rows, uint32_t long_cap) {
   const bool addrs = out.addrs || out.peers;
-  if (codes && addrs) return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
-  if (codes) return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
-  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s);
+  if (codes && addrs)
+    return launch_t<true, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s, long_rows, long_cap);
+  if (codes)
+    return launch_t<true, false>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s, long_rows, long_cap);
+  return launch_t<false, true>(row_ptr, col_idx, n_rows, K, L, range, keys, codes, out, s, long_rows, long_cap);
 }
 
 }  // namespace flash

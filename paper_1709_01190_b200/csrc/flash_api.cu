@@ -184,7 +184,7 @@ void free_handle(flash_index* h) {
   cudaFree(h->err);
   for (DevBuf* b : {&h->goff[0], &h->goff[1], &h->ids[0], &h->ids[1], &h->addrs, &h->cursor, &h->pool_cnt,
                     &h->pool_off, &h->keep_cnt, &h->pool, &h->big_list, &h->scan_tmp, &h->qscratch, &h->off_tmp,
-                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->raddr, &h->qraddr, &h->hbuf, &h->gslots, &h->h_rp, &h->h_col,
+                    &h->seg_off, &h->xscan_tmp, &h->addrsT, &h->raddr, &h->qraddr, &h->hbuf, &h->gslots, &h->long_rows, &h->h_rp, &h->h_col,
                     &h->h_ids, &h->h_cnt, &h->zero})
     release(*b);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
@@ -194,8 +194,19 @@ void free_handle(flash_index* h) {
 flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n,
                      uint32_t* codes, const AddrOut& out, cudaStream_t s) {
   Phase ph(h, 0, s);
-  const_cast<flash_index*>(h)->launches += launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes,
-                                                       out, s);
+  // the rows k_doph_sparse leaves to k_doph are listed (up to kLongCap; more: k_doph scans
+  // every row's extent) when K*L <= 256, so that k_doph does not read all n extents
+  flash_index* hm = const_cast<flash_index*>(h);
+  uint32_t* long_rows = nullptr;
+  uint32_t long_cap = 0;
+  if ((uint64_t)h->K * h->L <= 256 && n > 0) {
+    constexpr uint64_t kLongCap = 1u << 22;
+    long_cap = (uint32_t)(n < kLongCap ? n : kLongCap);
+    TRY(ensure(hm->long_rows, sizeof(uint32_t) * ((size_t)long_cap + 1)));
+    long_rows = hm->long_rows.as<uint32_t>();
+  }
+  hm->launches += launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, out, s, long_rows,
+                              long_cap);
   CUDA_TRY(cudaGetLastError());
   return FLASH_OK;
 }

@@ -100,9 +100,12 @@ inline AddrOut addr_out(uint32_t* addrs, uint32_t world = 1) { return AddrOut{ad
 
 // H1-H3: DOPH bin minima, densification, addresses.  codes may be null; addresses are
 // written when out.addrs or out.peers is set.
+// long_rows (optional, [long_cap + 1] u32 scratch): when the sparse kernel runs, it lists the
+// rows it leaves to k_doph there (the last word counts them), so k_doph need not scan every
+// row's extent; a count above long_cap makes k_doph scan as without the list.
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
-                cudaStream_t s);
+                cudaStream_t s, uint32_t* long_rows = nullptr, uint32_t long_cap = 0);
 
 // Reservoir sharing (R#23): addrs [n][L] -> reservoir indices [n][L]: entry (r, t) is
 // shared_reservoir(t, addrs[r][t]) unless the address is EMPTY/invalid or an earlier table of

@@ -78,6 +78,7 @@ struct flash_index {
   flash::api::DevBuf raddr, qraddr;       // shared mode: rows' / queries' distinct reservoir indices
   flash::api::DevBuf hbuf;                // build: slice histograms of the shared-memory passes
   flash::api::DevBuf gslots;              // build: group slot offsets of the grouped table-major passes
+  flash::api::DevBuf long_rows;           // hash: [cap] rows k_doph_sparse leaves to k_doph, + counter
   flash::api::DevBuf h_rp, h_col, h_ids, h_cnt;  // flash_knn_graph_host staging
   flash::api::DevBuf zero;                // 16 zero bytes (a valid device pointer for empty inputs)
   unsigned long long* err = nullptr;

@@ -28,6 +28,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="url")
 ap.add_argument("--build", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--extra", nargs="*", default=[], help="libflash_v_NAME.so builds of tools/variants_graph.py")
 args = ap.parse_args()
 if args.build:
     for name, defs in VARIANTS.items():
@@ -39,10 +40,11 @@ h_rp, h_col, nnz = bench.gen_local(shape, [0, shape.N], 0)
 d_rp, d_col = h_rp.cuda(), h_col.cuda()
 out = torch.empty((shape.N, L), dtype=torch.int32, device="cuda")
 ref = None
-for name in VARIANTS:
+for name in list(VARIANTS) + args.extra:
     flash._lib = None
     flash.load_library(flash.LIB_PATH if name == "base" else
-                       os.path.join(ROOT, "paper_1709_01190_b200", f"libflash_d_{name}.so"))
+                       os.path.join(ROOT, "paper_1709_01190_b200",
+                                    f"libflash_v_{name}.so" if name in args.extra else f"libflash_d_{name}.so"))
     h = flash.flash_create(K, L, 32, rng, seed)
     ts = []
     for r in range(args.reps + 1):
