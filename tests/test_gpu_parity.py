@@ -80,6 +80,24 @@ def test_hash_codes_and_addresses_bit_exact(name, make, K, L, rng):
         assert np.array_equal(flash.as_u32(a2), o_addrs)
 
 
+@pytest.mark.parametrize("cap", ["3", "100000"])
+def test_hash_long_row_list_and_its_overflow(monkeypatch, cap):
+    """K*L <= 256: k_doph_sparse lists the rows over 32 nonzeros for k_doph; with a list cap
+    below their number (3) k_doph falls back to scanning every row's extent."""
+    monkeypatch.setenv("FLASH_DOPH_LONGCAP", cap)
+    rp, col = shape_slice("url", 3000)  # ~116 nnz per row, a few rows <= 32
+    rows = [col[rp[i]:rp[i + 1]] for i in range(rp.size - 1)]
+    rows = [r[:20] if i % 3 else r for i, r in enumerate(rows)]  # two thirds short
+    rp, col = synth.csr_from_rows(rows)
+    K, L, seed = 4, 32, 0x5EED0104
+    d_rp, d_col = flash.to_device_csr(rp, col)
+    with flash.FlashIndex(K, L, 8, 1 << 15, seed) as idx:
+        codes, addrs = idx.hash(d_rp, d_col)
+        o_codes = oracle.doph(K, L, seed, rp, col)
+        assert np.array_equal(flash.as_u32(codes), o_codes)
+        assert np.array_equal(flash.as_u32(addrs), oracle.addresses(K, L, 1 << 15, seed, o_codes))
+
+
 @pytest.mark.parametrize("T1,mid_le", [("1", None), ("8", None), ("31", None), (None, "-1"), (None, "40")])
 def test_hash_inverted_chain_kernel_settings(monkeypatch, T1, mid_le):
     """k_doph_mid under other inverted-chain depths T1 (T1 = 1 sends most empty bins to the
