@@ -265,40 +265,42 @@ __global__ void __launch_bounds__(kGThreads) k_gcount(const uint32_t* __restrict
 
 // (tiles of kGTile rows are counting-sorted by group in shared memory first, so each
 // warp store writes runs of one group's consecutive slots)
+// (8 K-row tiles in 512-thread CTAs, two per SM, measured slower: kdd12 insert 204.7 vs
+// 189.4 ms)
 constexpr uint32_t kGTile = 16384;
+constexpr int kGSThreads = kGThreads;
+constexpr int kGSMinBlocks = 1;
 
 __host__ __device__ inline size_t gscatter_smem(uint32_t ng) {
-  return (size_t)ng * (8 + 4 + 4 + 4) + (size_t)kGTile * (4 + 2);
+  return (size_t)ng * (8 + 4 + 4) + (size_t)kGTile * (4 + 2);
 }
 
-__global__ void __launch_bounds__(kGThreads, 1) k_gscatter(const uint32_t* __restrict__ addrsT, uint64_t n,
+__global__ void __launch_bounds__(kGSThreads, kGSMinBlocks) k_gscatter(const uint32_t* __restrict__ addrsT, uint64_t n,
                                                            uint32_t range, GroupGeom g,
                                                            const uint64_t* __restrict__ goffs, uint32_t* __restrict__ ent) {
-  extern __shared__ uint64_t gbase[];                              // [ng] slot bases of this chunk
-  uint32_t* gcur = reinterpret_cast<uint32_t*>(gbase + g.ng);       // [ng] slots used so far
-  uint32_t* tcnt = gcur + g.ng;                                     // [ng] this tile's counts
+  // [ng] each group's next slot in this chunk; during a tile's write-out, minus the group's
+  // start in the tile's staging order (so an entry's slot is gbase[gi] + its stage index)
+  extern __shared__ uint64_t gbase[];
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(gbase + g.ng);       // [ng] this tile's counts
   uint32_t* toff = tcnt + g.ng;                                     // [ng] this tile's group starts
   uint32_t* stage = toff + g.ng;                                    // [kGTile] entries, by group
   uint16_t* sgrp = reinterpret_cast<uint16_t*>(stage + kGTile);     // [kGTile] their groups
-  __shared__ uint32_t wsum[kGThreads / 32];
-  constexpr uint32_t E = kGTile / kGThreads;
+  __shared__ uint32_t wsum[kGSThreads / 32];
+  constexpr uint32_t E = kGTile / kGSThreads;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t j = blockIdx.x / g.nch, c = blockIdx.x - j * g.nch;
-  for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) {
-    gbase[i] = goffs[((uint64_t)j * g.ng + i) * g.nch + c];
-    gcur[i] = 0;
-  }
+  for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) gbase[i] = goffs[((uint64_t)j * g.ng + i) * g.nch + c];
   const uint64_t r0 = (uint64_t)c << kGChunkLog2;
   const uint64_t r1 = n - r0 < (1ull << kGChunkLog2) ? n : r0 + (1ull << kGChunkLog2);
   const uint32_t* col = addrsT + (uint64_t)j * n;
   const uint32_t gmask = (1u << g.gshift) - 1;
-  const uint32_t gpt = (g.ng + kGThreads - 1) / kGThreads;  // groups per thread in the scan
+  const uint32_t gpt = (g.ng + kGSThreads - 1) / kGSThreads;  // groups per thread in the scan
   for (uint64_t t0 = r0; t0 < r1; t0 += kGTile) {
     for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) tcnt[i] = 0;
     uint32_t a[E], rk[E];
 #pragma unroll
     for (uint32_t u = 0; u < E; ++u) {
-      const uint64_t r = t0 + u * kGThreads + threadIdx.x;
+      const uint64_t r = t0 + u * kGSThreads + threadIdx.x;
       a[u] = r < r1 ? col[r] : kEmpty;
     }
     __syncthreads();
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gscatter(const uint32_t* __res
       const uint32_t gi = threadIdx.x * gpt + q;
       if (gi < g.ng) {
         toff[gi] = pos;
+        gbase[gi] -= pos;
         pos += tcnt[gi];
       }
     }
@@ -334,16 +337,13 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gscatter(const uint32_t* __res
       if (a[u] < range) {
         const uint32_t gi = a[u] >> g.gshift;
         const uint32_t s = toff[gi] + rk[u];
-        stage[s] = ((a[u] & gmask) << kGChunkLog2) | (uint32_t)(t0 + u * kGThreads + threadIdx.x - r0);
+        stage[s] = ((a[u] & gmask) << kGChunkLog2) | (uint32_t)(t0 + u * kGSThreads + threadIdx.x - r0);
         sgrp[s] = (uint16_t)gi;
       }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < tot; i += blockDim.x) {
-      const uint32_t gi = sgrp[i];
-      ent[gbase[gi] + gcur[gi] + (i - toff[gi])] = stage[i];
-    }
+    for (uint32_t i = threadIdx.x; i < tot; i += blockDim.x) ent[gbase[sgrp[i]] + i] = stage[i];
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) gcur[i] += tcnt[i];
+    for (uint32_t i = threadIdx.x; i < g.ng; i += blockDim.x) gbase[i] += toff[i] + tcnt[i];
   }
 }
 
@@ -1432,7 +1432,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     cudaMemsetAsync(ghist + nslots, 0, sizeof(uint64_t), s);
     size_t tmp = a.scan_tmp_bytes;
     cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, ghist, goffs, (int64_t)nslots + 1, s);
-    k_gscatter<<<W * gg.nch, kGThreads, gscatter_smem(gg.ng), s>>>(a.addrsT, a.n, a.range, gg, goffs, a.pool);
+    k_gscatter<<<W * gg.nch, kGSThreads, gscatter_smem(gg.ng), s>>>(a.addrsT, a.n, a.range, gg, goffs, a.pool);
     const size_t psm = gplace_smem(gg.gshift, gg.nch);
     const uint64_t ngroups = (uint64_t)W * gg.ng;
     gplace_grid = (unsigned)((uint64_t)device_sms() < ngroups ? device_sms() : ngroups);  // one group per SM
