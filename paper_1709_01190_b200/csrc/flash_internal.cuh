@@ -100,9 +100,10 @@ inline AddrOut addr_out(uint32_t* addrs, uint32_t world = 1) { return AddrOut{ad
 
 // H1-H3: DOPH bin minima, densification, addresses.  codes may be null; addresses are
 // written when out.addrs or out.peers is set.
-// long_rows (optional, [long_cap + 1] u32 scratch): when the sparse kernel runs, it lists the
-// rows it leaves to k_doph there (the last word counts them), so k_doph need not scan every
-// row's extent; a count above long_cap makes k_doph scan as without the list.
+// long_rows (optional, [long_cap + 2] u32 scratch): when the sparse kernel runs, it lists the
+// rows it leaves to k_doph there (the longest from the front, the rest from the back; the
+// last two words count them), so k_doph need not scan every row's extent and starts with
+// the longest rows; counts above long_cap make k_doph scan as without the list.
 int launch_doph(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, uint32_t K,
                 uint32_t L, uint32_t range, const HashKeys& keys, uint32_t* codes, const AddrOut& out,
                 cudaStream_t s, uint32_t* long_rows = nullptr, uint32_t long_cap = 0);
