@@ -16,6 +16,7 @@ from paper_1709_01190_b200 import flash  # noqa: E402
 CFG = {"webspam": (4, 50, 128, 1 << 15, 0x5EED0002, 128),
        "url": (4, 128, 32, 1 << 15, 0x5EED0003, 128),
        "kdd12": (4, 32, 64, 1 << 20, 0x5EED0004, 128),
+       "friendster": (4, 32, 64, 1 << 20, 0x5EED0005, 20),
        "tiny": (4, 16, 32, 1 << 15, 0x5EED0001, 10)}
 
 ap = argparse.ArgumentParser()
