@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph(const int64_t* __restrict_
 // One warp per row; persistent CTAs (the table is built once per CTA).
 constexpr uint32_t kSparseNnz = 32;
 // listed rows longer than this go first to k_doph (webspam, A/B in one process: hash 1.178 ->
-// 1.100 ms, graph 4.445 -> 4.368 ms; 2,048 and 8,192 the same within noise)
+// 1.100 ms, graph 4.445 -> 4.368 ms; 2,048 and 8,192 the same within noise; a third class
+// (rows over 1,024 next) 1.095 ms, not kept)
 constexpr int64_t kHugeNnz = 4096;
 constexpr uint32_t kSparseMaxB = 256;
 
