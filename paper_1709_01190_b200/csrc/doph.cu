@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(kMidThreads, 2) k_doph_mid(const int64_t* __re
                                                           uint64_t n_rows, uint32_t K, uint32_t L,
                                                           uint32_t range, HashKeys keys,
                                                           uint32_t* __restrict__ codes, AddrOut out,
-                                                          uint32_t T1, uint32_t C, int64_t mid_le) {
+                                                          uint32_t T1, uint32_t C, int64_t mid_le,
+                                                          unsigned long long* __restrict__ next_chunk) {
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t B = K * L, Bp = mid_pad(B), nc = Bp >> 7;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -486,8 +487,16 @@ __global__ void __launch_bounds__(kMidThreads, 2) k_doph_mid(const int64_t* __re
   for (uint32_t x = lane; x < (Bp + 4) / 4; x += 32) best4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
   __syncwarp();
 
+  // 32-row chunks handed out dynamically (a global counter; with next_chunk null, statically):
+  // warps whose chunks held longer rows take fewer, so no warp's share forms a tail
   const uint64_t nw = (uint64_t)gridDim.x * wpb;
-  for (uint64_t r0 = ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 += nw * 32) {
+  auto grab = [&](uint64_t cur) -> uint64_t {
+    if (!next_chunk) return cur + nw * 32;
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(next_chunk, 32ull);
+    return __shfl_sync(0xFFFFFFFFu, c, 0);
+  };
+  for (uint64_t r0 = next_chunk ? grab(0) : ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 = grab(r0)) {
     const uint64_t rl = r0 + lane;
     const int64_t my_e0 = rl < n_rows ? row_ptr[rl] : 0, my_e1 = rl < n_rows ? row_ptr[rl + 1] : 0;
     uint32_t todo = __ballot_sync(0xFFFFFFFFu, rl < n_rows && my_e1 - my_e0 <= mid_le);
@@ -613,6 +622,7 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
   const uint32_t B = K * L;
   int launched = 0;
   int64_t skip_le = -1;
+  unsigned long long* chunk_ctr = nullptr;
   if (B <= kSparseMaxB) {  // rows with <= kSparseNnz nonzeros: the table-driven kernel
     const size_t smem = ((size_t)sparse_table_words(B) + (size_t)sparse_warp_words(B) * (kThreads / 32)) * 4;
     ensure_smem_attr((const void*)k_doph_sparse<C, A>, 100 * 1024, true);
@@ -628,7 +638,10 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     ++launched;
     skip_le = kSparseNnz;
   } else {
-    long_rows = nullptr;  // (only the sparse kernel lists the rows it leaves)
+    // (only the sparse kernel lists the rows it leaves; the mid kernel takes the scratch's
+    // first 8 bytes as its chunk counter)
+    if (long_rows) chunk_ctr = reinterpret_cast<unsigned long long*>(long_rows);
+    long_rows = nullptr;
   }
   if (B > kSparseMaxB && B <= kMidMaxB) {  // rows with <= B/2 nonzeros: the inverted-chain kernel
     // FLASH_DOPH_MID_LE (tests, tuning): the row-length cut, -1 = off; FLASH_DOPH_T1 (tests):
@@ -656,8 +669,10 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
           const uint64_t need = (n_rows + wpb * 32 - 1) / (wpb * 32);  // 32 rows per warp-chunk
           if (blocks > need) blocks = need;
           if (blocks) {
+            unsigned long long* nc = chunk_ctr;
+            if (nc) cudaMemsetAsync(nc, 0, sizeof(unsigned long long), s);
             k_doph_mid<C, A><<<(unsigned)blocks, wpb * 32, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range,
-                                                                      keys, codes, out, T1, mc, mid_le);
+                                                                      keys, codes, out, T1, mc, mid_le, nc);
             ++launched;
           }
           skip_le = mid_le;

@@ -199,7 +199,10 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
   flash_index* hm = const_cast<flash_index*>(h);
   uint32_t* long_rows = nullptr;
   uint32_t long_cap = 0;
-  if ((uint64_t)h->K * h->L <= 256 && n > 0) {
+  if ((uint64_t)h->K * h->L > 256 && n > 0) {  // the mid kernel's chunk counter (8 B)
+    TRY(ensure(hm->long_rows, 8));
+    long_rows = hm->long_rows.as<uint32_t>();
+  } else if ((uint64_t)h->K * h->L <= 256 && n > 0) {
     const char* ce = getenv("FLASH_DOPH_LONGCAP");  // tests: a small cap (the full-scan fallback)
     const uint64_t kLongCap = ce ? strtoull(ce, nullptr, 10) : (1ull << 25);
     long_cap = (uint32_t)(n < kLongCap ? n : kLongCap);
