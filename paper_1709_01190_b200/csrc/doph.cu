@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
                                                           uint64_t n_rows, uint32_t K, uint32_t L,
                                                           uint32_t range, HashKeys keys,
                                                           uint32_t* __restrict__ codes, AddrOut out,
-                                                          uint32_t* __restrict__ long_rows, uint32_t long_cap) {
+                                                          uint32_t* __restrict__ long_rows, uint32_t long_cap,
+                                                          unsigned long long* __restrict__ next_chunk) {
   extern __shared__ uint32_t smem[];
   const uint32_t B = K * L;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -316,8 +317,15 @@ __global__ void __launch_bounds__(kThreads, 8) k_doph_sparse(const int64_t* __re
   __syncthreads();
 
   const uint64_t nw = (uint64_t)gridDim.x * wpb;
-  // chunks of 32 rows per warp: one coalesced read of their extents, then the sparse ones
-  for (uint64_t r0 = ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 += nw * 32) {
+  // chunks of 32 rows per warp (handed out by a global counter when next_chunk is set): one
+  // coalesced read of their extents, then the sparse ones
+  auto grab = [&](uint64_t cur) -> uint64_t {
+    if (!next_chunk) return cur + nw * 32;
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(next_chunk, 32ull);
+    return __shfl_sync(0xFFFFFFFFu, c, 0);
+  };
+  for (uint64_t r0 = next_chunk ? grab(0) : ((uint64_t)blockIdx.x * wpb + warp) * 32; r0 < n_rows; r0 = grab(r0)) {
    const uint64_t rl = r0 + lane;
    const int64_t my_e0 = rl < n_rows ? row_ptr[rl] : 0, my_e1 = rl < n_rows ? row_ptr[rl + 1] : 0;
    uint32_t todo = __ballot_sync(0xFFFFFFFFu, rl < n_rows && my_e1 - my_e0 <= (int64_t)kSparseNnz);
@@ -632,9 +640,12 @@ int launch_t(const int64_t* row_ptr, const uint32_t* col_idx, uint64_t n_rows, u
     uint64_t blocks = (uint64_t)device_sms() * per_sm;
     const uint64_t need = (n_rows + kThreads - 1) / kThreads;  // 32 rows per warp-chunk
     if (blocks > need) blocks = need;
-    if (long_rows) cudaMemsetAsync(long_rows + long_cap, 0, 2 * sizeof(uint32_t), s);
+    // (the scratch: the list, its two counts, then an 8-byte chunk counter)
+    unsigned long long* nc =
+        long_rows ? reinterpret_cast<unsigned long long*>(long_rows + ((long_cap + 3) & ~1u)) : nullptr;
+    if (long_rows) cudaMemsetAsync(long_rows + long_cap, 0, ((long_cap + 3) & ~1u) * 4 + 8 - long_cap * 4, s);
     k_doph_sparse<C, A><<<(unsigned)blocks, kThreads, smem, s>>>(row_ptr, col_idx, n_rows, K, L, range, keys,
-                                                                 codes, out, long_rows, long_cap);
+                                                                 codes, out, long_rows, long_cap, nc);
     ++launched;
     skip_le = kSparseNnz;
   } else {

@@ -206,7 +206,7 @@ flash_status do_hash(const flash_index* h, const int64_t* row_ptr, const uint32_
     const char* ce = getenv("FLASH_DOPH_LONGCAP");  // tests: a small cap (the full-scan fallback)
     const uint64_t kLongCap = ce ? strtoull(ce, nullptr, 10) : (1ull << 25);
     long_cap = (uint32_t)(n < kLongCap ? n : kLongCap);
-    TRY(ensure(hm->long_rows, sizeof(uint32_t) * ((size_t)long_cap + 2)));
+    TRY(ensure(hm->long_rows, sizeof(uint32_t) * (((size_t)long_cap + 3) & ~(size_t)1) + 8));
     long_rows = hm->long_rows.as<uint32_t>();
   }
   hm->launches += launch_doph(row_ptr, col_idx, n, h->K, h->L, h->range, h->keys, codes, out, s, long_rows,
