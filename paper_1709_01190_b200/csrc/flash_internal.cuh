@@ -206,7 +206,7 @@ int launch_query_mark(const QueryArgs& a, const uint32_t* list, const uint32_t* 
 int launch_csort(const QueryArgs& a, uint32_t cap, const uint32_t* list, const uint32_t* count, cudaStream_t s);
 // radix-partition warp-per-query kernel for queries with M <= mcap candidates (k <= 256)
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
-                      cudaStream_t s);
+                      cudaStream_t s, uint32_t* next = nullptr);
 
 // Candidate exchange, sender side (exchange.cu).  addrs: [n][t1-t0] (a table window's
 // columns).  sizes[q] = sum of the window buckets' sizes; off = exclusive scan (n+1).

@@ -959,7 +959,8 @@ bool query_shape_fits(uint32_t L, uint32_t R, uint32_t k) {
   return csort_smem_bytes(cap, L, L, k) <= 227 * 1024;
 }
 
-// lists [kLists][nq], counts [kLists], then the bitmap kernel's fallback list [nq] + count
+// lists [kLists][nq], counts [kLists], then the bitmap kernel's fallback list [nq] + count,
+// then the sort classes' query counter
 size_t query_scratch_bytes(uint64_t nq) { return sizeof(uint32_t) * (nq * (kLists + 1) + kLists + 4); }
 
 int launch_query_plan(const QueryArgs& a, void* scratch, cudaStream_t s) {
@@ -992,6 +993,8 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
   // FLASH_QUERY_CSORT=1 (tests): every class runs the CTA sort kernel
   const char* cs_env = getenv("FLASH_QUERY_CSORT");
   const bool all_csort = cs_env && cs_env[0] == '1';
+  // (a spare scratch word after the fallback list: the sort classes' query counter)
+  uint32_t* next_q = lists + (uint64_t)(kLists + 1) * a.nq + kLists + 1;
   int n = planned;
   for (int c = 0; c < kClasses && max_m; ++c) {
     if (c > 0 && class_max(c - 1) >= max_m) break;  // no query can be this large
@@ -1002,7 +1005,7 @@ int launch_query(const QueryArgs& a, void* scratch, cudaStream_t s) {
     // kernel, 8 warps on each query, finishes sooner: url 10 K queries 1.24 vs 1.31 ms)
     if (all_csort || c == kClasses - 1) r = launch_csort(a, cap, lc, counts + c, s);
     else if (c == kSortClasses - 1 && a.nq < few) r = launch_class<13, 256>(a, lc, counts + c, hist_len, s);
-    else if (c < kSortClasses) r = launch_query_sort(a, class_max(c), lc, counts + c, s);
+    else if (c < kSortClasses) r = launch_query_sort(a, class_max(c), lc, counts + c, s, next_q);
     else r = launch_class<14, 256>(a, lc, counts + c, hist_len, s);
     if (r == 0) r = launch_csort(a, cap, lc, counts + c, s);  // a warp class that does not fit
     if (r < 0) return -1;

@@ -101,7 +101,8 @@ __host__ __device__ inline size_t sort_slice_bytes(uint32_t mcap, uint32_t kBins
 
 template <int MCAP, int BINS_LOG2, int NW>
 __global__ void __launch_bounds__(32 * NW) k_query_sort(QueryArgs a, const uint32_t* __restrict__ qlist,
-                                                   const uint32_t* __restrict__ qcount, uint32_t shift) {
+                                                   const uint32_t* __restrict__ qcount, uint32_t shift,
+                                                   uint32_t* __restrict__ next) {
   constexpr uint32_t NBW = MCAP / 32 + 2;
   constexpr uint32_t kBins = 1u << BINS_LOG2;
   extern __shared__ __align__(16) uint8_t sms[];
@@ -127,7 +128,15 @@ __global__ void __launch_bounds__(32 * NW) k_query_sort(QueryArgs a, const uint3
 
   const uint32_t nq = *qcount;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t it = gw; it < nq; it += nw) {
+  // queries handed out by a global counter (next; null: statically), so warps that drew
+  // larger queries take fewer and none forms a tail
+  auto grab = [&](uint32_t cur) -> uint32_t {
+    if (!next) return cur + nw;
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(next, 1u);
+    return __shfl_sync(0xFFFFFFFFu, c, 0);
+  };
+  for (uint32_t it = next ? grab(0) : gw; it < nq; it = grab(it)) {
 #ifdef FLASH_QPROF
     long long qp_last = clock64();
 #endif
@@ -478,7 +487,7 @@ __global__ void __launch_bounds__(32 * NW) k_query_sort(QueryArgs a, const uint3
 
 // NW warps per CTA (one query each).
 template <int MCAP, int BL, int NW>
-int launch_sort_nw(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+int launch_sort_nw(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t* next, cudaStream_t s) {
   // digit = the top BL bits of the id range [0, max_id]
   const uint32_t bits = a.max_id ? 32u - (uint32_t)__builtin_clz(a.max_id) : 1u;
   const uint32_t shift = bits > (uint32_t)BL ? bits - BL : 0u;
@@ -493,7 +502,8 @@ int launch_sort_nw(const QueryArgs& a, const uint32_t* list, const uint32_t* cou
   uint64_t grid = (uint64_t)device_sms() * per_sm;
   const uint64_t need = (a.nq + NW - 1) / NW;
   if (grid > need) grid = need;
-  k_query_sort<MCAP, BL, NW><<<(unsigned)grid, 32 * NW, smem, s>>>(a, list, count, shift);
+  if (next) cudaMemsetAsync(next, 0, sizeof(uint32_t), s);
+  k_query_sort<MCAP, BL, NW><<<(unsigned)grid, 32 * NW, smem, s>>>(a, list, count, shift, next);
   return 1;
 }
 
@@ -511,7 +521,7 @@ int resident_warps(const QueryArgs& a) {
 // size depends on L: e.g. MCAP 4096 at L = 128 is 22.5 KB per warp — 2 CTAs of 4 = 8
 // warps per SM, 2 CTAs of 5 = 10).  Cached per (class, L, cmax).
 template <int MCAP, int BL>
-int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, cudaStream_t s) {
+int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* count, uint32_t* next, cudaStream_t s) {
   static thread_local uint64_t key = ~0ull;
   static thread_local bool five = false;
   const uint64_t k2 = ((uint64_t)a.L << 32) | a.cmax;
@@ -519,25 +529,25 @@ int launch_sort_t(const QueryArgs& a, const uint32_t* list, const uint32_t* coun
     five = resident_warps<MCAP, BL, 5>(a) > resident_warps<MCAP, BL, 4>(a);
     key = k2;
   }
-  return five ? launch_sort_nw<MCAP, BL, 5>(a, list, count, s) : launch_sort_nw<MCAP, BL, 4>(a, list, count, s);
+  return five ? launch_sort_nw<MCAP, BL, 5>(a, list, count, next, s) : launch_sort_nw<MCAP, BL, 4>(a, list, count, next, s);
 }
 
 }  // namespace
 
 int launch_query_sort(const QueryArgs& a, uint32_t mcap, const uint32_t* list, const uint32_t* count,
-                      cudaStream_t s) {
-  if (mcap <= 768) return launch_sort_t<768, 10>(a, list, count, s);
-  if (mcap <= 1024) return launch_sort_t<1024, 10>(a, list, count, s);
-  if (mcap <= 1280) return launch_sort_t<1280, 10>(a, list, count, s);
-  if (mcap <= 1536) return launch_sort_t<1536, 10>(a, list, count, s);
+                      cudaStream_t s, uint32_t* next) {
+  if (mcap <= 768) return launch_sort_t<768, 10>(a, list, count, next, s);
+  if (mcap <= 1024) return launch_sort_t<1024, 10>(a, list, count, next, s);
+  if (mcap <= 1280) return launch_sort_t<1280, 10>(a, list, count, next, s);
+  if (mcap <= 1536) return launch_sort_t<1536, 10>(a, list, count, next, s);
   // the 2048 class: 1024 bins (u16 run list, 10.8 instead of 12.9 KB per warp at L = 32)
   // when it is the top class — L*R <= 2048, saturated buckets put most queries there
   // (friendster graph query 1494 -> 1358 ms) — else 2048 bins (fewer inversions; webspam)
   if (mcap <= 2048)
-    return a.mmax <= 2048 ? launch_sort_t<2048, 10>(a, list, count, s)
-                                              : launch_sort_t<2048, 11>(a, list, count, s);
-  if (mcap <= 3072) return launch_sort_t<3072, 11>(a, list, count, s);
-  return launch_sort_t<4096, 11>(a, list, count, s);
+    return a.mmax <= 2048 ? launch_sort_t<2048, 10>(a, list, count, next, s)
+                                              : launch_sort_t<2048, 11>(a, list, count, next, s);
+  if (mcap <= 3072) return launch_sort_t<3072, 11>(a, list, count, next, s);
+  return launch_sort_t<4096, 11>(a, list, count, next, s);
 }
 
 }  // namespace flash
